@@ -1,0 +1,443 @@
+#!/usr/bin/env python
+"""Benchmark: orbit-steps/s of stochastic Kuramoto Euler-Maruyama on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload cfg2] [--coupling meanfield|pairwise]
+
+One "step" = one complete run of the workload (all orbits x all SDE steps)
+through the fused kernel.  Default workload = BASELINE.json configs[1]
+(cfg2): n=16, 65,536 orbits over a 256 K x 256 sigma grid, sfc64 streams,
+dt=1e-3, 10^4 steps, final state only.  Multi-GPU (torchrun): each rank
+integrates its own 65,536-orbit shard with global orbit ids
+[rank*M, (rank+1)*M) -- weak scaling, no data-path collective (the path is
+embarrassingly parallel); timing is max over ranks.
+
+  value    device-resident inputs (sdb_run_device), CUDA events around each
+           kernel launch, L2 flushed (512 MiB memset) between timed steps
+           outside the event pairs.
+  e2e      the public API run_batch() with numpy host buffers: H2D of
+           init/params and D2H of the store inside every timed step.
+  roofline FP64 pipe: algorithmic FP64 lane-ops of the kernel's algorithm
+            / kernel time, against the FP64 DFMA peak
+           measured live (sdb_fp64_peak; MEASURED_PEAKS.json has no FP64 figure).
+  cpu_baseline  the oracle port (numpy restatement of the reference's
+           run_batch, same op order, same thread pool) on a bounded sample.
+--impl reference times that CPU implementation alone (rank 0).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+
+WORKLOADS = {
+    # BASELINE.json configs[1] -- the headline
+    "cfg2": dict(n=16, orbits=65536, dt=1e-3, steps=10000, ksteps=10000, stream="sfc64",
+                 solver="em", batch="kgrid",
+                 desc="stochastic Kuramoto n=16, 65,536 orbits (256 K x 256 sigma grid), sfc64, "
+                      "E-M dt=1e-3, 10^4 steps, final state only"),
+    "cfg1": dict(n=4, orbits=1024, dt=1e-3, steps=10000, ksteps=10000, stream="xoshiro256pp",
+                 solver="em", batch="speed", desc="n=4, 1,024 orbits, xoshiro256++, 10^4 steps"),
+    "cfg3_n32": dict(n=32, orbits=1 << 20, dt=1e-3, steps=1000, ksteps=1000, stream="philox",
+                     solver="em", batch="speed", desc="n=32, 2^20 orbits, 1000 steps"),
+    "cfg3_n64": dict(n=64, orbits=1 << 20, dt=1e-3, steps=1000, ksteps=1000, stream="philox",
+                     solver="em", batch="speed", desc="n=64, 2^20 orbits, 1000 steps"),
+    "cfg3_n128": dict(n=128, orbits=1 << 20, dt=1e-3, steps=200, ksteps=200, stream="philox",
+                      solver="em", batch="speed", desc="n=128, 2^20 orbits, 200 steps"),
+    "cfg3_n256": dict(n=256, orbits=1 << 20, dt=1e-3, steps=100, ksteps=100, stream="philox",
+                      solver="em", batch="speed", desc="n=256, 2^20 orbits, 100 steps"),
+    "cfg4": dict(n=64, orbits=1 << 18, dt=1e-3, steps=1000, ksteps=1000, stream="philox",
+                 solver="rk4", batch="kgrid_ode",
+                 desc="deterministic Kuramoto n=64, RK4, 2^18 orbits (512 K x 512 omega draws)"),
+    "cfg5": dict(n=32, orbits=131072, dt=1e-3, steps=1000, ksteps=10, stream="philox",
+                 solver="em", batch="resample",
+                 desc="n=32, 512 parameter sets x 256 realisations, trajectory every 10 steps"),
+}
+
+
+def algorithmic_fp64_ops(n: int, solver: str, coupling: str) -> float:
+    """FP64 lane-ops per orbit-step of the algorithm the kernel runs
+    (per-function costs = libdevice fast paths on
+    sm_100a as counted in SURVEY.md 8d): sincos 22, sin 15, Box-Muller 35 per
+    normal, EM update 5 per oscillator, coupling accumulate 2 per term."""
+    if coupling == "meanfield":
+        drift = n * (22 + 2 + 2 + 2)           # sincos, 2 sums, S_i, f_i
+    else:
+        pairs = n * (n - 1) / 2
+        drift = pairs * 18 + n * 2             # diff + sin + 2 accumulates; f_i
+    if solver == "rk4":
+        return 4 * drift + n * 9               # 4 stages + stage/accumulate updates
+    if solver == "em":
+        return drift + n * (35 + 5)
+    return drift + n * 2
+
+
+def pairwise_equivalent_ops(n: int) -> float:
+    """SURVEY.md 8d W_EM(n) = 9 n(n-1) + 41 n (the reference algorithm's work)."""
+    return 9.0 * n * (n - 1) + 41.0 * n
+
+
+# ---------------------------------------------------------------------------
+
+def make_batch(sdb, w, orbit_offset: int, seed: int = 20260809):
+    n, m = w["n"], w["orbits"]
+    local = np.arange(m)
+    if w["batch"] == "speed":
+        return sdb.sample_kuramoto_batch(n, m, (0.01, 0.03), (0.001, 0.003), 1.0, seed,
+                                         orbit_offset=orbit_offset)
+    if w["batch"] == "kgrid":
+        b = sdb.sample_kuramoto_batch(n, m, (0.2, 0.4), (0.01, 0.03), 0.0, seed,
+                                      orbit_offset=orbit_offset)
+        params = b.params.copy()
+        params[:, 0] = np.linspace(0.0, 0.5, 256)[(local // 256) % 256]
+        params[:, n + 1:] = np.geomspace(1e-3, 1e-1, 256)[local % 256][:, None]
+        return sdb.OrbitBatch(init=b.init, params=params)
+    if w["batch"] == "kgrid_ode":  # cfg4: 512 K x 512 omega draws, zero diffusion
+        b = sdb.sample_kuramoto_batch(n, m, (0.2, 0.4), (0.0, 0.0), 0.0, seed,
+                                      orbit_offset=orbit_offset)
+        params = b.params.copy()
+        params[:, 0] = np.linspace(0.0, 2.0, 512)[(local // 512) % 512]
+        return sdb.OrbitBatch(init=b.init, params=params)
+    if w["batch"] == "resample":  # cfg5: 512 sets x 256 realisations
+        sets = m // 256
+        b = sdb.sample_kuramoto_batch(n, sets, (0.2, 0.4), (0.01, 0.03), 0.0, seed,
+                                      orbit_offset=orbit_offset // 256)
+        params = b.params.copy()
+        params[:, 0] = np.linspace(0.05, 0.8, 16)[np.arange(sets) % 16]
+        return sdb.OrbitBatch(init=np.repeat(b.init, 256, axis=0),
+                              params=np.repeat(params, 256, axis=0))
+    raise ValueError(w["batch"])
+
+
+def make_model(sdb, w):
+    n = w["n"]
+    if w["solver"] == "rk4":
+        return sdb.ModelSpec(name="kuramoto-ode:%d" % n, nequat=n, nparams=2 * n + 1, nnoise=0,
+                             drift=sdb.model._kuramoto_drift)
+    return sdb.kuramoto_model(n)
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines: list[str] = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), "--query-gpu=" + self.FIELDS,
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.thread.join(timeout=2)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[3:7]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        if not sm:
+            return None
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(mx)),
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+def dist_setup(want_gpus: int):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist_mod
+        torch.cuda.set_device(local)
+        dist_mod.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist = dist_mod
+    return world, rank, local, dist
+
+
+def reduce_max(dist, value: float) -> float:
+    if dist is None:
+        return value
+    import torch
+    t = torch.tensor([value], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(dist):
+    if dist is not None:
+        dist.barrier()
+
+
+# ---------------------------------------------------------------------------
+# CPU side: the oracle port (reference algorithm) on a bounded sample
+
+def cpu_sample_rate(w, seconds: float, threads: int, stream_override=None):
+    """orbit-steps/s of the oracle port (numpy restatement of the reference's
+    run_batch, engine.py:221-314) on M_cpu orbits x S_cpu steps of workload w."""
+    from oracle import sdeb_oracle as O
+    n = w["n"]
+    m_cpu = min(w["orbits"], 8192 if n <= 32 else 1024)
+    init, params = O.sample_kuramoto_batch(n, m_cpu, (0.2, 0.4), (0.01, 0.03), 0.3, 20260809)
+    if w["solver"] == "rk4":
+        params[:, n + 1:] = 0.0
+    stream = stream_override or w["stream"]
+    group = max(1, m_cpu // threads)
+    nnoise = 0 if w["solver"] == "rk4" else n
+
+    def run(steps):
+        t0 = time.perf_counter()
+        O.integrate(init, params, dt=w["dt"], ksteps=steps, chunks=1, seed=1,
+                    solver=w["solver"], nnoise=nnoise, stream=stream, threads=threads, group=group)
+        return time.perf_counter() - t0
+
+    probe = 3
+    dt_probe = run(probe)
+    s_cpu = int(max(probe, min(100000, seconds / max(dt_probe / probe, 1e-9))))
+    return m_cpu, s_cpu, group, run
+
+
+def cpu_baseline(w, seconds: float):
+    threads = os.cpu_count() or 1
+    m_cpu, s_cpu, group, run = cpu_sample_rate(w, seconds, threads, "philox")
+    elapsed = run(s_cpu)
+    return {"value": m_cpu * s_cpu / elapsed, "unit": "orbit-steps/s", "cores": threads,
+            "kind": "port",
+            "sample": "oracle port of run_batch (numpy, reference op order, %s stream), "
+                      "%d orbits x %d steps of %s, ThreadPool(%d) over groups of %d, %.1f s"
+                      % ("philox (the reference's own generator)" if w["solver"] == "em" else "no", m_cpu, s_cpu,
+                         w["desc"].split(",")[0], threads, group, elapsed)}
+
+
+def run_reference_arm(args, w, world, rank):
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    m_cpu, s_cpu, group, run = cpu_sample_rate(w, args.ref_seconds, threads, "philox")
+    for _ in range(args.warmup):
+        run(max(1, s_cpu // 10))
+    times = [run(s_cpu) for _ in range(args.steps)]
+    ms = 1e3 * float(np.mean(times))
+    value = m_cpu * s_cpu / (ms * 1e-3)
+    line = {
+        "impl": "reference", "metric": "orbit-steps/s", "value": value, "unit": "orbit-steps/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (sampled batch, reference sampler)",
+        "config": {"workload": args.workload, "desc": w["desc"], "n": w["n"],
+                   "cpu_sample_orbits": m_cpu, "cpu_sample_steps": s_cpu},
+        "cpu_baseline": {"value": value, "unit": "orbit-steps/s", "cores": threads,
+                         "kind": "port",
+                         "sample": "%d orbits x %d SDE steps per bench step, oracle port of "
+                                   "run_batch (reference is pure Python: no compiled _ref), "
+                                   "ThreadPool(%d) over groups of %d" % (m_cpu, s_cpu, threads,
+                                                                         group)},
+        "e2e": {"value": value, "unit": "orbit-steps/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+
+def run_ours(args, w, world, rank, local, dist):
+    import torch
+
+    import paper_1908_03869_b200 as sdb
+    from paper_1908_03869_b200 import _native as nat
+    from paper_1908_03869_b200.engine import make_desc
+
+    torch.cuda.set_device(local)
+    n, m, steps = w["n"], w["orbits"], w["steps"]
+    chunks = steps // w["ksteps"]
+    model = make_model(sdb, w)
+    offset = rank * m
+    batch = make_batch(sdb, w, offset)
+    cfg = sdb.EngineConfig(dt=w["dt"], tspan=w["dt"] * steps, ksteps=w["ksteps"], orbits=m,
+                           solver=w["solver"], seed=20260809, stream=w["stream"],
+                           coupling=args.coupling, devices=(local,),
+                           max_store_bytes=1 << 40)
+    assert sdb.iteration_count(cfg.tspan, cfg.dt, cfg.ksteps) == chunks
+    ctx = nat.context((local,))
+    lib = nat.lib()
+    desc = make_desc(model, cfg, chunks, m, orbit_offset=offset)
+
+    d_init = torch.from_numpy(np.ascontiguousarray(batch.init)).cuda()
+    d_params = torch.from_numpy(np.ascontiguousarray(batch.params)).cuda()
+    d_values = torch.empty((m, chunks, n), dtype=torch.float64, device="cuda")
+    d_fail = torch.empty(m, dtype=torch.int64, device="cuda")
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    def launch():
+        nat.check(lib.sdb_run_device(ctx, desc, d_init.data_ptr(), d_params.data_ptr(),
+                                     d_values.data_ptr(), d_fail.data_ptr(), stream.cuda_stream),
+                  ctx, "sdb_run_device")
+
+    for _ in range(max(args.warmup, 3)):
+        launch()
+    torch.cuda.synchronize()
+    lanes = int(lib.sdb_last_lanes(ctx))
+    launches_per_step = int(lib.sdb_last_launch_count(ctx))
+
+    clocks = ClockSampler(local)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    barrier(dist)
+    torch.cuda.synchronize()
+    clocks.start()
+    time.sleep(0.3)  # let the sampler attach before the first timed launch
+    for i in range(args.steps):
+        flush.zero_()
+        ev[i][0].record(stream)
+        launch()
+        ev[i][1].record(stream)
+    torch.cuda.synchronize()
+    barrier(dist)
+    clock_info = clocks.stop()
+    kernel_ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = reduce_max(dist, float(sum(kernel_ms)))
+    ms_per_step = total_ms / args.steps
+    orbit_steps = float(m) * steps
+    value = world * orbit_steps / (ms_per_step * 1e-3)
+
+    # sanity: the timed runs produced finite final states
+    assert torch.isfinite(d_values).all().item(), "non-finite states in the benchmark run"
+
+    # --- e2e through the public API (host numpy buffers) ---
+    host_batch = sdb.OrbitBatch(init=batch.init.copy(), params=batch.params.copy())
+    sdb.run_batch(model, cfg, host_batch)  # warm (autotune cache, pageable staging)
+    barrier(dist)
+    t0 = time.perf_counter()
+    e2e_steps = max(1, min(args.steps, 5))
+    for _ in range(e2e_steps):
+        store = sdb.run_batch(model, cfg, host_batch)
+    e2e_s = reduce_max(dist, time.perf_counter() - t0) / e2e_steps
+    h2d = batch.init.nbytes + batch.params.nbytes
+    d2h = m * chunks * n * 8 + m * 8
+    e2e = {"value": world * orbit_steps / e2e_s, "unit": "orbit-steps/s",
+           "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+           "ms_per_step": e2e_s * 1e3, "host_buffers": "pageable numpy (run_batch)"}
+    del store
+
+    # --- roofline (FP64 pipe) ---
+    peak_ops = ctypes_peak(lib, ctx)
+    ops = algorithmic_fp64_ops(n, w["solver"], args.coupling)
+    achieved = ops * orbit_steps / (np.mean(kernel_ms) * 1e-3)
+    roofline = {
+        "bound": "fp64", "unit": "TFLOP/s",
+        "achieved": 2 * achieved / 1e12, "peak": 2 * peak_ops / 1e12,
+        "frac": achieved / peak_ops,
+        "traffic": None,
+        "algorithmic_fp64_ops_per_orbit_step": ops,
+        "peak_source": "measured live: sdb_fp64_peak DFMA-throughput kernel (FLOP = 2 x DFMA)",
+        "pairwise_equivalent_frac": pairwise_equivalent_ops(n) * orbit_steps
+        / (np.mean(kernel_ms) * 1e-3) / peak_ops if w["solver"] == "em" else None,
+    }
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(w, args.cpu_seconds)
+
+    if rank == 0:
+        line = {
+            "metric": "orbit-steps/s", "value": value, "unit": "orbit-steps/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (device-sampled Kuramoto batch, reference sampler bit-exact)",
+            "config": {"workload": args.workload, "desc": w["desc"], "n": n,
+                       "orbits_per_gpu": m, "sde_steps": steps, "ksteps": w["ksteps"],
+                       "solver": w["solver"], "stream": w["stream"], "coupling": args.coupling,
+                       "lanes_per_orbit": lanes, "parallelism": "orbit-shard x%d" % world,
+                       "l2": "flushed (512 MiB memset) between timed steps, outside the "
+                             "event pairs"},
+            "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu,
+            "gpu_launches": launches_per_step * args.steps,
+            "clocks": clock_info,
+            "kernel_ms": kernel_ms,
+        }
+        print(json.dumps(line), flush=True)
+
+
+def ctypes_peak(lib, ctx) -> float:
+    import ctypes
+    ops = ctypes.c_double()
+    ms = ctypes.c_double()
+    from paper_1908_03869_b200 import _native as nat
+    nat.check(lib.sdb_fp64_peak(ctx, ctypes.byref(ops), ctypes.byref(ms)), ctx, "sdb_fp64_peak")
+    return ops.value
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="cfg2")
+    ap.add_argument("--coupling", choices=["meanfield", "pairwise"], default="meanfield")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--ref-seconds", type=float, default=2.0)
+    args = ap.parse_args()
+    w = WORKLOADS[args.workload]
+    world, rank, local, dist = (int(os.environ.get("WORLD_SIZE", "1")),
+                                int(os.environ.get("RANK", "0")),
+                                int(os.environ.get("LOCAL_RANK", "0")), None)
+    if args.impl == "reference":
+        run_reference_arm(args, w, world, rank)
+        return
+    world, rank, local, dist = dist_setup(args.gpus)
+    try:
+        run_ours(args, w, world, rank, local, dist)
+    finally:
+        if dist is not None:
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,155 @@
+/* sdeb200 -- C ABI of the B200-native ensemble SDE integrator.
+ *
+ * The reference (sdebatch, pure Python/numpy) has no C ABI or plugin
+ * registry: its hot path sits behind Python functions.  Each entry point
+ * below names the reference interface it replaces (paths relative to
+ * /root/reference/pkg/src/sdebatch).  The Python package
+ * paper_1908_03869_b200 binds this ABI with ctypes.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only; no torch or Python types cross the ABI.
+ *  - Host arrays are C-order float64 / uint32 / uint64 / int64 owned by the
+ *    caller.  "_device" entry points take device pointers plus a cudaStream_t
+ *    passed as void*.
+ *  - Status codes: SDB_OK, or an error whose message sdb_last_error(ctx)
+ *    returns (ctx may be NULL for context-free calls; the message is then
+ *    thread-local).  Per-orbit solver failures are data (fail_step), not errors.
+ *  - A context is used by one host thread at a time.
+ */
+#ifndef SDEB200_H
+#define SDEB200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SDB_ABI_VERSION 1
+
+typedef enum sdb_status {
+    SDB_OK = 0,
+    SDB_ERR_CONFIG = 1,      /* maps to ConfigError (engine.py:77) */
+    SDB_ERR_UNSUPPORTED = 2, /* maps to NotImplementedError */
+    SDB_ERR_CUDA = 3,        /* maps to RuntimeError */
+    SDB_ERR_ARGUMENT = 4     /* maps to ValueError */
+} sdb_status;
+
+enum { SDB_MODEL_KURAMOTO = 1 };                 /* model.py:188-220 */
+enum { SDB_SOLVER_EM = 0, SDB_SOLVER_EULER = 1, SDB_SOLVER_RK4 = 2 }; /* solvers.py:369-375 */
+enum { SDB_STREAM_PHILOX = 0, SDB_STREAM_SFC64 = 1, SDB_STREAM_XOSHIRO256PP = 2 };
+/* How the coupling sum S_i = sum_j sin(y_j - y_i) (model.py:193-195) is evaluated:
+ * MEANFIELD: S_i = cos(y_i) * sum_j sin(y_j) - sin(y_i) * sum_j cos(y_j)  (O(n));
+ * PAIRWISE : every term sin(fl(y_j - y_i)) as the reference rounds it (O(n^2)). */
+enum { SDB_COUPLING_MEANFIELD = 0, SDB_COUPLING_PAIRWISE = 1 };
+
+typedef struct sdb_ctx sdb_ctx;
+
+/* One integration run: the fields of EngineConfig (engine.py:81-101) that the
+ * device needs, after the host has validated them (engine.py:103-117,
+ * 229-245) and computed chunks = iteration_count(...) (engine.py:163-179). */
+typedef struct sdb_desc {
+    int32_t model;        /* SDB_MODEL_KURAMOTO */
+    int32_t nequat;       /* n oscillators */
+    int32_t nparams;      /* row length of params: (K, omega_1..n[, s_1..n, ...]) */
+    int32_t nnoise;       /* n (stochastic) or 0 (ODE) */
+    int32_t solver;       /* SDB_SOLVER_* */
+    int32_t stream;       /* SDB_STREAM_* (ignored unless solver=EM and nnoise>0) */
+    int32_t coupling;     /* SDB_COUPLING_* */
+    int32_t lanes;        /* lanes per orbit (power of two, <= 32); 0 = autotune */
+    uint64_t seed;        /* EngineConfig.seed reduced mod 2**64 (rng.py:145-147) */
+    double dt;
+    int64_t ksteps;       /* steps per chunk; one sample per chunk (engine.py:268-299) */
+    int64_t chunks;       /* k; samples = k + 1 */
+    int64_t orbits;       /* rows in this call */
+    int64_t orbit_offset; /* global orbit id of row 0 (noise is keyed by it) */
+} sdb_desc;
+
+int sdb_abi_version(void);
+int sdb_device_count(void);
+
+/* Context over a list of devices; orbits of one run are sharded across them
+ * in contiguous ranges (the analogue of partition_orbits + the worker pool,
+ * engine.py:182-187, 302-311).  A device id may repeat (two shards on one GPU). */
+sdb_status sdb_open(const int* devices, int ndevices, sdb_ctx** out);
+void sdb_close(sdb_ctx* ctx);
+const char* sdb_last_error(const sdb_ctx* ctx);
+
+/* Replaces run_batch's integration (engine.py:221-314).
+ * init:   [orbits][nequat]   params: [orbits][nparams]
+ * values: [orbits][chunks+1][nequat], caller-allocated; sample 0 is written
+ *         as a verbatim copy of init (engine.py:251), samples 1..k by the device.
+ * fail_step: [orbits]; absolute step index of the orbit's first non-finite
+ *         state (engine.py:281-298) or -1.  Rows of failed orbits are NaN from
+ *         that step on. */
+sdb_status sdb_run(sdb_ctx* ctx, const sdb_desc* desc, const double* init,
+                   const double* params, double* values, int64_t* fail_step);
+
+/* Same integration on device-resident buffers on the context's FIRST device
+ * (benchmarks: inputs already in HBM).  d_values: [orbits][chunks][nequat]
+ * (samples 1..k only).  Launches on `stream` (a cudaStream_t); asynchronous. */
+sdb_status sdb_run_device(sdb_ctx* ctx, const sdb_desc* desc, const double* d_init,
+                          const double* d_params, double* d_values, int64_t* d_fail_step,
+                          void* stream);
+
+/* Number of kernel launches the last sdb_run/sdb_run_device issued (all devices). */
+int64_t sdb_last_launch_count(const sdb_ctx* ctx);
+/* Lanes-per-orbit layout chosen by the last run (after autotune). */
+int32_t sdb_last_lanes(const sdb_ctx* ctx);
+
+/* ---- noise streams (rng.py) ------------------------------------------------ */
+
+/* Philox-4x32-10 blocks: in [count][6] = (k0, k1, c0, c1, c2, c3), out [count][4].
+ * Replaces rng._philox_words / philox_block (rng.py:74-118). */
+sdb_status sdb_philox_words(sdb_ctx* ctx, const uint32_t* in, int64_t count, uint32_t* out);
+
+/* Standard normals for one step of a group of orbits: out [count][m].
+ * Replaces rng.normals_for_orbits (rng.py:150-188) for stream=PHILOX
+ * (chunk/step are the two free counter words).  For SFC64/XOSHIRO256PP the
+ * draws are those of step index (chunk<<32 | step) of the per-(orbit, block)
+ * stream. */
+sdb_status sdb_normals(sdb_ctx* ctx, int32_t stream, uint64_t seed, const uint32_t* orbits,
+                       int64_t count, uint32_t chunk, uint32_t step, int32_t m, double* out);
+
+/* Raw 64-bit outputs of one per-(orbit, block) SFC64/XOSHIRO256PP stream. */
+sdb_status sdb_stream_raw(sdb_ctx* ctx, int32_t stream, uint64_t seed, uint64_t orbit,
+                          uint64_t block, int64_t count, uint64_t* out);
+
+/* Reserved-tag sampling uniforms on [0,1): out [count][ncols].
+ * Replaces rng.sampling_uniforms (rng.py:200-222). */
+sdb_status sdb_sampling_uniforms(sdb_ctx* ctx, uint64_t seed, const uint32_t* orbits,
+                                 int64_t count, int32_t ncols, double* out);
+
+/* Kuramoto batch sampler: init [count][n], params [count][2n+1].
+ * Replaces model.sample_kuramoto_batch (model.py:242-270). */
+sdb_status sdb_sample_kuramoto(sdb_ctx* ctx, int32_t n, uint64_t seed, const uint32_t* orbits,
+                               int64_t count, double omega_lo, double omega_hi,
+                               double noise_lo, double noise_hi, double coupling,
+                               double* init, double* params);
+
+/* ---- per-step API (solvers.py / model.py) --------------------------------- */
+
+/* Kuramoto drift f(y, p) for count rows: replaces model.drift_eval with the
+ * native _kuramoto_drift (model.py:142-157, 188-196). */
+sdb_status sdb_drift(sdb_ctx* ctx, int32_t n, int32_t nparams, int32_t coupling, int64_t count,
+                     const double* y, const double* p, double* f);
+
+/* One step of solver for count rows with explicit noise [count][n] (EM only;
+ * may be NULL otherwise): replaces euler_maruyama_step / euler_step / rk4_step
+ * (solvers.py:63-88) for the Kuramoto model. */
+sdb_status sdb_step(sdb_ctx* ctx, int32_t solver, int32_t n, int32_t nparams, int32_t nnoise,
+                    int32_t coupling, int64_t count, double dt, const double* y,
+                    const double* p, const double* noise, double* out);
+
+/* ---- measurement --------------------------------------------------------- */
+
+/* FP64 pipe peak of the context's first device: a DFMA-throughput kernel
+ * (ILP 8, one wave of resident CTAs per SM).  Writes FP64 lane-operations per
+ * second (one DFMA = one op = 2 flops) and the kernel time in ms.  This is the
+ * roofline denominator bench.py reports (MEASURED_PEAKS.json has no FP64 figure). */
+sdb_status sdb_fp64_peak(sdb_ctx* ctx, double* ops_per_s, double* ms);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SDEB200_H */

@@ -1,0 +1,165 @@
+"""ctypes binding of include/sdeb200.h (libsdeb200.so, built in-tree).
+
+There is deliberately no fallback: if the library is missing, or no CUDA
+device is visible, every device entry point raises.  ctypes releases the GIL
+for the duration of each call (the reference's worker pool, engine.py:302-311,
+becomes per-device host threads inside the library).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.environ.get("SDEB200_LIB", os.path.join(_HERE, "libsdeb200.so"))
+
+SDB_OK, SDB_ERR_CONFIG, SDB_ERR_UNSUPPORTED, SDB_ERR_CUDA, SDB_ERR_ARGUMENT = range(5)
+SDB_MODEL_KURAMOTO = 1
+SOLVER_IDS = {"em": 0, "euler": 1, "rk4": 2}
+STREAM_IDS = {"philox": 0, "sfc64": 1, "xoshiro256pp": 2}
+COUPLING_IDS = {"meanfield": 0, "pairwise": 1}
+
+_c_double_p = ctypes.POINTER(ctypes.c_double)
+_c_u32_p = ctypes.POINTER(ctypes.c_uint32)
+_c_u64_p = ctypes.POINTER(ctypes.c_uint64)
+_c_i64_p = ctypes.POINTER(ctypes.c_int64)
+
+
+class SdbDesc(ctypes.Structure):
+    _fields_ = [
+        ("model", ctypes.c_int32), ("nequat", ctypes.c_int32), ("nparams", ctypes.c_int32),
+        ("nnoise", ctypes.c_int32), ("solver", ctypes.c_int32), ("stream", ctypes.c_int32),
+        ("coupling", ctypes.c_int32), ("lanes", ctypes.c_int32), ("seed", ctypes.c_uint64),
+        ("dt", ctypes.c_double), ("ksteps", ctypes.c_int64), ("chunks", ctypes.c_int64),
+        ("orbits", ctypes.c_int64), ("orbit_offset", ctypes.c_int64),
+    ]
+
+
+# name -> (restype, argtypes); mirrors include/sdeb200.h one to one
+SIGNATURES = {
+    "sdb_abi_version": (ctypes.c_int, []),
+    "sdb_device_count": (ctypes.c_int, []),
+    "sdb_open": (ctypes.c_int, [ctypes.POINTER(ctypes.c_int), ctypes.c_int,
+                                ctypes.POINTER(ctypes.c_void_p)]),
+    "sdb_close": (None, [ctypes.c_void_p]),
+    "sdb_last_error": (ctypes.c_char_p, [ctypes.c_void_p]),
+    "sdb_run": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(SdbDesc), _c_double_p,
+                               _c_double_p, _c_double_p, _c_i64_p]),
+    "sdb_run_device": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(SdbDesc), ctypes.c_void_p,
+                                      ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                      ctypes.c_void_p]),
+    "sdb_last_launch_count": (ctypes.c_int64, [ctypes.c_void_p]),
+    "sdb_last_lanes": (ctypes.c_int32, [ctypes.c_void_p]),
+    "sdb_philox_words": (ctypes.c_int, [ctypes.c_void_p, _c_u32_p, ctypes.c_int64, _c_u32_p]),
+    "sdb_normals": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_uint64, _c_u32_p,
+                                   ctypes.c_int64, ctypes.c_uint32, ctypes.c_uint32,
+                                   ctypes.c_int32, _c_double_p]),
+    "sdb_stream_raw": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_uint64,
+                                      ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int64, _c_u64_p]),
+    "sdb_sampling_uniforms": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_uint64, _c_u32_p,
+                                             ctypes.c_int64, ctypes.c_int32, _c_double_p]),
+    "sdb_sample_kuramoto": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_uint64,
+                                           _c_u32_p, ctypes.c_int64, ctypes.c_double,
+                                           ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                           ctypes.c_double, _c_double_p, _c_double_p]),
+    "sdb_drift": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                 ctypes.c_int64, _c_double_p, _c_double_p, _c_double_p]),
+    "sdb_fp64_peak": (ctypes.c_int, [ctypes.c_void_p, _c_double_p, _c_double_p]),
+    "sdb_step": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                ctypes.c_int32, ctypes.c_int32, ctypes.c_int64, ctypes.c_double,
+                                _c_double_p, _c_double_p, _c_double_p, _c_double_p]),
+}
+
+_lib = None
+_lib_lock = threading.Lock()
+_contexts: dict = {}
+
+
+class DeviceError(RuntimeError):
+    """A CUDA / device-side failure reported by libsdeb200."""
+
+
+def lib():
+    """Load libsdeb200.so (raises if it has not been built)."""
+    global _lib
+    if _lib is None:
+        with _lib_lock:
+            if _lib is None:
+                if not os.path.exists(LIB_PATH):
+                    raise RuntimeError(
+                        "libsdeb200.so is not built (%s); run "
+                        "`python -m paper_1908_03869_b200._build` -- there is no CPU fallback"
+                        % LIB_PATH)
+                handle = ctypes.CDLL(LIB_PATH)
+                for name, (res, args) in SIGNATURES.items():
+                    fn = getattr(handle, name)
+                    fn.restype = res
+                    fn.argtypes = args
+                if handle.sdb_abi_version() != 1:
+                    raise RuntimeError("libsdeb200.so ABI mismatch")
+                _lib = handle
+    return _lib
+
+
+def last_error(ctx=None) -> str:
+    msg = lib().sdb_last_error(ctx)
+    return msg.decode() if msg else ""
+
+
+def check(status: int, ctx=None, what: str = "sdeb200"):
+    """Map an sdb_status onto the reference's exception types."""
+    if status == SDB_OK:
+        return
+    msg = "%s: %s" % (what, last_error(ctx))
+    if status == SDB_ERR_CONFIG:
+        from .engine import ConfigError
+        raise ConfigError(msg)
+    if status == SDB_ERR_UNSUPPORTED:
+        raise NotImplementedError(msg)
+    if status == SDB_ERR_ARGUMENT:
+        raise ValueError(msg)
+    raise DeviceError(msg)
+
+
+def device_count() -> int:
+    return int(lib().sdb_device_count())
+
+
+def context(devices=None):
+    """Cached sdb_ctx for a device tuple (default: SDEB200_DEVICES or (0,))."""
+    if devices is None:
+        env = os.environ.get("SDEB200_DEVICES")
+        devices = tuple(int(d) for d in env.split(",")) if env else (0,)
+    devices = tuple(int(d) for d in devices)
+    ctx = _contexts.get(devices)
+    if ctx is None:
+        arr = (ctypes.c_int * len(devices))(*devices)
+        out = ctypes.c_void_p()
+        check(lib().sdb_open(arr, len(devices), ctypes.byref(out)), None, "sdb_open")
+        ctx = out.value
+        _contexts[devices] = ctx
+    return ctx
+
+
+def dptr(a: np.ndarray):
+    return a.ctypes.data_as(_c_double_p)
+
+
+def u32ptr(a: np.ndarray):
+    return a.ctypes.data_as(_c_u32_p)
+
+
+def u64ptr(a: np.ndarray):
+    return a.ctypes.data_as(_c_u64_p)
+
+
+def i64ptr(a: np.ndarray):
+    return a.ctypes.data_as(_c_i64_p)
+
+
+def f64(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float64)

@@ -1,0 +1,680 @@
+// C ABI (include/sdeb200.h): contexts, validation, sharding, layout
+// autotune, host<->device staging.  The reference equivalent is run_batch's
+// driver (engine.py:221-314) and its thread pool over contiguous orbit
+// groups (engine.py:182-187, 302-311): here the groups are per-device shards
+// driven by one host thread each, and the per-group Python step loop is the
+// fused kernel of sdeb_kuramoto.cuh.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <thread>
+#include <tuple>
+#include <vector>
+
+#include "../../include/sdeb200.h"
+#include "sdeb_kuramoto.cuh"
+#include "sdeb_misc.h"
+
+namespace sdeb {
+template <int J>
+cudaError_t launch_kuramoto_j(const RunArgs& a, int solver, int stream, int coupling,
+                              cudaStream_t st);
+}
+
+namespace {
+
+thread_local std::string g_thread_error;
+
+struct DevBuf {
+    void* ptr = nullptr;
+    size_t cap = 0;
+    cudaError_t ensure(size_t bytes) {
+        if (bytes <= cap) return cudaSuccess;
+        if (ptr) cudaFree(ptr);
+        ptr = nullptr;
+        cap = 0;
+        const size_t want = std::max<size_t>(bytes, 256);
+        cudaError_t e = cudaMalloc(&ptr, want);
+        if (e == cudaSuccess) cap = want;
+        return e;
+    }
+    void release() {
+        if (ptr) cudaFree(ptr);
+        ptr = nullptr;
+        cap = 0;
+    }
+    template <class T>
+    T* as() const {
+        return static_cast<T*>(ptr);
+    }
+};
+
+struct Slot {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    DevBuf init, params, values, state, fail, rng;
+    DevBuf t_values, t_state, t_fail, t_rng;  // autotune scratch
+    int64_t launches = 0;
+    int32_t lanes = 0;
+    std::string error;
+};
+
+using TuneKey = std::tuple<int, int, int, int, int, int64_t, int>;
+
+}  // namespace
+
+struct sdb_ctx {
+    std::vector<Slot> slots;
+    std::string error;
+    int64_t launches = 0;
+    int32_t last_lanes = 0;
+    std::map<TuneKey, int> tune;
+};
+
+namespace {
+
+sdb_status fail_with(sdb_ctx* ctx, sdb_status st, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    if (ctx) ctx->error = buf;
+    g_thread_error = buf;
+    return st;
+}
+
+sdb_status cuda_fail(sdb_ctx* ctx, cudaError_t e, const char* what) {
+    return fail_with(ctx, SDB_ERR_CUDA, "%s: %s (%s)", what, cudaGetErrorString(e),
+                     cudaGetErrorName(e));
+}
+
+#define SDB_CUDA(ctx, expr)                                      \
+    do {                                                         \
+        cudaError_t e__ = (expr);                                \
+        if (e__ != cudaSuccess) return cuda_fail(ctx, e__, #expr); \
+    } while (0)
+
+int next_pow2(int n) {
+    int p = 1;
+    while (p < n) p <<= 1;
+    return p;
+}
+
+int ilog2(int x) {
+    int l = 0;
+    while ((1 << l) < x) ++l;
+    return l;
+}
+
+cudaError_t launch_run(const sdeb::RunArgs& a, int J, int solver, int stream, int coupling,
+                       cudaStream_t st) {
+    switch (J) {
+        case 1: return sdeb::launch_kuramoto_j<1>(a, solver, stream, coupling, st);
+        case 2: return sdeb::launch_kuramoto_j<2>(a, solver, stream, coupling, st);
+        case 4: return sdeb::launch_kuramoto_j<4>(a, solver, stream, coupling, st);
+        case 8: return sdeb::launch_kuramoto_j<8>(a, solver, stream, coupling, st);
+        case 16: return sdeb::launch_kuramoto_j<16>(a, solver, stream, coupling, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+// Kernel kind for a validated descriptor.
+void kernel_kind(const sdb_desc& d, int* solver, int* stream) {
+    if (d.solver == SDB_SOLVER_RK4) {
+        *solver = sdeb::KS_RK4;
+        *stream = sdeb::KS_NONE;
+    } else if (d.solver == SDB_SOLVER_EM && d.nnoise > 0) {
+        *solver = sdeb::KS_EM;
+        *stream = d.stream;  // KS_PHILOX/SFC64/XOSHIRO share the ABI values
+    } else {
+        *solver = sdeb::KS_EM;  // euler, or em on a noise-free model (solvers.py:63-71)
+        *stream = sdeb::KS_NONE;
+    }
+}
+
+constexpr int kMaxLanes = 32;
+constexpr int kMaxJ = 16;
+constexpr int kMaxN = kMaxLanes * kMaxJ;
+
+sdb_status validate(sdb_ctx* ctx, const sdb_desc* d) {
+    if (!d) return fail_with(ctx, SDB_ERR_ARGUMENT, "null descriptor");
+    if (d->model != SDB_MODEL_KURAMOTO)
+        return fail_with(ctx, SDB_ERR_UNSUPPORTED, "only the Kuramoto model has a device path");
+    if (d->nequat < 1) return fail_with(ctx, SDB_ERR_ARGUMENT, "nequat must be >= 1");
+    if (d->nequat > kMaxN)
+        return fail_with(ctx, SDB_ERR_UNSUPPORTED, "nequat=%d above the device limit %d", d->nequat,
+                         kMaxN);
+    if (d->nnoise != 0 && d->nnoise != d->nequat)
+        return fail_with(ctx, SDB_ERR_UNSUPPORTED, "Kuramoto needs nnoise == nequat or 0");
+    if (d->nparams < d->nequat + 1 || (d->nnoise > 0 && d->nparams != 2 * d->nequat + 1))
+        return fail_with(ctx, SDB_ERR_ARGUMENT, "nparams=%d does not fit Kuramoto(n=%d, nnoise=%d)",
+                         d->nparams, d->nequat, d->nnoise);
+    if (d->solver != SDB_SOLVER_EM && d->solver != SDB_SOLVER_EULER && d->solver != SDB_SOLVER_RK4)
+        return fail_with(ctx, SDB_ERR_ARGUMENT, "unknown solver %d", d->solver);
+    if (d->solver != SDB_SOLVER_EM && d->nnoise > 0)
+        return fail_with(ctx, SDB_ERR_CONFIG,
+                         "solver is deterministic but the model has %d noise terms", d->nnoise);
+    if (d->stream < SDB_STREAM_PHILOX || d->stream > SDB_STREAM_XOSHIRO256PP)
+        return fail_with(ctx, SDB_ERR_ARGUMENT, "unknown stream %d", d->stream);
+    if (d->coupling != SDB_COUPLING_MEANFIELD && d->coupling != SDB_COUPLING_PAIRWISE)
+        return fail_with(ctx, SDB_ERR_ARGUMENT, "unknown coupling %d", d->coupling);
+    if (!(d->dt > 0.0)) return fail_with(ctx, SDB_ERR_CONFIG, "dt must be positive");
+    if (d->ksteps < 1) return fail_with(ctx, SDB_ERR_CONFIG, "ksteps must be >= 1");
+    if (d->chunks < 1) return fail_with(ctx, SDB_ERR_CONFIG, "chunks must be >= 1");
+    if (d->orbits < 1) return fail_with(ctx, SDB_ERR_CONFIG, "orbits must be >= 1");
+    if (d->orbit_offset < 0 || d->orbit_offset + d->orbits > (int64_t(1) << 32))
+        return fail_with(ctx, SDB_ERR_CONFIG, "global orbit ids must fit in 32 bits");
+    if (d->chunks > INT64_MAX / d->ksteps)
+        return fail_with(ctx, SDB_ERR_CONFIG, "total step count does not fit in 63 bits");
+    const int P = next_pow2(d->nequat);
+    if (d->lanes != 0) {
+        const int L = d->lanes;
+        if (L < 1 || L > kMaxLanes || (L & (L - 1)) || L > P || P / L > kMaxJ)
+            return fail_with(ctx, SDB_ERR_ARGUMENT, "lanes=%d is not a valid layout for n=%d", L,
+                             d->nequat);
+    }
+    return SDB_OK;
+}
+
+std::vector<int> candidate_lanes(int n) {
+    const int P = next_pow2(n);
+    std::vector<int> out;
+    for (int L = 1; L <= kMaxLanes && L <= P; L <<= 1)
+        if (P / L <= kMaxJ) out.push_back(L);
+    return out;
+}
+
+sdeb::RunArgs make_args(const sdb_desc& d, int lanes) {
+    sdeb::RunArgs a{};
+    a.n = d.nequat;
+    a.nparams = d.nparams;
+    a.nnoise = d.nnoise;
+    a.lanes = lanes;
+    a.log2lanes = ilog2(lanes);
+    a.orbits = d.orbits;
+    a.orbit_offset = d.orbit_offset;
+    a.seed = d.seed;
+    a.dt = d.dt;
+    a.sqrt_dt = std::sqrt(d.dt);  // np.sqrt(dt), IEEE correctly rounded
+    a.half_dt = 0.5 * d.dt;
+    a.dt6 = d.dt / 6.0;
+    a.ksteps = d.ksteps;
+    a.chunk_begin = 0;
+    a.chunk_end = d.chunks;
+    a.vstride = d.chunks;
+    a.fresh = 1;
+    a.check_finite = 1;
+    return a;
+}
+
+size_t rng_words(const sdb_desc& d, int64_t rows) {
+    const bool stateful = d.solver == SDB_SOLVER_EM && d.nnoise > 0 &&
+                          (d.stream == SDB_STREAM_SFC64 || d.stream == SDB_STREAM_XOSHIRO256PP);
+    return stateful ? size_t(rows) * size_t((d.nnoise + 3) / 4) * 4 : 0;
+}
+
+// Pick lanes-per-orbit: explicit, cached, or timed on a short probe into
+// scratch buffers.  Every layout gives bit-identical results (canonical
+// summation tree), so this only affects speed.
+sdb_status choose_lanes(sdb_ctx* ctx, Slot& s, const sdb_desc& d, const double* d_init,
+                        const double* d_params, cudaStream_t st, int* lanes_out) {
+    if (d.lanes != 0) {
+        *lanes_out = d.lanes;
+        return SDB_OK;
+    }
+    std::vector<int> cands = candidate_lanes(d.nequat);
+    if (cands.size() == 1) {
+        *lanes_out = cands[0];
+        return SDB_OK;
+    }
+    int kind_solver, kind_stream;
+    kernel_kind(d, &kind_solver, &kind_stream);
+    const int64_t total = d.chunks * d.ksteps;
+    const TuneKey key{s.device, d.nequat, kind_solver, kind_stream, d.coupling, d.orbits,
+                      int(std::min<int64_t>(total, 1 << 20))};
+    auto it = ctx->tune.find(key);
+    if (it != ctx->tune.end()) {
+        *lanes_out = it->second;
+        return SDB_OK;
+    }
+    const int64_t probe = std::min<int64_t>(total, 32);
+    SDB_CUDA(ctx, s.t_values.ensure(size_t(d.orbits) * d.nequat * sizeof(double)));
+    SDB_CUDA(ctx, s.t_state.ensure(size_t(d.orbits) * d.nequat * sizeof(double)));
+    SDB_CUDA(ctx, s.t_fail.ensure(size_t(d.orbits) * sizeof(int64_t)));
+    SDB_CUDA(ctx, s.t_rng.ensure(std::max<size_t>(rng_words(d, d.orbits), 4) * sizeof(uint64_t)));
+    cudaEvent_t e0, e1;
+    SDB_CUDA(ctx, cudaEventCreate(&e0));
+    SDB_CUDA(ctx, cudaEventCreate(&e1));
+    float best = 1e30f;
+    int best_l = cands[0];
+    for (int L : cands) {
+        sdeb::RunArgs a = make_args(d, L);
+        a.state_in = d_init;
+        a.params = d_params;
+        a.state_out = s.t_state.as<double>();
+        a.values = s.t_values.as<double>();
+        a.vstride = 1;
+        a.fail_step = s.t_fail.as<int64_t>();
+        a.rng_state = s.t_rng.as<uint64_t>();
+        a.ksteps = probe;
+        a.chunk_end = 1;
+        float ms = 0.f;
+        for (int rep = 0; rep < 2; ++rep) {
+            cudaEventRecord(e0, st);
+            cudaError_t e = launch_run(a, next_pow2(d.nequat) / L, kind_solver, kind_stream,
+                                       d.coupling, st);
+            if (e != cudaSuccess) {
+                cudaEventDestroy(e0);
+                cudaEventDestroy(e1);
+                return cuda_fail(ctx, e, "autotune launch");
+            }
+            cudaEventRecord(e1, st);
+            s.launches += 1;
+        }
+        SDB_CUDA(ctx, cudaEventSynchronize(e1));
+        cudaEventElapsedTime(&ms, e0, e1);
+        if (ms < best) {
+            best = ms;
+            best_l = L;
+        }
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    ctx->tune[key] = best_l;
+    *lanes_out = best_l;
+    return SDB_OK;
+}
+
+sdb_status launch_device(sdb_ctx* ctx, Slot& s, const sdb_desc& d, const double* d_init,
+                         const double* d_params, double* d_values, int64_t* d_fail,
+                         cudaStream_t st) {
+    int lanes = 0;
+    sdb_status rc = choose_lanes(ctx, s, d, d_init, d_params, st, &lanes);
+    if (rc != SDB_OK) return rc;
+    SDB_CUDA(ctx, s.state.ensure(size_t(d.orbits) * d.nequat * sizeof(double)));
+    const size_t rw = rng_words(d, d.orbits);
+    if (rw) SDB_CUDA(ctx, s.rng.ensure(rw * sizeof(uint64_t)));
+    int kind_solver, kind_stream;
+    kernel_kind(d, &kind_solver, &kind_stream);
+    sdeb::RunArgs a = make_args(d, lanes);
+    a.state_in = d_init;
+    a.params = d_params;
+    a.state_out = s.state.as<double>();
+    a.values = d_values;
+    a.fail_step = d_fail;
+    a.rng_state = s.rng.as<uint64_t>();
+    cudaError_t e = launch_run(a, next_pow2(d.nequat) / lanes, kind_solver, kind_stream,
+                               d.coupling, st);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "kuramoto_run_kernel launch");
+    s.launches += 1;
+    s.lanes = lanes;
+    return SDB_OK;
+}
+
+// One device's contiguous shard [r0, r0+rows) of a host-buffer run.
+sdb_status run_shard(sdb_ctx* ctx, Slot& s, sdb_desc d, int64_t r0, int64_t rows,
+                     const double* init, const double* params, double* values, int64_t* fail) {
+    SDB_CUDA(ctx, cudaSetDevice(s.device));
+    const int n = d.nequat;
+    d.orbit_offset += r0;
+    d.orbits = rows;
+    SDB_CUDA(ctx, s.init.ensure(size_t(rows) * n * sizeof(double)));
+    SDB_CUDA(ctx, s.params.ensure(size_t(rows) * d.nparams * sizeof(double)));
+    SDB_CUDA(ctx, s.values.ensure(size_t(rows) * d.chunks * n * sizeof(double)));
+    SDB_CUDA(ctx, s.fail.ensure(size_t(rows) * sizeof(int64_t)));
+    SDB_CUDA(ctx, cudaMemcpyAsync(s.init.ptr, init + r0 * n, size_t(rows) * n * sizeof(double),
+                                  cudaMemcpyHostToDevice, s.stream));
+    SDB_CUDA(ctx, cudaMemcpyAsync(s.params.ptr, params + r0 * d.nparams,
+                                  size_t(rows) * d.nparams * sizeof(double),
+                                  cudaMemcpyHostToDevice, s.stream));
+    sdb_status rc = launch_device(ctx, s, d, s.init.as<double>(), s.params.as<double>(),
+                                  s.values.as<double>(), s.fail.as<int64_t>(), s.stream);
+    if (rc != SDB_OK) return rc;
+    const size_t row_bytes = size_t(d.chunks) * n * sizeof(double);
+    // samples 1..k of each row land after the verbatim sample 0 (engine.py:250-251)
+    SDB_CUDA(ctx, cudaMemcpy2DAsync(values + (r0 * (d.chunks + 1) + 1) * n,
+                                    size_t(d.chunks + 1) * n * sizeof(double), s.values.ptr,
+                                    row_bytes, row_bytes, size_t(rows), cudaMemcpyDeviceToHost,
+                                    s.stream));
+    SDB_CUDA(ctx, cudaMemcpyAsync(fail + r0, s.fail.ptr, size_t(rows) * sizeof(int64_t),
+                                  cudaMemcpyDeviceToHost, s.stream));
+    SDB_CUDA(ctx, cudaStreamSynchronize(s.stream));
+    return SDB_OK;
+}
+
+// Scoped device buffer for the context-free utility entry points.
+struct TmpBuf {
+    void* p = nullptr;
+    ~TmpBuf() {
+        if (p) cudaFree(p);
+    }
+};
+
+sdb_status utility_prologue(sdb_ctx* ctx) {
+    if (!ctx || ctx->slots.empty()) return fail_with(ctx, SDB_ERR_ARGUMENT, "null context");
+    SDB_CUDA(ctx, cudaSetDevice(ctx->slots[0].device));
+    return SDB_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int sdb_abi_version(void) { return SDB_ABI_VERSION; }
+
+int sdb_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+sdb_status sdb_open(const int* devices, int ndevices, sdb_ctx** out) {
+    if (!out) return fail_with(nullptr, SDB_ERR_ARGUMENT, "null output pointer");
+    *out = nullptr;
+    int count = sdb_device_count();
+    if (count < 1) return fail_with(nullptr, SDB_ERR_CUDA, "no CUDA device is visible");
+    std::vector<int> devs;
+    if (devices == nullptr || ndevices <= 0) {
+        devs.push_back(0);
+    } else {
+        devs.assign(devices, devices + ndevices);
+    }
+    auto* ctx = new sdb_ctx();
+    for (int dev : devs) {
+        if (dev < 0 || dev >= count) {
+            delete ctx;
+            return fail_with(nullptr, SDB_ERR_ARGUMENT, "device %d out of range (%d visible)", dev,
+                             count);
+        }
+        Slot s;
+        s.device = dev;
+        cudaError_t e = cudaSetDevice(dev);
+        if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking);
+        if (e != cudaSuccess) {
+            delete ctx;
+            return cuda_fail(nullptr, e, "sdb_open");
+        }
+        ctx->slots.push_back(s);
+    }
+    *out = ctx;
+    return SDB_OK;
+}
+
+void sdb_close(sdb_ctx* ctx) {
+    if (!ctx) return;
+    for (Slot& s : ctx->slots) {
+        cudaSetDevice(s.device);
+        for (DevBuf* b : {&s.init, &s.params, &s.values, &s.state, &s.fail, &s.rng, &s.t_values,
+                          &s.t_state, &s.t_fail, &s.t_rng})
+            b->release();
+        if (s.stream) cudaStreamDestroy(s.stream);
+    }
+    delete ctx;
+}
+
+const char* sdb_last_error(const sdb_ctx* ctx) {
+    if (ctx && !ctx->error.empty()) return ctx->error.c_str();
+    return g_thread_error.c_str();
+}
+
+int64_t sdb_last_launch_count(const sdb_ctx* ctx) { return ctx ? ctx->launches : 0; }
+int32_t sdb_last_lanes(const sdb_ctx* ctx) { return ctx ? ctx->last_lanes : 0; }
+
+sdb_status sdb_run(sdb_ctx* ctx, const sdb_desc* desc, const double* init, const double* params,
+                   double* values, int64_t* fail_step) {
+    if (!ctx) return fail_with(nullptr, SDB_ERR_ARGUMENT, "null context");
+    ctx->error.clear();
+    sdb_status rc = validate(ctx, desc);
+    if (rc != SDB_OK) return rc;
+    if (!init || !params || !values || !fail_step)
+        return fail_with(ctx, SDB_ERR_ARGUMENT, "null host buffer");
+    const sdb_desc d = *desc;
+    const int n = d.nequat;
+    // sample 0 is the initial state verbatim (engine.py:251)
+    for (int64_t r = 0; r < d.orbits; ++r)
+        std::memcpy(values + r * (d.chunks + 1) * n, init + r * n, size_t(n) * sizeof(double));
+    const int64_t nslots = int64_t(ctx->slots.size());
+    const int64_t used = std::min<int64_t>(nslots, d.orbits);
+    std::vector<sdb_status> status(used, SDB_OK);
+    std::vector<std::thread> threads;
+    for (Slot& s : ctx->slots) {
+        s.launches = 0;
+        s.error.clear();
+    }
+    // contiguous shards [g*M/G, (g+1)*M/G)
+    auto shard = [&](int64_t g) {
+        const int64_t r0 = g * d.orbits / used, r1 = (g + 1) * d.orbits / used;
+        status[g] = run_shard(ctx, ctx->slots[g], d, r0, r1 - r0, init, params, values, fail_step);
+    };
+    if (used == 1) {
+        shard(0);
+    } else {
+        for (int64_t g = 0; g < used; ++g) threads.emplace_back(shard, g);
+        for (auto& t : threads) t.join();
+    }
+    ctx->launches = 0;
+    for (int64_t g = 0; g < used; ++g) ctx->launches += ctx->slots[g].launches;
+    ctx->last_lanes = ctx->slots[0].lanes;
+    for (int64_t g = 0; g < used; ++g)
+        if (status[g] != SDB_OK) return status[g];
+    return SDB_OK;
+}
+
+sdb_status sdb_run_device(sdb_ctx* ctx, const sdb_desc* desc, const double* d_init,
+                          const double* d_params, double* d_values, int64_t* d_fail_step,
+                          void* stream) {
+    if (!ctx) return fail_with(nullptr, SDB_ERR_ARGUMENT, "null context");
+    ctx->error.clear();
+    sdb_status rc = validate(ctx, desc);
+    if (rc != SDB_OK) return rc;
+    if (!d_init || !d_params || !d_values || !d_fail_step)
+        return fail_with(ctx, SDB_ERR_ARGUMENT, "null device buffer");
+    Slot& s = ctx->slots[0];
+    SDB_CUDA(ctx, cudaSetDevice(s.device));
+    s.launches = 0;
+    rc = launch_device(ctx, s, *desc, d_init, d_params, d_values, d_fail_step,
+                       static_cast<cudaStream_t>(stream));
+    ctx->launches = s.launches;
+    ctx->last_lanes = s.lanes;
+    return rc;
+}
+
+sdb_status sdb_philox_words(sdb_ctx* ctx, const uint32_t* in, int64_t count, uint32_t* out) {
+    sdb_status rc = utility_prologue(ctx);
+    if (rc != SDB_OK) return rc;
+    if (count <= 0) return SDB_OK;
+    TmpBuf din, dout;
+    SDB_CUDA(ctx, cudaMalloc(&din.p, size_t(count) * 6 * sizeof(uint32_t)));
+    SDB_CUDA(ctx, cudaMalloc(&dout.p, size_t(count) * 4 * sizeof(uint32_t)));
+    SDB_CUDA(ctx, cudaMemcpy(din.p, in, size_t(count) * 6 * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    SDB_CUDA(ctx, sdeb::launch_philox_words(static_cast<uint32_t*>(din.p), count,
+                                            static_cast<uint32_t*>(dout.p), nullptr));
+    SDB_CUDA(ctx, cudaMemcpy(out, dout.p, size_t(count) * 4 * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+    return SDB_OK;
+}
+
+sdb_status sdb_normals(sdb_ctx* ctx, int32_t stream, uint64_t seed, const uint32_t* orbits,
+                       int64_t count, uint32_t chunk, uint32_t step, int32_t m, double* out) {
+    sdb_status rc = utility_prologue(ctx);
+    if (rc != SDB_OK) return rc;
+    if (stream < SDB_STREAM_PHILOX || stream > SDB_STREAM_XOSHIRO256PP)
+        return fail_with(ctx, SDB_ERR_ARGUMENT, "unknown stream %d", stream);
+    if (m < 0) return fail_with(ctx, SDB_ERR_ARGUMENT, "noise count must be >= 0");
+    if (stream == SDB_STREAM_PHILOX && chunk == sdeb::kSamplingTag)
+        return fail_with(ctx, SDB_ERR_ARGUMENT,
+                         "counter word 0x%08X is reserved for sampling streams", chunk);
+    if (count <= 0 || m == 0) return SDB_OK;
+    TmpBuf dorb, dout;
+    SDB_CUDA(ctx, cudaMalloc(&dorb.p, size_t(count) * sizeof(uint32_t)));
+    SDB_CUDA(ctx, cudaMalloc(&dout.p, size_t(count) * m * sizeof(double)));
+    SDB_CUDA(ctx, cudaMemcpy(dorb.p, orbits, size_t(count) * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    SDB_CUDA(ctx, sdeb::launch_normals(stream, seed, static_cast<uint32_t*>(dorb.p), count, chunk,
+                                       step, m, static_cast<double*>(dout.p), nullptr));
+    SDB_CUDA(ctx, cudaMemcpy(out, dout.p, size_t(count) * m * sizeof(double), cudaMemcpyDeviceToHost));
+    return SDB_OK;
+}
+
+sdb_status sdb_stream_raw(sdb_ctx* ctx, int32_t stream, uint64_t seed, uint64_t orbit,
+                          uint64_t block, int64_t count, uint64_t* out) {
+    sdb_status rc = utility_prologue(ctx);
+    if (rc != SDB_OK) return rc;
+    if (stream != SDB_STREAM_SFC64 && stream != SDB_STREAM_XOSHIRO256PP)
+        return fail_with(ctx, SDB_ERR_ARGUMENT, "stream %d has no state", stream);
+    if (count <= 0) return SDB_OK;
+    TmpBuf dout;
+    SDB_CUDA(ctx, cudaMalloc(&dout.p, size_t(count) * sizeof(uint64_t)));
+    SDB_CUDA(ctx, sdeb::launch_stream_raw(stream, seed, orbit, block, count,
+                                          static_cast<uint64_t*>(dout.p), nullptr));
+    SDB_CUDA(ctx, cudaMemcpy(out, dout.p, size_t(count) * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+    return SDB_OK;
+}
+
+sdb_status sdb_sampling_uniforms(sdb_ctx* ctx, uint64_t seed, const uint32_t* orbits,
+                                 int64_t count, int32_t ncols, double* out) {
+    sdb_status rc = utility_prologue(ctx);
+    if (rc != SDB_OK) return rc;
+    if (ncols < 0) return fail_with(ctx, SDB_ERR_ARGUMENT, "count must be >= 0");
+    if (count <= 0 || ncols == 0) return SDB_OK;
+    TmpBuf dorb, dout;
+    SDB_CUDA(ctx, cudaMalloc(&dorb.p, size_t(count) * sizeof(uint32_t)));
+    SDB_CUDA(ctx, cudaMalloc(&dout.p, size_t(count) * ncols * sizeof(double)));
+    SDB_CUDA(ctx, cudaMemcpy(dorb.p, orbits, size_t(count) * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    SDB_CUDA(ctx, sdeb::launch_sampling(seed, static_cast<uint32_t*>(dorb.p), count, ncols,
+                                        static_cast<double*>(dout.p), nullptr));
+    SDB_CUDA(ctx, cudaMemcpy(out, dout.p, size_t(count) * ncols * sizeof(double), cudaMemcpyDeviceToHost));
+    return SDB_OK;
+}
+
+sdb_status sdb_sample_kuramoto(sdb_ctx* ctx, int32_t n, uint64_t seed, const uint32_t* orbits,
+                               int64_t count, double omega_lo, double omega_hi, double noise_lo,
+                               double noise_hi, double coupling, double* init, double* params) {
+    sdb_status rc = utility_prologue(ctx);
+    if (rc != SDB_OK) return rc;
+    if (n < 1) return fail_with(ctx, SDB_ERR_ARGUMENT, "need at least one oscillator");
+    if (count <= 0) return SDB_OK;
+    TmpBuf dorb, dinit, dpar;
+    SDB_CUDA(ctx, cudaMalloc(&dorb.p, size_t(count) * sizeof(uint32_t)));
+    SDB_CUDA(ctx, cudaMalloc(&dinit.p, size_t(count) * n * sizeof(double)));
+    SDB_CUDA(ctx, cudaMalloc(&dpar.p, size_t(count) * (2 * n + 1) * sizeof(double)));
+    SDB_CUDA(ctx, cudaMemcpy(dorb.p, orbits, size_t(count) * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    SDB_CUDA(ctx, sdeb::launch_sample_kuramoto(
+                      n, seed, static_cast<uint32_t*>(dorb.p), count, omega_lo,
+                      omega_hi - omega_lo, noise_lo, noise_hi - noise_lo, coupling,
+                      static_cast<double*>(dinit.p), static_cast<double*>(dpar.p), nullptr));
+    SDB_CUDA(ctx, cudaMemcpy(init, dinit.p, size_t(count) * n * sizeof(double), cudaMemcpyDeviceToHost));
+    SDB_CUDA(ctx, cudaMemcpy(params, dpar.p, size_t(count) * (2 * n + 1) * sizeof(double),
+                             cudaMemcpyDeviceToHost));
+    return SDB_OK;
+}
+
+static sdb_status per_step(sdb_ctx* ctx, int kind_solver, int kind_stream, int32_t n,
+                           int32_t nparams, int32_t nnoise, int32_t coupling, int64_t count,
+                           double dt, const double* y, const double* p, const double* noise,
+                           double* out) {
+    sdb_status rc = utility_prologue(ctx);
+    if (rc != SDB_OK) return rc;
+    if (n < 1 || n > kMaxN) return fail_with(ctx, SDB_ERR_UNSUPPORTED, "nequat=%d unsupported", n);
+    if (nparams < n + 1 || (nnoise > 0 && nparams < 2 * n + 1))
+        return fail_with(ctx, SDB_ERR_ARGUMENT, "nparams=%d does not fit Kuramoto(n=%d)", nparams, n);
+    if (coupling != SDB_COUPLING_MEANFIELD && coupling != SDB_COUPLING_PAIRWISE)
+        return fail_with(ctx, SDB_ERR_ARGUMENT, "unknown coupling %d", coupling);
+    if (count <= 0) return SDB_OK;
+    TmpBuf dy, dp, dn, dout;
+    SDB_CUDA(ctx, cudaMalloc(&dy.p, size_t(count) * n * sizeof(double)));
+    SDB_CUDA(ctx, cudaMalloc(&dp.p, size_t(count) * nparams * sizeof(double)));
+    SDB_CUDA(ctx, cudaMalloc(&dout.p, size_t(count) * n * sizeof(double)));
+    SDB_CUDA(ctx, cudaMemcpy(dy.p, y, size_t(count) * n * sizeof(double), cudaMemcpyHostToDevice));
+    SDB_CUDA(ctx, cudaMemcpy(dp.p, p, size_t(count) * nparams * sizeof(double), cudaMemcpyHostToDevice));
+    if (kind_stream == sdeb::KS_EXPLICIT) {
+        SDB_CUDA(ctx, cudaMalloc(&dn.p, size_t(count) * n * sizeof(double)));
+        SDB_CUDA(ctx, cudaMemcpy(dn.p, noise, size_t(count) * n * sizeof(double), cudaMemcpyHostToDevice));
+    }
+    const int P = next_pow2(n);
+    const int L = std::max(1, P / kMaxJ);
+    sdb_desc d{};
+    d.nequat = n;
+    d.nparams = nparams;
+    d.nnoise = nnoise;
+    d.dt = dt;
+    d.ksteps = 1;
+    d.chunks = 1;
+    d.orbits = count;
+    sdeb::RunArgs a = make_args(d, L);
+    a.state_in = static_cast<double*>(dy.p);
+    a.params = static_cast<double*>(dp.p);
+    a.noise = static_cast<double*>(dn.p);
+    a.values = static_cast<double*>(dout.p);
+    a.vstride = 1;
+    a.check_finite = 0;
+    SDB_CUDA(ctx, launch_run(a, P / L, kind_solver, kind_stream, coupling, nullptr));
+    SDB_CUDA(ctx, cudaMemcpy(out, dout.p, size_t(count) * n * sizeof(double), cudaMemcpyDeviceToHost));
+    return SDB_OK;
+}
+
+sdb_status sdb_drift(sdb_ctx* ctx, int32_t n, int32_t nparams, int32_t coupling, int64_t count,
+                     const double* y, const double* p, double* f) {
+    return per_step(ctx, sdeb::KS_DRIFT, sdeb::KS_NONE, n, nparams, 0, coupling, count, 1.0, y, p,
+                    nullptr, f);
+}
+
+sdb_status sdb_step(sdb_ctx* ctx, int32_t solver, int32_t n, int32_t nparams, int32_t nnoise,
+                    int32_t coupling, int64_t count, double dt, const double* y, const double* p,
+                    const double* noise, double* out) {
+    if (!(dt > 0.0)) return fail_with(ctx, SDB_ERR_ARGUMENT, "dt must be positive");
+    if (solver == SDB_SOLVER_EM && nnoise > 0) {
+        if (!noise) return fail_with(ctx, SDB_ERR_ARGUMENT, "em step needs a noise array");
+        return per_step(ctx, sdeb::KS_EM, sdeb::KS_EXPLICIT, n, nparams, nnoise, coupling, count,
+                        dt, y, p, noise, out);
+    }
+    if (solver == SDB_SOLVER_RK4)
+        return per_step(ctx, sdeb::KS_RK4, sdeb::KS_NONE, n, nparams, 0, coupling, count, dt, y, p,
+                        nullptr, out);
+    if (solver == SDB_SOLVER_EM || solver == SDB_SOLVER_EULER)
+        return per_step(ctx, sdeb::KS_EM, sdeb::KS_NONE, n, nparams, 0, coupling, count, dt, y, p,
+                        nullptr, out);
+    return fail_with(ctx, SDB_ERR_ARGUMENT, "unknown solver %d", solver);
+}
+
+sdb_status sdb_fp64_peak(sdb_ctx* ctx, double* ops_per_s, double* ms_out) {
+    sdb_status rc = utility_prologue(ctx);
+    if (rc != SDB_OK) return rc;
+    int sms = 0;
+    SDB_CUDA(ctx, cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->slots[0].device));
+    const int blocks = sms * 8;  // 8 x 256 threads = 64 warps per SM
+    const int iters = 2000;
+    TmpBuf dout;
+    SDB_CUDA(ctx, cudaMalloc(&dout.p, sizeof(double)));
+    cudaEvent_t e0, e1;
+    SDB_CUDA(ctx, cudaEventCreate(&e0));
+    SDB_CUDA(ctx, cudaEventCreate(&e1));
+    SDB_CUDA(ctx, sdeb::launch_fp64_peak(blocks, iters / 10, static_cast<double*>(dout.p), nullptr));
+    float best = 1e30f;
+    for (int rep = 0; rep < 3; ++rep) {
+        cudaEventRecord(e0, nullptr);
+        sdeb::launch_fp64_peak(blocks, iters, static_cast<double*>(dout.p), nullptr);
+        cudaEventRecord(e1, nullptr);
+        SDB_CUDA(ctx, cudaEventSynchronize(e1));
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, e0, e1);
+        best = std::min(best, ms);
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    SDB_CUDA(ctx, cudaGetLastError());
+    const double ops = double(blocks) * 256.0 * double(iters) * 128.0;
+    if (ops_per_s) *ops_per_s = ops / (double(best) * 1e-3);
+    if (ms_out) *ms_out = best;
+    return SDB_OK;
+}
+
+}  // extern "C"

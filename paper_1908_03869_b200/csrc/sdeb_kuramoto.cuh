@@ -1,0 +1,415 @@
+// Fused Kuramoto ensemble stepper for sm_100a.
+//
+// Replaces the reference's chunk x step loop (engine.py:260-300) with the
+// noise draw (rng.py:150-188), the drift (model.py:188-196), the diffusion
+// (model.py:199-201) and the em/euler/rk4 update (solvers.py:63-88) fused
+// into ONE persistent-per-orbit kernel: state, parameters and stateful RNG
+// words stay in registers for all steps of a launch; HBM sees one read of
+// init/params and one n-vector write per sample.
+//
+// Layout ("lane groups"): each orbit is owned by L = lanes consecutive
+// threads of a warp (L in {1,2,..,32}); lane l owns oscillators
+// [l*J, l*J+J) with L*J = P = next_pow2(n).  Sums over oscillators use ONE
+// canonical binary tree over the P leaves (adjacent leaves first, padding
+// leaves = +0.0): in-lane levels in registers, upper levels by
+// __shfl_xor_sync.  IEEE addition is commutative, so every (L, J) layout
+// produces bit-identical results -- the host may autotune the layout freely
+// (results never depend on it, nor on shard boundaries or GPU count).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <math_constants.h>
+
+#include "sdeb_rng.cuh"
+
+namespace sdeb {
+
+constexpr int kBlock = 128;
+
+enum SolverKind : int { KS_EM = 0, KS_RK4 = 2, KS_DRIFT = 3 };
+// S_NONE: deterministic (euler, or em with nnoise=0); S_EXPLICIT: caller-given noise
+enum StreamKind : int { KS_PHILOX = 0, KS_SFC64 = 1, KS_XOSHIRO = 2, KS_NONE = 3, KS_EXPLICIT = 4 };
+enum CouplingKind : int { KC_MEANFIELD = 0, KC_PAIRWISE = 1 };
+
+struct RunArgs {
+    const double* state_in;   // [orbits][n] state at chunk_begin (init on the first launch)
+    const double* params;     // [orbits][nparams]
+    const double* noise;      // [orbits][n] explicit noise (KS_EXPLICIT) or null
+    double* state_out;        // [orbits][n] state at chunk_end (may be null)
+    double* values;           // sample of chunk c, row r: values[(r*vstride + c-chunk_begin)*n + i]
+    int64_t* fail_step;       // [orbits] first non-finite absolute step or -1 (may be null)
+    uint64_t* rng_state;      // [orbits][nblocks][4] for stateful streams
+    int64_t orbits, orbit_offset, vstride;
+    int64_t ksteps, chunk_begin, chunk_end;
+    uint64_t seed;
+    double dt, sqrt_dt, half_dt, dt6;
+    int n, nparams, nnoise, lanes, log2lanes;
+    int fresh;                // 1: fail=-1 and seed stateful streams in-kernel
+    int check_finite;         // 1: run_batch failure semantics; 0: raw per-step API
+};
+
+__device__ __forceinline__ bool finite_bits(double x) {
+    return (__double2hiint(x) & 0x7ff00000) != 0x7ff00000;
+}
+
+__device__ __forceinline__ int64_t fail_combine(int64_t a, int64_t b) {
+    return a < 0 ? b : (b < 0 ? a : (a < b ? a : b));
+}
+
+// Canonical in-lane tree: level s combines leaves (q, q+s) for q % 2s == 0.
+template <int J>
+__device__ __forceinline__ double lane_tree_sum(double (&v)[J]) {
+#pragma unroll
+    for (int s = 1; s < J; s <<= 1) {
+#pragma unroll
+        for (int q = 0; q + s < J; q += 2 * s) v[q] = __dadd_rn(v[q], v[q + s]);
+    }
+    return v[0];
+}
+
+__device__ __forceinline__ double group_sum(double x, int lanes) {
+    for (int o = 1; o < lanes; o <<= 1) x = __dadd_rn(x, __shfl_xor_sync(0xffffffffu, x, o));
+    return x;
+}
+
+__device__ __forceinline__ int64_t group_fail(int64_t f, int lanes) {
+    for (int o = 1; o < lanes; o <<= 1) {
+        const long long other = __shfl_xor_sync(0xffffffffu, (long long)f, o);
+        f = fail_combine(f, other);
+    }
+    return f;
+}
+
+// ---- drift f_i = omega_i + (K/n) * S_i (model.py:193-196) -----------------
+
+// MEANFIELD: S_i = cos(y_i) * sum_j sin(y_j) - sin(y_i) * sum_j cos(y_j).
+template <int J>
+__device__ __forceinline__ void drift_meanfield(const double (&y)[J], const double (&om)[J],
+                                                double kn, int base, int n, int lanes,
+                                                double (&f)[J]) {
+    double sn[J], cs[J], ts[J], tc[J];
+#pragma unroll
+    for (int q = 0; q < J; ++q) {
+        if (base + q < n) {
+            sincos(y[q], &sn[q], &cs[q]);
+        } else {
+            sn[q] = 0.0;
+            cs[q] = 0.0;
+        }
+        ts[q] = sn[q];
+        tc[q] = cs[q];
+    }
+    double a = lane_tree_sum<J>(ts);
+    double b = lane_tree_sum<J>(tc);
+    a = group_sum(a, lanes);
+    b = group_sum(b, lanes);
+#pragma unroll
+    for (int q = 0; q < J; ++q) {
+        const double s = __fma_rn(cs[q], a, -__dmul_rn(sn[q], b));
+        f[q] = __dadd_rn(om[q], __dmul_rn(kn, s));
+    }
+}
+
+// PAIRWISE: S_i = sum_{j=0}^{n-1} sin(fl(y_j - y_i)), accumulated in j order.
+// The group's state is staged in shared memory sh[q][tid] (conflict-free for
+// the owner).  L == 1 uses the antisymmetric tiling (each unordered pair
+// once: sin(y_i - y_j) = -sin(y_j - y_i), the accumulation order per row
+// stays j-sequential); L > 1 evaluates the full row per lane.
+template <int J>
+__device__ __forceinline__ void drift_pairwise(const double (&y)[J], const double (&om)[J],
+                                               double kn, int base, int n, int lanes,
+                                               double* sh, double* shs, double (&f)[J]) {
+    const int tid = threadIdx.x;
+    const int gbase = tid & ~(lanes - 1);  // first thread of this group in the block
+#pragma unroll
+    for (int q = 0; q < J; ++q) sh[q * kBlock + tid] = y[q];
+    __syncwarp();
+    double s[J];
+    if (lanes == 1) {
+#pragma unroll
+        for (int q = 0; q < J; ++q) shs[q * kBlock + tid] = 0.0;
+        for (int i = 0; i < n; ++i) {
+            const double yi = sh[i * kBlock + tid];
+            double si = shs[i * kBlock + tid];
+            for (int j = i + 1; j < n; ++j) {
+                const double t = sin(__dsub_rn(sh[j * kBlock + tid], yi));
+                si = __dadd_rn(si, t);
+                shs[j * kBlock + tid] = __dadd_rn(shs[j * kBlock + tid], -t);
+            }
+            shs[i * kBlock + tid] = si;
+        }
+#pragma unroll
+        for (int q = 0; q < J; ++q) s[q] = shs[q * kBlock + tid];
+    } else {
+#pragma unroll
+        for (int q = 0; q < J; ++q) s[q] = 0.0;
+        for (int j = 0; j < n; ++j) {
+            const double yj = sh[(j % J) * kBlock + gbase + j / J];
+#pragma unroll
+            for (int q = 0; q < J; ++q) s[q] = __dadd_rn(s[q], sin(__dsub_rn(yj, y[q])));
+        }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int q = 0; q < J; ++q) {
+        f[q] = (base + q < n) ? __dadd_rn(om[q], __dmul_rn(kn, s[q])) : 0.0;
+    }
+}
+
+template <int J, int COUPLING>
+__device__ __forceinline__ void drift(const double (&y)[J], const double (&om)[J], double kn,
+                                      int base, int n, int lanes, double* sh, double* shs,
+                                      double (&f)[J]) {
+    if constexpr (COUPLING == KC_MEANFIELD) {
+        drift_meanfield<J>(y, om, kn, base, n, lanes, f);
+    } else {
+        drift_pairwise<J>(y, om, kn, base, n, lanes, sh, shs, f);
+    }
+}
+
+// ---- noise for one step (rng.py:150-188 / DESIGN.md streams) ---------------
+
+template <int J>
+__host__ __device__ constexpr int blocks_per_lane() {
+    return J >= 4 ? J / 4 : 1;
+}
+
+template <int J, int STREAM>
+__device__ __forceinline__ void step_noise(double (&z)[J], const RunArgs& a, int64_t row,
+                                           uint32_t orbit_g, uint64_t step, int base,
+                                           StreamState (&rs)[blocks_per_lane<J>()]) {
+    if constexpr (STREAM == KS_EXPLICIT) {
+#pragma unroll
+        for (int q = 0; q < J; ++q) z[q] = (base + q < a.n) ? a.noise[row * a.n + base + q] : 0.0;
+    } else {
+        const uint32_t seed_lo = uint32_t(a.seed), seed_hi = uint32_t(a.seed >> 32);
+        const uint32_t step_hi = uint32_t(step >> 32), step_lo = uint32_t(step);
+        const int nn = a.nnoise;
+        if constexpr (J >= 4) {
+#pragma unroll
+            for (int t = 0; t < J / 4; ++t) {
+                const int b = base / 4 + t;
+                double* zz = z + 4 * t;
+                if (4 * b < nn) {
+                    Words4 w;
+                    if constexpr (STREAM == KS_PHILOX) {
+                        w = philox4x32_10(seed_hi, step_hi, step_lo, uint32_t(b), seed_lo, orbit_g);
+                    } else {
+                        w = stream_block<STREAM>(rs[t]);
+                    }
+                    box_muller_pair(w.w0, w.w1, zz[0], zz[1]);
+                    if (4 * b + 2 < nn) {
+                        box_muller_pair(w.w2, w.w3, zz[2], zz[3]);
+                    } else {
+                        zz[2] = 0.0;
+                        zz[3] = 0.0;
+                    }
+                } else {
+                    zz[0] = zz[1] = zz[2] = zz[3] = 0.0;
+                }
+            }
+        } else {
+            // J in {1, 2}: the lane's oscillators sit inside one block shared
+            // with neighbouring lanes; each lane derives the same words.
+            const int b = base / 4;
+            if (base < nn) {
+                Words4 w;
+                if constexpr (STREAM == KS_PHILOX) {
+                    w = philox4x32_10(seed_hi, step_hi, step_lo, uint32_t(b), seed_lo, orbit_g);
+                } else {
+                    w = stream_block<STREAM>(rs[0]);
+                }
+                const bool second = (base >> 1) & 1;
+                const uint32_t wa = second ? w.w2 : w.w0, wb = second ? w.w3 : w.w1;
+                double z0, z1;
+                box_muller_pair(wa, wb, z0, z1);
+                if constexpr (J == 2) {
+                    z[0] = z0;
+                    z[1] = z1;
+                } else {
+                    z[0] = (base & 1) ? z1 : z0;
+                }
+            } else {
+#pragma unroll
+                for (int q = 0; q < J; ++q) z[q] = 0.0;
+            }
+        }
+    }
+}
+
+// ---- the fused run kernel ----------------------------------------------------
+
+template <int J, int SOLVER, int STREAM, int COUPLING>
+__global__ void __launch_bounds__(kBlock) kuramoto_run_kernel(const RunArgs a) {
+    constexpr bool kStochastic = (SOLVER == KS_EM) && (STREAM != KS_NONE);
+    constexpr bool kStateful = kStochastic && (STREAM == KS_SFC64 || STREAM == KS_XOSHIRO);
+    constexpr int NB = blocks_per_lane<J>();
+    extern __shared__ double smem[];
+    double* sh = smem;                  // pairwise: [J][kBlock]
+    double* shs = smem + J * kBlock;    // pairwise L==1: [J][kBlock]
+
+    const int64_t gtid = int64_t(blockIdx.x) * kBlock + threadIdx.x;
+    const int lanes = a.lanes;
+    const int64_t group = gtid >> a.log2lanes;
+    const int lane = int(gtid & (lanes - 1));
+    const bool active = group < a.orbits;
+    const int64_t row = active ? group : a.orbits - 1;  // idle tail groups mirror the last row
+    const int n = a.n;
+    const int base = lane * J;
+    const uint32_t orbit_g = uint32_t(a.orbit_offset + row);
+
+    double y[J], om[J], sg[J];
+    const double* prow = a.params + row * a.nparams;
+    const double kn = __ddiv_rn(__ldg(prow), double(n));  // np.divide(p[...,0:1], float(n))
+#pragma unroll
+    for (int q = 0; q < J; ++q) {
+        const int i = base + q;
+        const bool valid = i < n;
+        y[q] = valid ? a.state_in[row * n + i] : 0.0;
+        om[q] = valid ? __ldg(prow + 1 + i) : 0.0;
+        sg[q] = (kStochastic && valid) ? __ldg(prow + 1 + n + i) : 0.0;
+    }
+
+    if constexpr (SOLVER == KS_DRIFT) {
+        double f[J];
+        drift<J, COUPLING>(y, om, kn, base, n, lanes, sh, shs, f);
+        if (active) {
+#pragma unroll
+            for (int q = 0; q < J; ++q)
+                if (base + q < n) a.values[row * n + base + q] = f[q];
+        }
+        return;
+    } else {
+        int64_t fail = (a.fresh || a.fail_step == nullptr) ? -1 : a.fail_step[row];
+        const int nblocks = (a.nnoise + 3) / 4;
+
+        StreamState rs[NB];
+        if constexpr (kStateful) {
+#pragma unroll
+            for (int t = 0; t < NB; ++t) {
+                const int b = base / 4 + t;
+                if (b < nblocks) {
+                    if (a.fresh) {
+                        rs[t] = stream_init<STREAM>(a.seed, uint64_t(orbit_g), uint64_t(b));
+                    } else {
+                        const uint64_t* p = a.rng_state + (row * nblocks + b) * 4;
+                        rs[t] = StreamState{p[0], p[1], p[2], p[3]};
+                    }
+                } else {
+                    rs[t] = StreamState{0, 0, 0, 0};
+                }
+            }
+        }
+
+        uint64_t step = uint64_t(a.chunk_begin) * uint64_t(a.ksteps);
+        const double dt = a.dt;
+        for (int64_t c = a.chunk_begin; c < a.chunk_end; ++c) {
+            for (int64_t ls = 0; ls < a.ksteps; ++ls, ++step) {
+                if constexpr (SOLVER == KS_EM) {
+                    double f[J];
+                    if constexpr (kStochastic) {
+                        double z[J];
+                        step_noise<J, STREAM>(z, a, row, orbit_g, step, base, rs);
+                        drift<J, COUPLING>(y, om, kn, base, n, lanes, sh, shs, f);
+#pragma unroll
+                        for (int q = 0; q < J; ++q) {
+                            // (y + f*dt) + sqrt(dt) * (s_i * N_i)   (solvers.py:70-71, model.py:201)
+                            const double g = __dmul_rn(sg[q], z[q]);
+                            y[q] = __dadd_rn(__dadd_rn(y[q], __dmul_rn(f[q], dt)),
+                                             __dmul_rn(a.sqrt_dt, g));
+                        }
+                    } else {
+                        drift<J, COUPLING>(y, om, kn, base, n, lanes, sh, shs, f);
+#pragma unroll
+                        for (int q = 0; q < J; ++q) y[q] = __dadd_rn(y[q], __dmul_rn(f[q], dt));
+                    }
+                } else {  // KS_RK4 (solvers.py:80-88)
+                    double k[J], acc[J], ys[J];
+                    drift<J, COUPLING>(y, om, kn, base, n, lanes, sh, shs, k);  // k1
+#pragma unroll
+                    for (int q = 0; q < J; ++q) {
+                        acc[q] = k[q];
+                        ys[q] = __dadd_rn(y[q], __dmul_rn(a.half_dt, k[q]));
+                    }
+                    drift<J, COUPLING>(ys, om, kn, base, n, lanes, sh, shs, k);  // k2
+#pragma unroll
+                    for (int q = 0; q < J; ++q) {
+                        acc[q] = __dadd_rn(acc[q], __dmul_rn(2.0, k[q]));
+                        ys[q] = __dadd_rn(y[q], __dmul_rn(a.half_dt, k[q]));
+                    }
+                    drift<J, COUPLING>(ys, om, kn, base, n, lanes, sh, shs, k);  // k3
+#pragma unroll
+                    for (int q = 0; q < J; ++q) {
+                        acc[q] = __dadd_rn(acc[q], __dmul_rn(2.0, k[q]));
+                        ys[q] = __dadd_rn(y[q], __dmul_rn(dt, k[q]));
+                    }
+                    drift<J, COUPLING>(ys, om, kn, base, n, lanes, sh, shs, k);  // k4
+#pragma unroll
+                    for (int q = 0; q < J; ++q) {
+                        acc[q] = __dadd_rn(acc[q], k[q]);
+                        y[q] = __dadd_rn(y[q], __dmul_rn(a.dt6, acc[q]));
+                    }
+                }
+                // isfinite(y).all(-1) per orbit; first failure recorded, row -> NaN
+                // (engine.py:281-298).  Lanes record independently; the group
+                // minimum is the orbit's first failing step.
+                bool bad = false;
+#pragma unroll
+                for (int q = 0; q < J; ++q) bad |= (base + q < n) && !finite_bits(y[q]);
+                if (bad && a.check_finite) {
+                    if (fail < 0) fail = int64_t(step);
+#pragma unroll
+                    for (int q = 0; q < J; ++q) y[q] = CUDART_NAN;
+                }
+            }
+            // one sample per chunk (engine.py:299)
+            const int64_t gf = group_fail(fail, lanes);
+            if (gf >= 0 && a.check_finite) {
+#pragma unroll
+                for (int q = 0; q < J; ++q) y[q] = CUDART_NAN;
+            }
+            if (active) {
+                double* out = a.values + (row * a.vstride + (c - a.chunk_begin)) * n + base;
+#pragma unroll
+                for (int q = 0; q < J; ++q)
+                    if (base + q < n) out[q] = y[q];
+            }
+        }
+
+        const int64_t gf = group_fail(fail, lanes);
+        if (active) {
+            if (a.state_out != nullptr) {
+#pragma unroll
+                for (int q = 0; q < J; ++q)
+                    if (base + q < n) a.state_out[row * n + base + q] = gf >= 0 ? CUDART_NAN : y[q];
+            }
+            if (a.fail_step != nullptr && lane == 0) a.fail_step[row] = gf;
+            if constexpr (kStateful) {
+                if (base % 4 == 0) {
+#pragma unroll
+                    for (int t = 0; t < NB; ++t) {
+                        const int b = base / 4 + t;
+                        if (b < nblocks) {
+                            uint64_t* p = a.rng_state + (row * nblocks + b) * 4;
+                            p[0] = rs[t].s0;
+                            p[1] = rs[t].s1;
+                            p[2] = rs[t].s2;
+                            p[3] = rs[t].s3;
+                        }
+                    }
+                }
+            }
+        }
+    }
+}
+
+// Host-side dispatch (sdeb_kuramoto_j*.cu instantiate per J).
+template <int J>
+cudaError_t launch_kuramoto_j(const RunArgs& a, int solver, int stream, int coupling,
+                              cudaStream_t st);
+
+inline size_t pairwise_smem_bytes(int J, int coupling) {
+    return coupling == KC_PAIRWISE ? size_t(2) * J * kBlock * sizeof(double) : 0;
+}
+
+}  // namespace sdeb
