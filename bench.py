@@ -208,6 +208,16 @@ def reduce_max(dist, value: float) -> float:
     return float(t.item())
 
 
+def reduce_max_cpu(dist, value: float) -> float:
+    """Max over ranks on the host (gloo) -- same reduction as reduce_max."""
+    if dist is None:
+        return value
+    import torch
+    t = torch.tensor([value], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def barrier(dist):
     if dist is not None:
         dist.barrier()
@@ -350,12 +360,12 @@ def run_ours(args, w, world, rank, local, dist):
 
     # --- e2e through the public API (host numpy buffers) ---
     host_batch = sdb.OrbitBatch(init=batch.init.copy(), params=batch.params.copy())
-    sdb.run_batch(model, cfg, host_batch)  # warm (autotune cache, pageable staging)
+    sdb.run_batch(model, cfg, host_batch, orbit_offset=offset)  # warm (autotune cache, pageable staging)
     barrier(dist)
     t0 = time.perf_counter()
     e2e_steps = max(1, min(args.steps, 5))
     for _ in range(e2e_steps):
-        store = sdb.run_batch(model, cfg, host_batch)
+        store = sdb.run_batch(model, cfg, host_batch, orbit_offset=offset)
     e2e_s = reduce_max(dist, time.perf_counter() - t0) / e2e_steps
     h2d = batch.init.nbytes + batch.params.nbytes
     d2h = m * chunks * n * 8 + m * 8

@@ -105,7 +105,9 @@ __device__ __forceinline__ void drift_meanfield(const double (&y)[J], const doub
     b = group_sum(b, lanes);
 #pragma unroll
     for (int q = 0; q < J; ++q) {
-        const double s = __fma_rn(cs[q], a, -__dmul_rn(sn[q], b));
+        // two rounded products, not an FMA: the self term cos*sin - sin*cos
+        // then cancels exactly (n=1 gives f == omega, like sin(0) == 0)
+        const double s = __dsub_rn(__dmul_rn(cs[q], a), __dmul_rn(sn[q], b));
         f[q] = __dadd_rn(om[q], __dmul_rn(kn, s));
     }
 }

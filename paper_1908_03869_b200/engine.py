@@ -22,6 +22,7 @@ New, optional fields on EngineConfig (defaults keep reference behaviour):
 
 from __future__ import annotations
 
+import dataclasses
 import math
 import os
 from dataclasses import dataclass, field
@@ -34,7 +35,7 @@ from .solvers import get_solver
 
 __all__ = [
     "ConfigError", "EngineConfig", "TrajectoryStore", "OrbitFailure",
-    "iteration_count", "partition_orbits", "run_batch",
+    "iteration_count", "partition_orbits", "run_batch", "shard_bounds", "run_batch_sharded",
 ]
 
 _MASK32 = 0xFFFFFFFF
@@ -209,16 +210,32 @@ def failures_from_steps(fail_step: np.ndarray, ksteps: int, dt: float,
     return out
 
 
-def run_batch(model: ModelSpec, config: EngineConfig, batch: OrbitBatch) -> TrajectoryStore:
+def shard_bounds(orbits: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous shard [r*M/W, (r+1)*M/W) of rank r -- the same split sdb_run
+    uses across the devices of one context."""
+    if world < 1 or not 0 <= rank < world:
+        raise ConfigError("bad shard rank %r of world %r" % (rank, world))
+    return rank * orbits // world, (rank + 1) * orbits // world
+
+
+def run_batch(model: ModelSpec, config: EngineConfig, batch: OrbitBatch, *,
+              orbit_offset: int = 0) -> TrajectoryStore:
     """Integrate every orbit of the batch on the GPU and sample once per chunk
     (engine.py:221-314).  Validation happens before any device allocation,
-    in the reference's order."""
+    in the reference's order.
+
+    ``orbit_offset`` (keyword, default 0 = the reference's numbering) is the
+    global id of row 0: noise is keyed by global id and failures report it, so
+    a shard of a larger batch integrates exactly as those rows of the whole.
+    """
     batch.check_against(model)
     if batch.orbits != config.orbits:
         raise ConfigError("config says %d orbits but batch has %d"
                           % (config.orbits, batch.orbits))
     if batch.orbits > _MASK32:
         raise ConfigError("orbit count must fit in 32 bits")
+    if orbit_offset < 0 or orbit_offset + batch.orbits > _MASK32 + 1:
+        raise ConfigError("global orbit ids must fit in 32 bits")
     chunks = iteration_count(config.tspan, config.dt, config.ksteps, pad=config.pad)
     if chunks * config.ksteps >= 2 ** 63:
         raise ConfigError("total step count does not fit in 63 bits")
@@ -231,7 +248,7 @@ def run_batch(model: ModelSpec, config: EngineConfig, batch: OrbitBatch) -> Traj
             "above the configured cap of %d"
             % (store_bytes, batch.orbits, samples, model.nequat, config.max_store_bytes))
     _check_stepper(model, config)
-    desc = make_desc(model, config, chunks, batch.orbits)
+    desc = make_desc(model, config, chunks, batch.orbits, orbit_offset)
 
     sample_dt = config.ksteps * config.dt
     times = np.arange(samples, dtype=np.float64) * sample_dt
@@ -242,8 +259,31 @@ def run_batch(model: ModelSpec, config: EngineConfig, batch: OrbitBatch) -> Traj
     ctx = nat.context(config.devices)
     nat.check(nat.lib().sdb_run(ctx, desc, nat.dptr(init), nat.dptr(params), nat.dptr(values),
                                 nat.i64ptr(fail_step)), ctx, "sdb_run")
-    failures = failures_from_steps(fail_step, config.ksteps, config.dt)
+    failures = failures_from_steps(fail_step, config.ksteps, config.dt, orbit_offset)
     return TrajectoryStore(times=times, values=values, model_name=model.name,
+                           config=config, failures=failures)
+
+
+def run_batch_sharded(model: ModelSpec, config: EngineConfig, batch: OrbitBatch, *,
+                      world: int, rank: int, devices=None, gather=None) -> TrajectoryStore:
+    """Multi-process form (one process per GPU, e.g. under torchrun): rank r
+    integrates rows shard_bounds(M, world, r) of ``batch`` on its device(s)
+    with their global orbit ids.  There is no collective on the data path;
+    ``gather`` (e.g. a torch.distributed all_gather_object wrapper) may
+    assemble the full store on the host afterwards.  The assembled store is
+    bit-identical to a single-process run (noise is keyed by global id)."""
+    lo, hi = shard_bounds(batch.orbits, world, rank)
+    part = OrbitBatch(init=batch.init[lo:hi], params=batch.params[lo:hi])
+    cfg = dataclasses.replace(config, orbits=hi - lo,
+                              devices=devices if devices is not None else config.devices)
+    store = run_batch(model, cfg, part, orbit_offset=lo)
+    if gather is None:
+        return store
+    parts = gather((lo, store.values, store.failures))
+    parts.sort(key=lambda t: t[0])
+    values = np.concatenate([p[1] for p in parts], axis=0)
+    failures = sorted((f for p in parts for f in p[2]), key=lambda f: f.orbit)
+    return TrajectoryStore(times=store.times, values=values, model_name=model.name,
                            config=config, failures=failures)
 
 
