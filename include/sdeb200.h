@@ -149,6 +149,12 @@ sdb_status sdb_step(sdb_ctx* ctx, int32_t solver, int32_t n, int32_t nparams, in
  * roofline denominator bench.py reports (MEASURED_PEAKS.json has no FP64 figure). */
 sdb_status sdb_fp64_peak(sdb_ctx* ctx, double* ops_per_s, double* ms);
 
+/* Evaluate one of the stepper's device math routines element-wise (accuracy
+ * tests): func 0 = sin, 1 = cos (the stepper's sincos), 2 = log (Box-Muller
+ * radius), 3 = sqrt, 4 = sin / 5 = cos / 6 = log of libdevice for comparison. */
+sdb_status sdb_math_probe(sdb_ctx* ctx, int32_t func, const double* x, int64_t count,
+                          double* out);
+
 #ifdef __cplusplus
 }
 #endif

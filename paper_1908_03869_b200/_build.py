@@ -21,7 +21,7 @@ OBJ = os.path.join(PKG, "_obj")
 LIB = os.path.join(PKG, "libsdeb200.so")
 
 SOURCES = ["sdeb_capi.cu", "sdeb_misc.cu"] + ["sdeb_kuramoto_j%d.cu" % j for j in (1, 2, 4, 8, 16)]
-HEADERS = ["sdeb_kuramoto.cuh", "sdeb_kuramoto_inst.cuh", "sdeb_rng.cuh", "sdeb_misc.h"]
+HEADERS = sorted(f for f in os.listdir(CSRC) if f.endswith((".cuh", ".h")))
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",

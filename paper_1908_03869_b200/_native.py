@@ -69,6 +69,8 @@ SIGNATURES = {
     "sdb_drift": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
                                  ctypes.c_int64, _c_double_p, _c_double_p, _c_double_p]),
     "sdb_fp64_peak": (ctypes.c_int, [ctypes.c_void_p, _c_double_p, _c_double_p]),
+    "sdb_math_probe": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, _c_double_p,
+                                      ctypes.c_int64, _c_double_p]),
     "sdb_step": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
                                 ctypes.c_int32, ctypes.c_int32, ctypes.c_int64, ctypes.c_double,
                                 _c_double_p, _c_double_p, _c_double_p, _c_double_p]),

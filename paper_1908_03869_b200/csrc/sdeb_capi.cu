@@ -677,4 +677,20 @@ sdb_status sdb_fp64_peak(sdb_ctx* ctx, double* ops_per_s, double* ms_out) {
     return SDB_OK;
 }
 
+sdb_status sdb_math_probe(sdb_ctx* ctx, int32_t func, const double* x, int64_t count,
+                          double* out) {
+    sdb_status rc = utility_prologue(ctx);
+    if (rc != SDB_OK) return rc;
+    if (func < 0 || func > 6) return fail_with(ctx, SDB_ERR_ARGUMENT, "unknown math probe %d", func);
+    if (count <= 0) return SDB_OK;
+    TmpBuf dx, dout;
+    SDB_CUDA(ctx, cudaMalloc(&dx.p, size_t(count) * sizeof(double)));
+    SDB_CUDA(ctx, cudaMalloc(&dout.p, size_t(count) * sizeof(double)));
+    SDB_CUDA(ctx, cudaMemcpy(dx.p, x, size_t(count) * sizeof(double), cudaMemcpyHostToDevice));
+    SDB_CUDA(ctx, sdeb::launch_math_probe(func, static_cast<double*>(dx.p), count,
+                                          static_cast<double*>(dout.p), nullptr));
+    SDB_CUDA(ctx, cudaMemcpy(out, dout.p, size_t(count) * sizeof(double), cudaMemcpyDeviceToHost));
+    return SDB_OK;
+}
+
 }  // extern "C"

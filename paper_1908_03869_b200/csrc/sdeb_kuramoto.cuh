@@ -87,12 +87,13 @@ template <int J>
 __device__ __forceinline__ void drift_meanfield(const double (&y)[J], const double (&om)[J],
                                                 double kn, int base, int n, int lanes,
                                                 double (&f)[J]) {
-    double sn[J], cs[J], ts[J], tc[J];
+    double sn[J], cs[J], ts[J], tc[J], x[J];
+#pragma unroll
+    for (int q = 0; q < J; ++q) x[q] = (base + q < n) ? y[q] : 0.0;
+    sincos_vec<J>(x, sn, cs);
 #pragma unroll
     for (int q = 0; q < J; ++q) {
-        if (base + q < n) {
-            sincos(y[q], &sn[q], &cs[q]);
-        } else {
+        if (base + q >= n) {
             sn[q] = 0.0;
             cs[q] = 0.0;
         }
@@ -134,7 +135,8 @@ __device__ __forceinline__ void drift_pairwise(const double (&y)[J], const doubl
             const double yi = sh[i * kBlock + tid];
             double si = shs[i * kBlock + tid];
             for (int j = i + 1; j < n; ++j) {
-                const double t = sin(__dsub_rn(sh[j * kBlock + tid], yi));
+                double t, unused;
+                sincos_any(__dsub_rn(sh[j * kBlock + tid], yi), t, unused);
                 si = __dadd_rn(si, t);
                 shs[j * kBlock + tid] = __dadd_rn(shs[j * kBlock + tid], -t);
             }
@@ -148,7 +150,11 @@ __device__ __forceinline__ void drift_pairwise(const double (&y)[J], const doubl
         for (int j = 0; j < n; ++j) {
             const double yj = sh[(j % J) * kBlock + gbase + j / J];
 #pragma unroll
-            for (int q = 0; q < J; ++q) s[q] = __dadd_rn(s[q], sin(__dsub_rn(yj, y[q])));
+            for (int q = 0; q < J; ++q) {
+                double t, unused;
+                sincos_any(__dsub_rn(yj, y[q]), t, unused);
+                s[q] = __dadd_rn(s[q], t);
+            }
         }
     }
     __syncwarp();

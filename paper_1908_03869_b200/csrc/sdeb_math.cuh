@@ -1,0 +1,173 @@
+// Branch-free FP64 sincos / log / sqrt for the stepper (sm_100a).
+//
+// Why: ncu on the v1 kernel (profiles/r01/SUMMARY_v1.md) showed the fused
+// stepper ISSUE-bound, not FP64-bound: libdevice's sincos/log/sqrt spend
+// F2I/I2F.F64 round trips (XU pipe), BSSY/BSYNC-guarded slow paths and
+// re-materialised 64-bit constants around ~60 FP64 ops per oscillator-step.
+// These versions keep the FP64 work (~20 ops per sincos, ~12 per log) and
+// drop almost everything else:
+//   - round-to-nearest quadrant by the 1.5*2^52 magic add (no F2I/I2F; the
+//     quadrant is the low word of the sum);
+//   - 3-part Cody-Waite pi/2 reduction with FMA (exact first step);
+//   - fdlibm __kernel_sin/__kernel_cos minimax coefficients on [-pi/4, pi/4];
+//   - quadrant rotation by integer select + sign-bit xor on the high word;
+//   - log: 128-entry (1/c, -ln(1/c)) table (sdeb_log_table.cuh, generated
+//     with 60-digit decimal arithmetic) + degree-8 log1p polynomial;
+//   - sqrt: MUFU.RSQ64H seed + one Goldschmidt step + Markstein correction.
+// Accuracy (tests/test_gpu_math.py): sincos/log/sqrt within 2 ulp of
+// numpy/glibc on the argument ranges the stepper uses.  sin is bitwise odd
+// and cos even, which the antisymmetric pairwise tiling relies on.
+// |x| >= 2^29 falls back to libdevice sincos (exact Payne-Hanek reduction).
+#pragma once
+#include <cstdint>
+
+#include "sdeb_log_table.cuh"
+
+namespace sdeb {
+
+// Polynomial coefficients and reduction constants live in the constant bank:
+// DFMA cannot encode a full 64-bit immediate, and as literals ptxas
+// re-materialised each one with two UMOVs per use inside the step loop
+// (~220 issue slots per iteration in the v2 SASS); from c[] one LDCU.128
+// fetches two.  Values that fit a 32-bit high-word immediate (0.5, 1.0,
+// 1.5*2^52, ...) stay literals.
+enum MathConst : int {
+    MC_S1, MC_S2, MC_S3, MC_S4, MC_S5, MC_S6,  // fdlibm k_sin.c (|r| <= pi/4)
+    MC_C1, MC_C2, MC_C3, MC_C4, MC_C5, MC_C6,  // fdlibm k_cos.c
+    MC_TWO_OVER_PI, MC_PIO2_1, MC_PIO2_2, MC_PIO2_3,
+    MC_LN2_HI, MC_LN2_LO, MC_U32_BIAS, MC_INV7, MC_NEG_INV6, MC_INV5, MC_INV3,
+    MC_COUNT
+};
+
+__constant__ static double kMC[MC_COUNT] = {  // non-const: keeps ptxas from folding them back into UMOV pairs
+    -1.66666666666666324348e-01, 8.33333333332248946124e-03, -1.98412698298579493134e-04,
+    2.75573137070700676789e-06, -2.50507602534068634195e-08, 1.58969099521155010221e-10,
+    4.16666666666666019037e-02, -1.38888888888741095749e-03, 2.48015872894767294178e-05,
+    -2.75573143513906633035e-07, 2.08757232129817482790e-09, -1.13596475577881948265e-11,
+    6.36619772367581382433e-01,  // 2/pi
+    1.5707963267948966,          // fl(pi/2)
+    6.123233995736766e-17,       // fl(pi/2 - fl(pi/2))
+    -1.4973849048591698e-33,     // next 53 bits of pi/2
+    6.93147180559945286227e-01,  // fl(ln 2)
+    2.31904681384629955842e-17,  // fl(ln 2 - fl(ln 2))
+    1048576.0 - 2.3283064365386963e-10,  // 2^20 - 2^-32 (exact)
+    0.14285714285714285, -0.16666666666666666, 0.2, 0.3333333333333333,
+};
+
+constexpr double kRoundMagic = 6755399441055744.0;  // 1.5 * 2^52
+constexpr double kSmallArg = 536870912.0;           // 2^29: fast reduction bound
+
+// (w + 1) * 2^-32 (rng.py:121-129) in ONE exact DADD, no I2F conversion.
+__device__ __forceinline__ double u32_to_uniform(uint32_t w) {
+    return __dsub_rn(__hiloint2double(0x41300000, int(w)), kMC[MC_U32_BIAS]);
+}
+
+// w * 2^-32 (rng.py:221, sampling uniforms) in one exact DADD.
+__device__ __forceinline__ double u32_to_unit(uint32_t w) {
+    return __dsub_rn(__hiloint2double(0x41300000, int(w)), 1048576.0);
+}
+
+// sin / cos of r in [-pi/4, pi/4] (slightly beyond is fine), rotated by q*pi/2.
+__device__ __forceinline__ void sincos_reduced(double r, int q, double& s, double& c) {
+    const double r2 = __dmul_rn(r, r);
+    double ps = __fma_rn(r2, kMC[MC_S6], kMC[MC_S5]);
+    ps = __fma_rn(r2, ps, kMC[MC_S4]);
+    ps = __fma_rn(r2, ps, kMC[MC_S3]);
+    ps = __fma_rn(r2, ps, kMC[MC_S2]);
+    ps = __fma_rn(r2, ps, kMC[MC_S1]);
+    const double sr = __fma_rn(__dmul_rn(r2, r), ps, r);
+    double pc = __fma_rn(r2, kMC[MC_C6], kMC[MC_C5]);
+    pc = __fma_rn(r2, pc, kMC[MC_C4]);
+    pc = __fma_rn(r2, pc, kMC[MC_C3]);
+    pc = __fma_rn(r2, pc, kMC[MC_C2]);
+    pc = __fma_rn(r2, pc, kMC[MC_C1]);
+    const double cr = __fma_rn(__dmul_rn(r2, r2), pc, __fma_rn(r2, -0.5, 1.0));
+    const bool swap = (q & 1) != 0;
+    const double so = swap ? cr : sr;
+    const double co = swap ? sr : cr;
+    const int ssign = (q & 2) << 30;        // sin < 0 in quadrants 2, 3
+    const int csign = ((q + 1) & 2) << 30;  // cos < 0 in quadrants 1, 2
+    s = __hiloint2double(__double2hiint(so) ^ ssign, __double2loint(so));
+    c = __hiloint2double(__double2hiint(co) ^ csign, __double2loint(co));
+}
+
+// |x| < 2^29 (or NaN/inf -> NaN through the arithmetic).
+__device__ __forceinline__ void sincos_small(double x, double& s, double& c) {
+    const double t = __fma_rn(x, kMC[MC_TWO_OVER_PI], kRoundMagic);
+    const int q = __double2loint(t);
+    const double qd = __dsub_rn(t, kRoundMagic);
+    double r = __fma_rn(-qd, kMC[MC_PIO2_1], x);  // exact for |q| < 2^29
+    r = __fma_rn(-qd, kMC[MC_PIO2_2], r);
+    r = __fma_rn(-qd, kMC[MC_PIO2_3], r);
+    sincos_reduced(r, q, s, c);
+}
+
+// |x| >= 2^29, inf or NaN -- integer test on the high word (ALU, not FP64).
+__device__ __forceinline__ bool big_arg(double x) {
+    return (__double2hiint(x) & 0x7fffffff) >= 0x41C00000;
+}
+
+// Any argument: unwrapped phases beyond 2^29 take libdevice's exact reduction.
+__device__ __forceinline__ void sincos_any(double x, double& s, double& c) {
+    if (!big_arg(x)) {
+        sincos_small(x, s, c);
+    } else {
+        sincos(x, &s, &c);
+    }
+}
+
+// J values at once: ONE branch per call site; the fast path carries no
+// per-element slow-path code (the stepper's phases are almost never huge).
+template <int J>
+__device__ __forceinline__ void sincos_vec(const double (&x)[J], double (&s)[J], double (&c)[J]) {
+    bool big = false;
+#pragma unroll
+    for (int q = 0; q < J; ++q) big |= big_arg(x[q]);
+    if (!big) {
+#pragma unroll
+        for (int q = 0; q < J; ++q) sincos_small(x[q], s[q], c[q]);
+    } else {
+#pragma unroll
+        for (int q = 0; q < J; ++q) sincos(x[q], &s[q], &c[q]);
+    }
+}
+
+// ln(x) for a positive normal double.
+__device__ __forceinline__ double log_pos(double x) {
+    const uint64_t ix = uint64_t(__double_as_longlong(x));
+    const uint64_t tmp = ix - kLogOff;
+    const int i = int((tmp >> (52 - kLogTableBits)) & ((1u << kLogTableBits) - 1));
+    const int64_t k = int64_t(tmp) >> 52;
+    const double z = __longlong_as_double((long long)(ix - (tmp & (0xFFFull << 52))));
+    const double2 e = __ldg(reinterpret_cast<const double2*>(kLogTable[i]));  // (invc, logc)
+    const double r = __fma_rn(z, e.x, -1.0);
+    const double kd = __dsub_rn(__longlong_as_double((long long)(0x4338000000000000ll + k)),
+                                kRoundMagic);
+    // log1p(r) = r - r^2/2 + r^3/3 - ... - r^8/8, |r| < 2^-7
+    double p = __fma_rn(r, -0.125, kMC[MC_INV7]);
+    p = __fma_rn(r, p, kMC[MC_NEG_INV6]);
+    p = __fma_rn(r, p, kMC[MC_INV5]);
+    p = __fma_rn(r, p, -0.25);
+    p = __fma_rn(r, p, kMC[MC_INV3]);
+    p = __fma_rn(r, p, -0.5);
+    const double lp = __fma_rn(__dmul_rn(r, r), p, r);
+    const double hi = __fma_rn(kd, kMC[MC_LN2_HI], e.y);
+    const double lo = __fma_rn(kd, kMC[MC_LN2_LO], lp);
+    return __dadd_rn(hi, lo);
+}
+
+// sqrt(x) for x >= 0 (x == 0 -> 0).
+__device__ __forceinline__ double sqrt_nonneg(double x) {
+    double r;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    double g = __dmul_rn(x, r);
+    double h = __dmul_rn(0.5, r);
+    const double d = __fma_rn(-g, h, 0.5);
+    g = __fma_rn(g, d, g);
+    h = __fma_rn(h, d, h);
+    const double e = __fma_rn(-g, g, x);
+    g = __fma_rn(e, h, g);
+    return x > 0.0 ? g : x;
+}
+
+}  // namespace sdeb

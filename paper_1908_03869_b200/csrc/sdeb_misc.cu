@@ -135,7 +135,32 @@ cudaError_t launch_fp64_peak(int blocks, int iters, double* out, cudaStream_t st
     return cudaGetLastError();
 }
 
+__global__ void math_probe_kernel(int func, const double* __restrict__ x, int64_t count,
+                                  double* __restrict__ out) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    const double v = x[i];
+    double s, c, r = 0.0;
+    switch (func) {
+        case 0: sincos_any(v, s, c); r = s; break;
+        case 1: sincos_any(v, s, c); r = c; break;
+        case 2: r = log_pos(v); break;
+        case 3: r = sqrt_nonneg(v); break;
+        case 4: r = sin(v); break;
+        case 5: r = cos(v); break;
+        case 6: r = log(v); break;
+        default: r = CUDART_NAN;
+    }
+    out[i] = r;
+}
+
 static unsigned grid_for(int64_t items, int block) { return unsigned((items + block - 1) / block); }
+
+cudaError_t launch_math_probe(int func, const double* x, int64_t count, double* out,
+                              cudaStream_t st) {
+    math_probe_kernel<<<grid_for(count, 256), 256, 0, st>>>(func, x, count, out);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_philox_words(const uint32_t* in, int64_t count, uint32_t* out, cudaStream_t st) {
     philox_words_kernel<<<grid_for(count, 256), 256, 0, st>>>(in, count, out);

@@ -20,5 +20,7 @@ cudaError_t launch_sample_kuramoto(int n, uint64_t seed, const uint32_t* orbits,
 
 // FP64 DFMA-throughput probe: blocks x 256 threads x iters x 128 DFMA.
 cudaError_t launch_fp64_peak(int blocks, int iters, double* out, cudaStream_t st);
+cudaError_t launch_math_probe(int func, const double* x, int64_t count, double* out,
+                              cudaStream_t st);
 
 }  // namespace sdeb
