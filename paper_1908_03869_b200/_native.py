@@ -54,6 +54,8 @@ SIGNATURES = {
                                       ctypes.c_void_p]),
     "sdb_last_launch_count": (ctypes.c_int64, [ctypes.c_void_p]),
     "sdb_last_lanes": (ctypes.c_int32, [ctypes.c_void_p]),
+    "sdb_last_layout": (None, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int32),
+                               ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32)]),
     "sdb_philox_words": (ctypes.c_int, [ctypes.c_void_p, _c_u32_p, ctypes.c_int64, _c_u32_p]),
     "sdb_normals": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_uint64, _c_u32_p,
                                    ctypes.c_int64, ctypes.c_uint32, ctypes.c_uint32,

@@ -10,6 +10,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
@@ -62,10 +63,21 @@ struct Slot {
     DevBuf t_values, t_state, t_fail, t_rng;  // autotune scratch
     int64_t launches = 0;
     int32_t lanes = 0;
+    int32_t tight = 0;
+    int32_t ctas_per_sm = 0;
     std::string error;
 };
 
-using TuneKey = std::tuple<int, int, int, int, int, int64_t, int>;
+// One launch layout: lanes per orbit, register-capped variant, dynamic
+// shared memory used to cap resident CTAs per SM (wave shaping).
+struct Layout {
+    int lanes = 0;
+    int tight = 0;
+    int smem = 0;
+    int ctas_per_sm = 0;
+};
+
+using TuneKey = std::tuple<int, int, int, int, int, int64_t, int, int>;
 
 }  // namespace
 
@@ -74,7 +86,9 @@ struct sdb_ctx {
     std::string error;
     int64_t launches = 0;
     int32_t last_lanes = 0;
-    std::map<TuneKey, int> tune;
+    int32_t last_tight = 0;
+    int32_t last_ctas_per_sm = 0;
+    std::map<TuneKey, Layout> tune;
 };
 
 namespace {
@@ -114,15 +128,31 @@ int ilog2(int x) {
 }
 
 cudaError_t launch_run(const sdeb::RunArgs& a, int J, int solver, int stream, int coupling,
-                       cudaStream_t st) {
+                       int tight, cudaStream_t st) {
     switch (J) {
-        case 1: return sdeb::launch_kuramoto_j<1>(a, solver, stream, coupling, st);
-        case 2: return sdeb::launch_kuramoto_j<2>(a, solver, stream, coupling, st);
-        case 4: return sdeb::launch_kuramoto_j<4>(a, solver, stream, coupling, st);
-        case 8: return sdeb::launch_kuramoto_j<8>(a, solver, stream, coupling, st);
-        case 16: return sdeb::launch_kuramoto_j<16>(a, solver, stream, coupling, st);
+        case 1: return sdeb::launch_kuramoto_j<1>(a, solver, stream, coupling, tight, st);
+        case 2: return sdeb::launch_kuramoto_j<2>(a, solver, stream, coupling, tight, st);
+        case 4: return sdeb::launch_kuramoto_j<4>(a, solver, stream, coupling, tight, st);
+        case 8: return sdeb::launch_kuramoto_j<8>(a, solver, stream, coupling, tight, st);
+        case 16: return sdeb::launch_kuramoto_j<16>(a, solver, stream, coupling, tight, st);
         default: return cudaErrorInvalidValue;
     }
+}
+
+cudaError_t occupancy_run(int J, int solver, int stream, int coupling, int tight, size_t smem,
+                          int* blocks) {
+    switch (J) {
+        case 1: return sdeb::occupancy_kuramoto_j<1>(solver, stream, coupling, tight, smem, blocks);
+        case 2: return sdeb::occupancy_kuramoto_j<2>(solver, stream, coupling, tight, smem, blocks);
+        case 4: return sdeb::occupancy_kuramoto_j<4>(solver, stream, coupling, tight, smem, blocks);
+        case 8: return sdeb::occupancy_kuramoto_j<8>(solver, stream, coupling, tight, smem, blocks);
+        case 16: return sdeb::occupancy_kuramoto_j<16>(solver, stream, coupling, tight, smem, blocks);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+int tight_minb_of(int J) {
+    return J == 4 ? sdeb::tight_minb<4>() : (J == 8 ? sdeb::tight_minb<8>() : 1);
 }
 
 // Kernel kind for a validated descriptor.
@@ -220,28 +250,88 @@ size_t rng_words(const sdb_desc& d, int64_t rows) {
     return stateful ? size_t(rows) * size_t((d.nnoise + 3) / 4) * 4 : 0;
 }
 
-// Pick lanes-per-orbit: explicit, cached, or timed on a short probe into
-// scratch buffers.  Every layout gives bit-identical results (canonical
-// summation tree), so this only affects speed.
-sdb_status choose_lanes(sdb_ctx* ctx, Slot& s, const sdb_desc& d, const double* d_init,
-                        const double* d_params, cudaStream_t st, int* lanes_out) {
+// Shared memory that caps a kernel at `cap` resident CTAs per SM.
+int smem_for_cap(int device, int cap) {
+    int per_sm = 0;
+    cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device);
+    const int reserved = 1024;  // per-CTA reservation on sm_100
+    return std::max(0, per_sm / cap - reserved) & ~255;
+}
+
+// Candidate layouts: every lanes-per-orbit, the register-capped variant where
+// one exists, and CTA-per-SM caps below the natural occupancy (waves shaped so
+// the last one is not mostly idle).
+sdb_status candidate_layouts(sdb_ctx* ctx, const Slot& s, const sdb_desc& d, int kind_solver,
+                             int kind_stream, std::vector<Layout>* out) {
+    const int P = next_pow2(d.nequat);
+    int sms = 0;
+    SDB_CUDA(ctx, cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s.device));
+    std::vector<int> lanes_list;
     if (d.lanes != 0) {
-        *lanes_out = d.lanes;
-        return SDB_OK;
+        lanes_list.push_back(d.lanes);
+    } else {
+        for (int L : candidate_lanes(d.nequat)) lanes_list.push_back(L);
     }
-    std::vector<int> cands = candidate_lanes(d.nequat);
-    if (cands.size() == 1) {
-        *lanes_out = cands[0];
-        return SDB_OK;
+    for (int L : lanes_list) {
+        const int J = P / L;
+        const int tights = (d.coupling == SDB_COUPLING_MEANFIELD && tight_minb_of(J) > 1) ? 2 : 1;
+        for (int t = 0; t < tights; ++t) {
+            int occ = 0;
+            SDB_CUDA(ctx, occupancy_run(J, kind_solver, kind_stream, d.coupling, t, 0, &occ));
+            if (occ < 1) continue;
+            const int64_t ctas = (d.orbits * L + sdeb::kBlock - 1) / sdeb::kBlock;
+            out->push_back(Layout{L, t, 0, occ});
+            // caps that turn a ragged last wave into full ones
+            for (int cap = occ - 1; cap >= 1 && cap >= occ - 4; --cap) {
+                const double waves_cap = double(ctas) / (double(sms) * cap);
+                const double waves_occ = double(ctas) / (double(sms) * occ);
+                const double eff_cap = waves_cap / std::ceil(waves_cap);
+                const double eff_occ = waves_occ / std::ceil(waves_occ);
+                if (eff_cap <= eff_occ + 0.02) continue;
+                const int smem = smem_for_cap(s.device, cap);
+                int got = 0;
+                SDB_CUDA(ctx, occupancy_run(J, kind_solver, kind_stream, d.coupling, t,
+                                            size_t(smem), &got));
+                if (got == cap) out->push_back(Layout{L, t, smem, cap});
+            }
+        }
     }
+    return SDB_OK;
+}
+
+// Pick the launch layout: cached, single candidate, or timed on a short probe
+// into scratch buffers.  Every layout gives bit-identical results (canonical
+// summation tree), so this only affects speed.
+sdb_status choose_layout(sdb_ctx* ctx, Slot& s, const sdb_desc& d, const double* d_init,
+                         const double* d_params, cudaStream_t st, Layout* out) {
     int kind_solver, kind_stream;
     kernel_kind(d, &kind_solver, &kind_stream);
     const int64_t total = d.chunks * d.ksteps;
     const TuneKey key{s.device, d.nequat, kind_solver, kind_stream, d.coupling, d.orbits,
-                      int(std::min<int64_t>(total, 1 << 20))};
+                      int(std::min<int64_t>(total, 1 << 20)), d.lanes};
     auto it = ctx->tune.find(key);
     if (it != ctx->tune.end()) {
-        *lanes_out = it->second;
+        *out = it->second;
+        return SDB_OK;
+    }
+    // SDEB200_LAYOUT="lanes,tight,ctas_per_sm" pins the layout (profiling runs
+    // must not capture autotune probes); ctas_per_sm 0 = natural occupancy.
+    if (const char* env = std::getenv("SDEB200_LAYOUT")) {
+        int L = 0, t = 0, cap = 0;
+        if (std::sscanf(env, "%d,%d,%d", &L, &t, &cap) >= 1 && L > 0) {
+            Layout lay{L, t, cap > 0 ? smem_for_cap(s.device, cap) : 0, cap};
+            ctx->tune[key] = lay;
+            *out = lay;
+            return SDB_OK;
+        }
+    }
+    std::vector<Layout> cands;
+    sdb_status rc = candidate_layouts(ctx, s, d, kind_solver, kind_stream, &cands);
+    if (rc != SDB_OK) return rc;
+    if (cands.empty()) return fail_with(ctx, SDB_ERR_CUDA, "no launchable layout for n=%d", d.nequat);
+    if (cands.size() == 1) {
+        *out = cands[0];
+        ctx->tune[key] = cands[0];
         return SDB_OK;
     }
     const int64_t probe = std::min<int64_t>(total, 32);
@@ -253,9 +343,10 @@ sdb_status choose_lanes(sdb_ctx* ctx, Slot& s, const sdb_desc& d, const double* 
     SDB_CUDA(ctx, cudaEventCreate(&e0));
     SDB_CUDA(ctx, cudaEventCreate(&e1));
     float best = 1e30f;
-    int best_l = cands[0];
-    for (int L : cands) {
-        sdeb::RunArgs a = make_args(d, L);
+    Layout best_l = cands[0];
+    const int P = next_pow2(d.nequat);
+    for (const Layout& lay : cands) {
+        sdeb::RunArgs a = make_args(d, lay.lanes);
         a.state_in = d_init;
         a.params = d_params;
         a.state_out = s.t_state.as<double>();
@@ -265,56 +356,62 @@ sdb_status choose_lanes(sdb_ctx* ctx, Slot& s, const sdb_desc& d, const double* 
         a.rng_state = s.t_rng.as<uint64_t>();
         a.ksteps = probe;
         a.chunk_end = 1;
-        float ms = 0.f;
+        a.smem_pad = lay.smem;
+        float ms_best = 1e30f;
         for (int rep = 0; rep < 2; ++rep) {
             cudaEventRecord(e0, st);
-            cudaError_t e = launch_run(a, next_pow2(d.nequat) / L, kind_solver, kind_stream,
-                                       d.coupling, st);
+            cudaError_t e = launch_run(a, P / lay.lanes, kind_solver, kind_stream, d.coupling,
+                                       lay.tight, st);
+            cudaEventRecord(e1, st);
+            if (e == cudaSuccess) e = cudaEventSynchronize(e1);
             if (e != cudaSuccess) {
                 cudaEventDestroy(e0);
                 cudaEventDestroy(e1);
                 return cuda_fail(ctx, e, "autotune launch");
             }
-            cudaEventRecord(e1, st);
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, e0, e1);
+            ms_best = std::min(ms_best, ms);
             s.launches += 1;
         }
-        SDB_CUDA(ctx, cudaEventSynchronize(e1));
-        cudaEventElapsedTime(&ms, e0, e1);
-        if (ms < best) {
-            best = ms;
-            best_l = L;
+        if (ms_best < best) {
+            best = ms_best;
+            best_l = lay;
         }
     }
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     ctx->tune[key] = best_l;
-    *lanes_out = best_l;
+    *out = best_l;
     return SDB_OK;
 }
 
 sdb_status launch_device(sdb_ctx* ctx, Slot& s, const sdb_desc& d, const double* d_init,
                          const double* d_params, double* d_values, int64_t* d_fail,
                          cudaStream_t st) {
-    int lanes = 0;
-    sdb_status rc = choose_lanes(ctx, s, d, d_init, d_params, st, &lanes);
+    Layout lay;
+    sdb_status rc = choose_layout(ctx, s, d, d_init, d_params, st, &lay);
     if (rc != SDB_OK) return rc;
     SDB_CUDA(ctx, s.state.ensure(size_t(d.orbits) * d.nequat * sizeof(double)));
     const size_t rw = rng_words(d, d.orbits);
     if (rw) SDB_CUDA(ctx, s.rng.ensure(rw * sizeof(uint64_t)));
     int kind_solver, kind_stream;
     kernel_kind(d, &kind_solver, &kind_stream);
-    sdeb::RunArgs a = make_args(d, lanes);
+    sdeb::RunArgs a = make_args(d, lay.lanes);
     a.state_in = d_init;
     a.params = d_params;
     a.state_out = s.state.as<double>();
     a.values = d_values;
     a.fail_step = d_fail;
     a.rng_state = s.rng.as<uint64_t>();
-    cudaError_t e = launch_run(a, next_pow2(d.nequat) / lanes, kind_solver, kind_stream,
-                               d.coupling, st);
+    a.smem_pad = lay.smem;
+    cudaError_t e = launch_run(a, next_pow2(d.nequat) / lay.lanes, kind_solver, kind_stream,
+                               d.coupling, lay.tight, st);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "kuramoto_run_kernel launch");
     s.launches += 1;
-    s.lanes = lanes;
+    s.lanes = lay.lanes;
+    s.tight = lay.tight;
+    s.ctas_per_sm = lay.ctas_per_sm;
     return SDB_OK;
 }
 
@@ -430,6 +527,12 @@ const char* sdb_last_error(const sdb_ctx* ctx) {
 int64_t sdb_last_launch_count(const sdb_ctx* ctx) { return ctx ? ctx->launches : 0; }
 int32_t sdb_last_lanes(const sdb_ctx* ctx) { return ctx ? ctx->last_lanes : 0; }
 
+void sdb_last_layout(const sdb_ctx* ctx, int32_t* lanes, int32_t* tight, int32_t* ctas_per_sm) {
+    if (lanes) *lanes = ctx ? ctx->last_lanes : 0;
+    if (tight) *tight = ctx ? ctx->last_tight : 0;
+    if (ctas_per_sm) *ctas_per_sm = ctx ? ctx->last_ctas_per_sm : 0;
+}
+
 sdb_status sdb_run(sdb_ctx* ctx, const sdb_desc* desc, const double* init, const double* params,
                    double* values, int64_t* fail_step) {
     if (!ctx) return fail_with(nullptr, SDB_ERR_ARGUMENT, "null context");
@@ -465,6 +568,8 @@ sdb_status sdb_run(sdb_ctx* ctx, const sdb_desc* desc, const double* init, const
     ctx->launches = 0;
     for (int64_t g = 0; g < used; ++g) ctx->launches += ctx->slots[g].launches;
     ctx->last_lanes = ctx->slots[0].lanes;
+    ctx->last_tight = ctx->slots[0].tight;
+    ctx->last_ctas_per_sm = ctx->slots[0].ctas_per_sm;
     for (int64_t g = 0; g < used; ++g)
         if (status[g] != SDB_OK) return status[g];
     return SDB_OK;
@@ -486,6 +591,8 @@ sdb_status sdb_run_device(sdb_ctx* ctx, const sdb_desc* desc, const double* d_in
                        static_cast<cudaStream_t>(stream));
     ctx->launches = s.launches;
     ctx->last_lanes = s.lanes;
+    ctx->last_tight = s.tight;
+    ctx->last_ctas_per_sm = s.ctas_per_sm;
     return rc;
 }
 
@@ -616,7 +723,7 @@ static sdb_status per_step(sdb_ctx* ctx, int kind_solver, int kind_stream, int32
     a.values = static_cast<double*>(dout.p);
     a.vstride = 1;
     a.check_finite = 0;
-    SDB_CUDA(ctx, launch_run(a, P / L, kind_solver, kind_stream, coupling, nullptr));
+    SDB_CUDA(ctx, launch_run(a, P / L, kind_solver, kind_stream, coupling, 0, nullptr));
     SDB_CUDA(ctx, cudaMemcpy(out, dout.p, size_t(count) * n * sizeof(double), cudaMemcpyDeviceToHost));
     return SDB_OK;
 }

@@ -46,6 +46,7 @@ struct RunArgs {
     int n, nparams, nnoise, lanes, log2lanes;
     int fresh;                // 1: fail=-1 and seed stateful streams in-kernel
     int check_finite;         // 1: run_batch failure semantics; 0: raw per-step API
+    int smem_pad;             // dynamic shared memory per CTA (caps CTAs/SM; 0 = none)
 };
 
 __device__ __forceinline__ bool finite_bits(double x) {
@@ -182,13 +183,19 @@ __host__ __device__ constexpr int blocks_per_lane() {
     return J >= 4 ? J / 4 : 1;
 }
 
-template <int J, int STREAM>
-__device__ __forceinline__ void step_noise(double (&z)[J], const RunArgs& a, int64_t row,
-                                           uint32_t orbit_g, uint64_t step, int base,
-                                           StreamState (&rs)[blocks_per_lane<J>()]) {
+// Draws the step's normals pair by pair and hands each to apply(q, z) as
+// soon as it exists, so at most one Box-Muller pair is live at a time (the
+// v2 kernel materialised z[J] next to the drift's sin/cos arrays: 124
+// registers at J=4).
+template <int J, int STREAM, class Apply>
+__device__ __forceinline__ void step_noise_apply(const RunArgs& a, int64_t row, uint32_t orbit_g,
+                                                 uint64_t step, int base,
+                                                 StreamState (&rs)[blocks_per_lane<J>()],
+                                                 Apply&& apply) {
     if constexpr (STREAM == KS_EXPLICIT) {
 #pragma unroll
-        for (int q = 0; q < J; ++q) z[q] = (base + q < a.n) ? a.noise[row * a.n + base + q] : 0.0;
+        for (int q = 0; q < J; ++q)
+            if (base + q < a.n) apply(q, a.noise[row * a.n + base + q]);
     } else {
         const uint32_t seed_lo = uint32_t(a.seed), seed_hi = uint32_t(a.seed >> 32);
         const uint32_t step_hi = uint32_t(step >> 32), step_lo = uint32_t(step);
@@ -197,7 +204,6 @@ __device__ __forceinline__ void step_noise(double (&z)[J], const RunArgs& a, int
 #pragma unroll
             for (int t = 0; t < J / 4; ++t) {
                 const int b = base / 4 + t;
-                double* zz = z + 4 * t;
                 if (4 * b < nn) {
                     Words4 w;
                     if constexpr (STREAM == KS_PHILOX) {
@@ -205,15 +211,15 @@ __device__ __forceinline__ void step_noise(double (&z)[J], const RunArgs& a, int
                     } else {
                         w = stream_block<STREAM>(rs[t]);
                     }
-                    box_muller_pair(w.w0, w.w1, zz[0], zz[1]);
+                    double z0, z1;
+                    box_muller_pair(w.w0, w.w1, z0, z1);
+                    apply(4 * t, z0);
+                    apply(4 * t + 1, z1);
                     if (4 * b + 2 < nn) {
-                        box_muller_pair(w.w2, w.w3, zz[2], zz[3]);
-                    } else {
-                        zz[2] = 0.0;
-                        zz[3] = 0.0;
+                        box_muller_pair(w.w2, w.w3, z0, z1);
+                        apply(4 * t + 2, z0);
+                        apply(4 * t + 3, z1);
                     }
-                } else {
-                    zz[0] = zz[1] = zz[2] = zz[3] = 0.0;
                 }
             }
         } else {
@@ -232,14 +238,11 @@ __device__ __forceinline__ void step_noise(double (&z)[J], const RunArgs& a, int
                 double z0, z1;
                 box_muller_pair(wa, wb, z0, z1);
                 if constexpr (J == 2) {
-                    z[0] = z0;
-                    z[1] = z1;
+                    apply(0, z0);
+                    apply(1, z1);
                 } else {
-                    z[0] = (base & 1) ? z1 : z0;
+                    apply(0, (base & 1) ? z1 : z0);
                 }
-            } else {
-#pragma unroll
-                for (int q = 0; q < J; ++q) z[q] = 0.0;
             }
         }
     }
@@ -247,8 +250,10 @@ __device__ __forceinline__ void step_noise(double (&z)[J], const RunArgs& a, int
 
 // ---- the fused run kernel ----------------------------------------------------
 
-template <int J, int SOLVER, int STREAM, int COUPLING>
-__global__ void __launch_bounds__(kBlock) kuramoto_run_kernel(const RunArgs a) {
+// MINB > 1 ("tight" variants) caps registers so more CTAs are resident: the
+// autotuner weighs latency hiding against per-thread ILP and wave quantisation.
+template <int J, int SOLVER, int STREAM, int COUPLING, int MINB>
+__global__ void __launch_bounds__(kBlock, MINB) kuramoto_run_kernel(const RunArgs a) {
     constexpr bool kStochastic = (SOLVER == KS_EM) && (STREAM != KS_NONE);
     constexpr bool kStateful = kStochastic && (STREAM == KS_SFC64 || STREAM == KS_XOSHIRO);
     constexpr int NB = blocks_per_lane<J>();
@@ -316,16 +321,14 @@ __global__ void __launch_bounds__(kBlock) kuramoto_run_kernel(const RunArgs a) {
                 if constexpr (SOLVER == KS_EM) {
                     double f[J];
                     if constexpr (kStochastic) {
-                        double z[J];
-                        step_noise<J, STREAM>(z, a, row, orbit_g, step, base, rs);
                         drift<J, COUPLING>(y, om, kn, base, n, lanes, sh, shs, f);
-#pragma unroll
-                        for (int q = 0; q < J; ++q) {
-                            // (y + f*dt) + sqrt(dt) * (s_i * N_i)   (solvers.py:70-71, model.py:201)
-                            const double g = __dmul_rn(sg[q], z[q]);
-                            y[q] = __dadd_rn(__dadd_rn(y[q], __dmul_rn(f[q], dt)),
-                                             __dmul_rn(a.sqrt_dt, g));
-                        }
+                        // (y + f*dt) + sqrt(dt) * (s_i * N_i)   (solvers.py:70-71, model.py:201)
+                        step_noise_apply<J, STREAM>(
+                            a, row, orbit_g, step, base, rs, [&](int q, double z) {
+                                const double g = __dmul_rn(sg[q], z);
+                                y[q] = __dadd_rn(__dadd_rn(y[q], __dmul_rn(f[q], dt)),
+                                                 __dmul_rn(a.sqrt_dt, g));
+                            });
                     } else {
                         drift<J, COUPLING>(y, om, kn, base, n, lanes, sh, shs, f);
 #pragma unroll
@@ -411,10 +414,20 @@ __global__ void __launch_bounds__(kBlock) kuramoto_run_kernel(const RunArgs a) {
     }
 }
 
-// Host-side dispatch (sdeb_kuramoto_j*.cu instantiate per J).
+// Host-side dispatch (sdeb_kuramoto_j*.cu instantiate per J).  tight=1 selects
+// the register-capped variant where one exists (tight_minb<J>() > 1).
 template <int J>
-cudaError_t launch_kuramoto_j(const RunArgs& a, int solver, int stream, int coupling,
+cudaError_t launch_kuramoto_j(const RunArgs& a, int solver, int stream, int coupling, int tight,
                               cudaStream_t st);
+// Resident CTAs per SM of that kernel at the given dynamic shared memory.
+template <int J>
+cudaError_t occupancy_kuramoto_j(int solver, int stream, int coupling, int tight, size_t smem,
+                                 int* blocks);
+
+template <int J>
+__host__ __device__ constexpr int tight_minb() {
+    return J == 4 ? 6 : (J == 8 ? 4 : 1);
+}
 
 inline size_t pairwise_smem_bytes(int J, int coupling) {
     return coupling == KC_PAIRWISE ? size_t(2) * J * kBlock * sizeof(double) : 0;

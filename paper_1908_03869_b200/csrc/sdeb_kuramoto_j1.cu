@@ -2,5 +2,6 @@
 #include "sdeb_kuramoto_inst.cuh"
 
 namespace sdeb {
-template cudaError_t launch_kuramoto_j<1>(const RunArgs&, int, int, int, cudaStream_t);
+template cudaError_t launch_kuramoto_j<1>(const RunArgs&, int, int, int, int, cudaStream_t);
+template cudaError_t occupancy_kuramoto_j<1>(int, int, int, int, size_t, int*);
 }  // namespace sdeb
