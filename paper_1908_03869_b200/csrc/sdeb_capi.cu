@@ -22,12 +22,6 @@
 #include "sdeb_kuramoto.cuh"
 #include "sdeb_misc.h"
 
-namespace sdeb {
-template <int J>
-cudaError_t launch_kuramoto_j(const RunArgs& a, int solver, int stream, int coupling,
-                              cudaStream_t st);
-}
-
 namespace {
 
 thread_local std::string g_thread_error;
