@@ -122,32 +122,29 @@ int ilog2(int x) {
 }
 
 cudaError_t launch_run(const sdeb::RunArgs& a, int J, int solver, int stream, int coupling,
-                       int tight, cudaStream_t st) {
+                       int padded, cudaStream_t st) {
     switch (J) {
-        case 1: return sdeb::launch_kuramoto_j<1>(a, solver, stream, coupling, tight, st);
-        case 2: return sdeb::launch_kuramoto_j<2>(a, solver, stream, coupling, tight, st);
-        case 4: return sdeb::launch_kuramoto_j<4>(a, solver, stream, coupling, tight, st);
-        case 8: return sdeb::launch_kuramoto_j<8>(a, solver, stream, coupling, tight, st);
-        case 16: return sdeb::launch_kuramoto_j<16>(a, solver, stream, coupling, tight, st);
+        case 1: return sdeb::launch_kuramoto_j<1>(a, solver, stream, coupling, padded, st);
+        case 2: return sdeb::launch_kuramoto_j<2>(a, solver, stream, coupling, padded, st);
+        case 4: return sdeb::launch_kuramoto_j<4>(a, solver, stream, coupling, padded, st);
+        case 8: return sdeb::launch_kuramoto_j<8>(a, solver, stream, coupling, padded, st);
+        case 16: return sdeb::launch_kuramoto_j<16>(a, solver, stream, coupling, padded, st);
         default: return cudaErrorInvalidValue;
     }
 }
 
-cudaError_t occupancy_run(int J, int solver, int stream, int coupling, int tight, size_t smem,
+cudaError_t occupancy_run(int J, int solver, int stream, int coupling, int padded, size_t smem,
                           int* blocks) {
     switch (J) {
-        case 1: return sdeb::occupancy_kuramoto_j<1>(solver, stream, coupling, tight, smem, blocks);
-        case 2: return sdeb::occupancy_kuramoto_j<2>(solver, stream, coupling, tight, smem, blocks);
-        case 4: return sdeb::occupancy_kuramoto_j<4>(solver, stream, coupling, tight, smem, blocks);
-        case 8: return sdeb::occupancy_kuramoto_j<8>(solver, stream, coupling, tight, smem, blocks);
-        case 16: return sdeb::occupancy_kuramoto_j<16>(solver, stream, coupling, tight, smem, blocks);
+        case 1: return sdeb::occupancy_kuramoto_j<1>(solver, stream, coupling, padded, smem, blocks);
+        case 2: return sdeb::occupancy_kuramoto_j<2>(solver, stream, coupling, padded, smem, blocks);
+        case 4: return sdeb::occupancy_kuramoto_j<4>(solver, stream, coupling, padded, smem, blocks);
+        case 8: return sdeb::occupancy_kuramoto_j<8>(solver, stream, coupling, padded, smem, blocks);
+        case 16: return sdeb::occupancy_kuramoto_j<16>(solver, stream, coupling, padded, smem, blocks);
         default: return cudaErrorInvalidValue;
     }
 }
 
-int tight_minb_of(int J) {
-    return J == 4 ? sdeb::tight_minb<4>() : (J == 8 ? sdeb::tight_minb<8>() : 1);
-}
 
 // Kernel kind for a validated descriptor.
 void kernel_kind(const sdb_desc& d, int* solver, int* stream) {
@@ -268,26 +265,24 @@ sdb_status candidate_layouts(sdb_ctx* ctx, const Slot& s, const sdb_desc& d, int
     }
     for (int L : lanes_list) {
         const int J = P / L;
-        const int tights = (d.coupling == SDB_COUPLING_MEANFIELD && tight_minb_of(J) > 1) ? 2 : 1;
-        for (int t = 0; t < tights; ++t) {
-            int occ = 0;
-            SDB_CUDA(ctx, occupancy_run(J, kind_solver, kind_stream, d.coupling, t, 0, &occ));
-            if (occ < 1) continue;
-            const int64_t ctas = (d.orbits * L + sdeb::kBlock - 1) / sdeb::kBlock;
-            out->push_back(Layout{L, t, 0, occ});
-            // caps that turn a ragged last wave into full ones
-            for (int cap = occ - 1; cap >= 1 && cap >= occ - 4; --cap) {
-                const double waves_cap = double(ctas) / (double(sms) * cap);
-                const double waves_occ = double(ctas) / (double(sms) * occ);
-                const double eff_cap = waves_cap / std::ceil(waves_cap);
-                const double eff_occ = waves_occ / std::ceil(waves_occ);
-                if (eff_cap <= eff_occ + 0.02) continue;
-                const int smem = smem_for_cap(s.device, cap);
-                int got = 0;
-                SDB_CUDA(ctx, occupancy_run(J, kind_solver, kind_stream, d.coupling, t,
-                                            size_t(smem), &got));
-                if (got == cap) out->push_back(Layout{L, t, smem, cap});
-            }
+        const int padded = d.nequat < P ? 1 : 0;
+        int occ = 0;
+        SDB_CUDA(ctx, occupancy_run(J, kind_solver, kind_stream, d.coupling, padded, 0, &occ));
+        if (occ < 1) continue;
+        const int64_t ctas = (d.orbits * L + sdeb::kBlock - 1) / sdeb::kBlock;
+        out->push_back(Layout{L, 0, 0, occ});
+        // caps that turn a ragged last wave into full ones
+        for (int cap = occ - 1; cap >= 1 && cap >= occ - 4; --cap) {
+            const double waves_cap = double(ctas) / (double(sms) * cap);
+            const double waves_occ = double(ctas) / (double(sms) * occ);
+            const double eff_cap = waves_cap / std::ceil(waves_cap);
+            const double eff_occ = waves_occ / std::ceil(waves_occ);
+            if (eff_cap <= eff_occ + 0.02) continue;
+            const int smem = smem_for_cap(s.device, cap);
+            int got = 0;
+            SDB_CUDA(ctx, occupancy_run(J, kind_solver, kind_stream, d.coupling, padded,
+                                        size_t(smem), &got));
+            if (got == cap) out->push_back(Layout{L, 0, smem, cap});
         }
     }
     return SDB_OK;
@@ -328,7 +323,7 @@ sdb_status choose_layout(sdb_ctx* ctx, Slot& s, const sdb_desc& d, const double*
         ctx->tune[key] = cands[0];
         return SDB_OK;
     }
-    const int64_t probe = std::min<int64_t>(total, 32);
+    const int64_t probe = std::min<int64_t>(total, 128);
     SDB_CUDA(ctx, s.t_values.ensure(size_t(d.orbits) * d.nequat * sizeof(double)));
     SDB_CUDA(ctx, s.t_state.ensure(size_t(d.orbits) * d.nequat * sizeof(double)));
     SDB_CUDA(ctx, s.t_fail.ensure(size_t(d.orbits) * sizeof(int64_t)));
@@ -355,7 +350,7 @@ sdb_status choose_layout(sdb_ctx* ctx, Slot& s, const sdb_desc& d, const double*
         for (int rep = 0; rep < 2; ++rep) {
             cudaEventRecord(e0, st);
             cudaError_t e = launch_run(a, P / lay.lanes, kind_solver, kind_stream, d.coupling,
-                                       lay.tight, st);
+                                       d.nequat < P ? 1 : 0, st);
             cudaEventRecord(e1, st);
             if (e == cudaSuccess) e = cudaEventSynchronize(e1);
             if (e != cudaSuccess) {
@@ -399,8 +394,9 @@ sdb_status launch_device(sdb_ctx* ctx, Slot& s, const sdb_desc& d, const double*
     a.fail_step = d_fail;
     a.rng_state = s.rng.as<uint64_t>();
     a.smem_pad = lay.smem;
-    cudaError_t e = launch_run(a, next_pow2(d.nequat) / lay.lanes, kind_solver, kind_stream,
-                               d.coupling, lay.tight, st);
+    const int P = next_pow2(d.nequat);
+    cudaError_t e = launch_run(a, P / lay.lanes, kind_solver, kind_stream, d.coupling,
+                               d.nequat < P ? 1 : 0, st);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "kuramoto_run_kernel launch");
     s.launches += 1;
     s.lanes = lay.lanes;
@@ -717,7 +713,7 @@ static sdb_status per_step(sdb_ctx* ctx, int kind_solver, int kind_stream, int32
     a.values = static_cast<double*>(dout.p);
     a.vstride = 1;
     a.check_finite = 0;
-    SDB_CUDA(ctx, launch_run(a, P / L, kind_solver, kind_stream, coupling, 0, nullptr));
+    SDB_CUDA(ctx, launch_run(a, P / L, kind_solver, kind_stream, coupling, 1, nullptr));
     SDB_CUDA(ctx, cudaMemcpy(out, dout.p, size_t(count) * n * sizeof(double), cudaMemcpyDeviceToHost));
     return SDB_OK;
 }

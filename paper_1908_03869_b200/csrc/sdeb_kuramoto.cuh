@@ -84,17 +84,18 @@ __device__ __forceinline__ int64_t group_fail(int64_t f, int lanes) {
 // ---- drift f_i = omega_i + (K/n) * S_i (model.py:193-196) -----------------
 
 // MEANFIELD: S_i = cos(y_i) * sum_j sin(y_j) - sin(y_i) * sum_j cos(y_j).
-template <int J>
+// PADDED (n < L*J): padding leaves (whose y stays 0) are forced to +0.0 in
+// the sums; the unpadded instantiation (n a power of two: every BASELINE
+// config) carries no per-oscillator predicates at all.
+template <int J, bool PADDED>
 __device__ __forceinline__ void drift_meanfield(const double (&y)[J], const double (&om)[J],
                                                 double kn, int base, int n, int lanes,
                                                 double (&f)[J]) {
-    double sn[J], cs[J], ts[J], tc[J], x[J];
-#pragma unroll
-    for (int q = 0; q < J; ++q) x[q] = (base + q < n) ? y[q] : 0.0;
-    sincos_vec<J>(x, sn, cs);
+    double sn[J], cs[J], ts[J], tc[J];
+    sincos_vec<J>(y, sn, cs);
 #pragma unroll
     for (int q = 0; q < J; ++q) {
-        if (base + q >= n) {
+        if (PADDED && base + q >= n) {
             sn[q] = 0.0;
             cs[q] = 0.0;
         }
@@ -165,12 +166,12 @@ __device__ __forceinline__ void drift_pairwise(const double (&y)[J], const doubl
     }
 }
 
-template <int J, int COUPLING>
+template <int J, int COUPLING, bool PADDED>
 __device__ __forceinline__ void drift(const double (&y)[J], const double (&om)[J], double kn,
                                       int base, int n, int lanes, double* sh, double* shs,
                                       double (&f)[J]) {
     if constexpr (COUPLING == KC_MEANFIELD) {
-        drift_meanfield<J>(y, om, kn, base, n, lanes, f);
+        drift_meanfield<J, PADDED>(y, om, kn, base, n, lanes, f);
     } else {
         drift_pairwise<J>(y, om, kn, base, n, lanes, sh, shs, f);
     }
@@ -187,7 +188,7 @@ __host__ __device__ constexpr int blocks_per_lane() {
 // soon as it exists, so at most one Box-Muller pair is live at a time (the
 // v2 kernel materialised z[J] next to the drift's sin/cos arrays: 124
 // registers at J=4).
-template <int J, int STREAM, class Apply>
+template <int J, int STREAM, bool PADDED, class Apply>
 __device__ __forceinline__ void step_noise_apply(const RunArgs& a, int64_t row, uint32_t orbit_g,
                                                  uint64_t step, int base,
                                                  StreamState (&rs)[blocks_per_lane<J>()],
@@ -204,7 +205,7 @@ __device__ __forceinline__ void step_noise_apply(const RunArgs& a, int64_t row, 
 #pragma unroll
             for (int t = 0; t < J / 4; ++t) {
                 const int b = base / 4 + t;
-                if (4 * b < nn) {
+                if (!PADDED || 4 * b < nn) {  // unpadded: n = L*J >= 4, whole blocks
                     Words4 w;
                     if constexpr (STREAM == KS_PHILOX) {
                         w = philox4x32_10(seed_hi, step_hi, step_lo, uint32_t(b), seed_lo, orbit_g);
@@ -215,7 +216,7 @@ __device__ __forceinline__ void step_noise_apply(const RunArgs& a, int64_t row, 
                     box_muller_pair(w.w0, w.w1, z0, z1);
                     apply(4 * t, z0);
                     apply(4 * t + 1, z1);
-                    if (4 * b + 2 < nn) {
+                    if (!PADDED || 4 * b + 2 < nn) {
                         box_muller_pair(w.w2, w.w3, z0, z1);
                         apply(4 * t + 2, z0);
                         apply(4 * t + 3, z1);
@@ -250,10 +251,9 @@ __device__ __forceinline__ void step_noise_apply(const RunArgs& a, int64_t row, 
 
 // ---- the fused run kernel ----------------------------------------------------
 
-// MINB > 1 ("tight" variants) caps registers so more CTAs are resident: the
-// autotuner weighs latency hiding against per-thread ILP and wave quantisation.
-template <int J, int SOLVER, int STREAM, int COUPLING, int MINB>
-__global__ void __launch_bounds__(kBlock, MINB) kuramoto_run_kernel(const RunArgs a) {
+// PADDED = (n < lanes * J): instantiated with and without padding handling.
+template <int J, int SOLVER, int STREAM, int COUPLING, bool PADDED>
+__global__ void __launch_bounds__(kBlock) kuramoto_run_kernel(const RunArgs a) {
     constexpr bool kStochastic = (SOLVER == KS_EM) && (STREAM != KS_NONE);
     constexpr bool kStateful = kStochastic && (STREAM == KS_SFC64 || STREAM == KS_XOSHIRO);
     constexpr int NB = blocks_per_lane<J>();
@@ -285,7 +285,7 @@ __global__ void __launch_bounds__(kBlock, MINB) kuramoto_run_kernel(const RunArg
 
     if constexpr (SOLVER == KS_DRIFT) {
         double f[J];
-        drift<J, COUPLING>(y, om, kn, base, n, lanes, sh, shs, f);
+        drift<J, COUPLING, PADDED>(y, om, kn, base, n, lanes, sh, shs, f);
         if (active) {
 #pragma unroll
             for (int q = 0; q < J; ++q)
@@ -321,40 +321,40 @@ __global__ void __launch_bounds__(kBlock, MINB) kuramoto_run_kernel(const RunArg
                 if constexpr (SOLVER == KS_EM) {
                     double f[J];
                     if constexpr (kStochastic) {
-                        drift<J, COUPLING>(y, om, kn, base, n, lanes, sh, shs, f);
+                        drift<J, COUPLING, PADDED>(y, om, kn, base, n, lanes, sh, shs, f);
                         // (y + f*dt) + sqrt(dt) * (s_i * N_i)   (solvers.py:70-71, model.py:201)
-                        step_noise_apply<J, STREAM>(
+                        step_noise_apply<J, STREAM, PADDED>(
                             a, row, orbit_g, step, base, rs, [&](int q, double z) {
                                 const double g = __dmul_rn(sg[q], z);
                                 y[q] = __dadd_rn(__dadd_rn(y[q], __dmul_rn(f[q], dt)),
                                                  __dmul_rn(a.sqrt_dt, g));
                             });
                     } else {
-                        drift<J, COUPLING>(y, om, kn, base, n, lanes, sh, shs, f);
+                        drift<J, COUPLING, PADDED>(y, om, kn, base, n, lanes, sh, shs, f);
 #pragma unroll
                         for (int q = 0; q < J; ++q) y[q] = __dadd_rn(y[q], __dmul_rn(f[q], dt));
                     }
                 } else {  // KS_RK4 (solvers.py:80-88)
                     double k[J], acc[J], ys[J];
-                    drift<J, COUPLING>(y, om, kn, base, n, lanes, sh, shs, k);  // k1
+                    drift<J, COUPLING, PADDED>(y, om, kn, base, n, lanes, sh, shs, k);  // k1
 #pragma unroll
                     for (int q = 0; q < J; ++q) {
                         acc[q] = k[q];
                         ys[q] = __dadd_rn(y[q], __dmul_rn(a.half_dt, k[q]));
                     }
-                    drift<J, COUPLING>(ys, om, kn, base, n, lanes, sh, shs, k);  // k2
+                    drift<J, COUPLING, PADDED>(ys, om, kn, base, n, lanes, sh, shs, k);  // k2
 #pragma unroll
                     for (int q = 0; q < J; ++q) {
                         acc[q] = __dadd_rn(acc[q], __dmul_rn(2.0, k[q]));
                         ys[q] = __dadd_rn(y[q], __dmul_rn(a.half_dt, k[q]));
                     }
-                    drift<J, COUPLING>(ys, om, kn, base, n, lanes, sh, shs, k);  // k3
+                    drift<J, COUPLING, PADDED>(ys, om, kn, base, n, lanes, sh, shs, k);  // k3
 #pragma unroll
                     for (int q = 0; q < J; ++q) {
                         acc[q] = __dadd_rn(acc[q], __dmul_rn(2.0, k[q]));
                         ys[q] = __dadd_rn(y[q], __dmul_rn(dt, k[q]));
                     }
-                    drift<J, COUPLING>(ys, om, kn, base, n, lanes, sh, shs, k);  // k4
+                    drift<J, COUPLING, PADDED>(ys, om, kn, base, n, lanes, sh, shs, k);  // k4
 #pragma unroll
                     for (int q = 0; q < J; ++q) {
                         acc[q] = __dadd_rn(acc[q], k[q]);
@@ -366,7 +366,8 @@ __global__ void __launch_bounds__(kBlock, MINB) kuramoto_run_kernel(const RunArg
                 // minimum is the orbit's first failing step.
                 bool bad = false;
 #pragma unroll
-                for (int q = 0; q < J; ++q) bad |= (base + q < n) && !finite_bits(y[q]);
+                // (padding oscillators stay 0: no validity predicate needed)
+                for (int q = 0; q < J; ++q) bad |= !finite_bits(y[q]);
                 if (bad && a.check_finite) {
                     if (fail < 0) fail = int64_t(step);
 #pragma unroll
@@ -414,20 +415,15 @@ __global__ void __launch_bounds__(kBlock, MINB) kuramoto_run_kernel(const RunArg
     }
 }
 
-// Host-side dispatch (sdeb_kuramoto_j*.cu instantiate per J).  tight=1 selects
-// the register-capped variant where one exists (tight_minb<J>() > 1).
+// Host-side dispatch (sdeb_kuramoto_j*.cu instantiate per J).  padded=0 selects
+// the predicate-free instantiation (requires n == lanes * J).
 template <int J>
-cudaError_t launch_kuramoto_j(const RunArgs& a, int solver, int stream, int coupling, int tight,
-                              cudaStream_t st);
+cudaError_t launch_kuramoto_j(const RunArgs& a, int solver, int stream, int coupling,
+                              int padded, cudaStream_t st);
 // Resident CTAs per SM of that kernel at the given dynamic shared memory.
 template <int J>
-cudaError_t occupancy_kuramoto_j(int solver, int stream, int coupling, int tight, size_t smem,
+cudaError_t occupancy_kuramoto_j(int solver, int stream, int coupling, int padded, size_t smem,
                                  int* blocks);
-
-template <int J>
-__host__ __device__ constexpr int tight_minb() {
-    return J == 4 ? 6 : (J == 8 ? 4 : 1);
-}
 
 inline size_t pairwise_smem_bytes(int J, int coupling) {
     return coupling == KC_PAIRWISE ? size_t(2) * J * kBlock * sizeof(double) : 0;

@@ -5,66 +5,65 @@
 
 namespace sdeb {
 
-template <int J, int S, int R, int C, int M>
+template <int J, int S, int R, int C, bool P>
 static cudaError_t launch_one(const RunArgs& a, cudaStream_t st) {
     const int64_t threads = a.orbits * int64_t(a.lanes);
     const unsigned grid = unsigned((threads + kBlock - 1) / kBlock);
     const size_t need = pairwise_smem_bytes(J, C);
     const size_t smem = need > size_t(a.smem_pad) ? need : size_t(a.smem_pad);
     if (smem > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(kuramoto_run_kernel<J, S, R, C, M>,
+        cudaError_t e = cudaFuncSetAttribute(kuramoto_run_kernel<J, S, R, C, P>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              int(smem));
         if (e != cudaSuccess) return e;
     }
-    kuramoto_run_kernel<J, S, R, C, M><<<grid, kBlock, smem, st>>>(a);
+    kuramoto_run_kernel<J, S, R, C, P><<<grid, kBlock, smem, st>>>(a);
     return cudaGetLastError();
 }
 
-template <int J, int S, int R, int C, int M>
+template <int J, int S, int R, int C, bool P>
 static cudaError_t occupancy_one(size_t smem, int* blocks) {
     const size_t need = pairwise_smem_bytes(J, C);
     if (smem < need) smem = need;
     if (smem > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(kuramoto_run_kernel<J, S, R, C, M>,
+        cudaError_t e = cudaFuncSetAttribute(kuramoto_run_kernel<J, S, R, C, P>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              int(smem));
         if (e != cudaSuccess) return e;
     }
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, kuramoto_run_kernel<J, S, R, C, M>,
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, kuramoto_run_kernel<J, S, R, C, P>,
                                                          kBlock, smem);
 }
 
-// Visits the kernel instantiation for (solver, stream, coupling, tight) with
-// op.template run<J, S, R, C, M>().  Tight variants exist for the meanfield
-// em / rk4 paths at J in {4, 8}.
+// Visits the kernel instantiation for (solver, stream, coupling, padded) with
+// op.template run<J, S, R, C, P>().  The predicate-free (P = false) variants
+// exist for the meanfield paths; pairwise and the explicit-noise / drift
+// entry points always use the padded form.
 template <int J, class Op>
-static cudaError_t dispatch(int solver, int stream, int coupling, int tight, Op&& op) {
-    constexpr int MT = tight_minb<J>();
-    const bool t = tight && MT > 1 && coupling == KC_MEANFIELD;
-#define SDEB_PICK(S, R, C)                                                      \
-    return t ? op.template run<J, S, R, C, (C == KC_MEANFIELD ? MT : 1)>()     \
-             : op.template run<J, S, R, C, 1>()
+static cudaError_t dispatch(int solver, int stream, int coupling, int padded, Op&& op) {
+    const bool p = padded != 0;
+#define SDEB_PICK(S, R) \
+    return p ? op.template run<J, S, R, KC_MEANFIELD, true>() : op.template run<J, S, R, KC_MEANFIELD, false>()
     if (coupling == KC_PAIRWISE) {
-        if (solver == KS_RK4) SDEB_PICK(KS_RK4, KS_NONE, KC_PAIRWISE);
-        if (solver == KS_DRIFT) SDEB_PICK(KS_DRIFT, KS_NONE, KC_PAIRWISE);
+        if (solver == KS_RK4) return op.template run<J, KS_RK4, KS_NONE, KC_PAIRWISE, true>();
+        if (solver == KS_DRIFT) return op.template run<J, KS_DRIFT, KS_NONE, KC_PAIRWISE, true>();
         switch (stream) {
-            case KS_PHILOX: SDEB_PICK(KS_EM, KS_PHILOX, KC_PAIRWISE);
-            case KS_SFC64: SDEB_PICK(KS_EM, KS_SFC64, KC_PAIRWISE);
-            case KS_XOSHIRO: SDEB_PICK(KS_EM, KS_XOSHIRO, KC_PAIRWISE);
-            case KS_NONE: SDEB_PICK(KS_EM, KS_NONE, KC_PAIRWISE);
-            case KS_EXPLICIT: SDEB_PICK(KS_EM, KS_EXPLICIT, KC_PAIRWISE);
+            case KS_PHILOX: return op.template run<J, KS_EM, KS_PHILOX, KC_PAIRWISE, true>();
+            case KS_SFC64: return op.template run<J, KS_EM, KS_SFC64, KC_PAIRWISE, true>();
+            case KS_XOSHIRO: return op.template run<J, KS_EM, KS_XOSHIRO, KC_PAIRWISE, true>();
+            case KS_NONE: return op.template run<J, KS_EM, KS_NONE, KC_PAIRWISE, true>();
+            case KS_EXPLICIT: return op.template run<J, KS_EM, KS_EXPLICIT, KC_PAIRWISE, true>();
             default: return cudaErrorInvalidValue;
         }
     }
-    if (solver == KS_RK4) SDEB_PICK(KS_RK4, KS_NONE, KC_MEANFIELD);
-    if (solver == KS_DRIFT) return op.template run<J, KS_DRIFT, KS_NONE, KC_MEANFIELD, 1>();
+    if (solver == KS_RK4) SDEB_PICK(KS_RK4, KS_NONE);
+    if (solver == KS_DRIFT) return op.template run<J, KS_DRIFT, KS_NONE, KC_MEANFIELD, true>();
     switch (stream) {
-        case KS_PHILOX: SDEB_PICK(KS_EM, KS_PHILOX, KC_MEANFIELD);
-        case KS_SFC64: SDEB_PICK(KS_EM, KS_SFC64, KC_MEANFIELD);
-        case KS_XOSHIRO: SDEB_PICK(KS_EM, KS_XOSHIRO, KC_MEANFIELD);
-        case KS_NONE: SDEB_PICK(KS_EM, KS_NONE, KC_MEANFIELD);
-        case KS_EXPLICIT: return op.template run<J, KS_EM, KS_EXPLICIT, KC_MEANFIELD, 1>();
+        case KS_PHILOX: SDEB_PICK(KS_EM, KS_PHILOX);
+        case KS_SFC64: SDEB_PICK(KS_EM, KS_SFC64);
+        case KS_XOSHIRO: SDEB_PICK(KS_EM, KS_XOSHIRO);
+        case KS_NONE: SDEB_PICK(KS_EM, KS_NONE);
+        case KS_EXPLICIT: return op.template run<J, KS_EM, KS_EXPLICIT, KC_MEANFIELD, true>();
         default: return cudaErrorInvalidValue;
     }
 #undef SDEB_PICK
@@ -73,31 +72,31 @@ static cudaError_t dispatch(int solver, int stream, int coupling, int tight, Op&
 struct LaunchOp {
     const RunArgs& a;
     cudaStream_t st;
-    template <int J, int S, int R, int C, int M>
+    template <int J, int S, int R, int C, bool P>
     cudaError_t run() const {
-        return launch_one<J, S, R, C, M>(a, st);
+        return launch_one<J, S, R, C, P>(a, st);
     }
 };
 
 struct OccupancyOp {
     size_t smem;
     int* blocks;
-    template <int J, int S, int R, int C, int M>
+    template <int J, int S, int R, int C, bool P>
     cudaError_t run() const {
-        return occupancy_one<J, S, R, C, M>(smem, blocks);
+        return occupancy_one<J, S, R, C, P>(smem, blocks);
     }
 };
 
 template <int J>
-cudaError_t launch_kuramoto_j(const RunArgs& a, int solver, int stream, int coupling, int tight,
-                              cudaStream_t st) {
-    return dispatch<J>(solver, stream, coupling, tight, LaunchOp{a, st});
+cudaError_t launch_kuramoto_j(const RunArgs& a, int solver, int stream, int coupling,
+                              int padded, cudaStream_t st) {
+    return dispatch<J>(solver, stream, coupling, padded, LaunchOp{a, st});
 }
 
 template <int J>
-cudaError_t occupancy_kuramoto_j(int solver, int stream, int coupling, int tight, size_t smem,
+cudaError_t occupancy_kuramoto_j(int solver, int stream, int coupling, int padded, size_t smem,
                                  int* blocks) {
-    return dispatch<J>(solver, stream, coupling, tight, OccupancyOp{smem, blocks});
+    return dispatch<J>(solver, stream, coupling, padded, OccupancyOp{smem, blocks});
 }
 
 }  // namespace sdeb
