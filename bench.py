@@ -334,7 +334,7 @@ def run_ours(args, w, world, rank, local, dist):
     import ctypes
     lay = [ctypes.c_int32() for _ in range(3)]
     lib.sdb_last_layout(ctx, *(ctypes.byref(v) for v in lay))
-    lanes, tight, ctas_per_sm = (int(v.value) for v in lay)
+    lanes, persistent, ctas_per_sm = (int(v.value) for v in lay)
     launches_per_step = int(lib.sdb_last_launch_count(ctx))
 
     clocks = ClockSampler(local)
@@ -405,7 +405,7 @@ def run_ours(args, w, world, rank, local, dist):
             "config": {"workload": args.workload, "desc": w["desc"], "n": n,
                        "orbits_per_gpu": m, "sde_steps": steps, "ksteps": w["ksteps"],
                        "solver": w["solver"], "stream": w["stream"], "coupling": args.coupling,
-                       "lanes_per_orbit": lanes, "register_capped": bool(tight),
+                       "lanes_per_orbit": lanes, "persistent_grid": bool(persistent),
                        "ctas_per_sm": ctas_per_sm, "parallelism": "orbit-shard x%d" % world,
                        "l2": "flushed (512 MiB memset) between timed steps, outside the "
                              "event pairs"},

@@ -96,9 +96,11 @@ sdb_status sdb_run_device(sdb_ctx* ctx, const sdb_desc* desc, const double* d_in
 int64_t sdb_last_launch_count(const sdb_ctx* ctx);
 /* Lanes-per-orbit layout chosen by the last run (after autotune). */
 int32_t sdb_last_lanes(const sdb_ctx* ctx);
-/* Full layout of the last run: lanes per orbit, register-capped variant (0/1),
- * resident CTAs per SM it ran at. */
-void sdb_last_layout(const sdb_ctx* ctx, int32_t* lanes, int32_t* tight, int32_t* ctas_per_sm);
+/* Full layout of the last run: lanes per orbit, persistent work-pulling grid
+ * (0/1), resident CTAs per SM it ran at.  SDEB200_LAYOUT="lanes,persistent,ctas"
+ * in the environment pins it (profiling). */
+void sdb_last_layout(const sdb_ctx* ctx, int32_t* lanes, int32_t* persistent,
+                     int32_t* ctas_per_sm);
 
 /* ---- noise streams (rng.py) ------------------------------------------------ */
 

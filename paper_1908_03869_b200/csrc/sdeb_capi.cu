@@ -54,19 +54,21 @@ struct Slot {
     int device = 0;
     cudaStream_t stream = nullptr;
     DevBuf init, params, values, state, fail, rng;
-    DevBuf t_values, t_state, t_fail, t_rng;  // autotune scratch
+    DevBuf t_values, t_state, t_fail, t_rng, t_work;  // autotune scratch
+    DevBuf work;  // persistent mode: item counter + per-group slab counters
     int64_t launches = 0;
     int32_t lanes = 0;
-    int32_t tight = 0;
+    int32_t persistent = 0;
     int32_t ctas_per_sm = 0;
     std::string error;
 };
 
-// One launch layout: lanes per orbit, register-capped variant, dynamic
-// shared memory used to cap resident CTAs per SM (wave shaping).
+// One launch layout: lanes per orbit, persistent work-pulling grid or one
+// CTA per CTA-group, dynamic shared memory used to cap resident CTAs per SM
+// (wave shaping), and the resident CTAs per SM it runs at.
 struct Layout {
     int lanes = 0;
-    int tight = 0;
+    int persistent = 0;
     int smem = 0;
     int ctas_per_sm = 0;
 };
@@ -80,7 +82,7 @@ struct sdb_ctx {
     std::string error;
     int64_t launches = 0;
     int32_t last_lanes = 0;
-    int32_t last_tight = 0;
+    int32_t last_persistent = 0;
     int32_t last_ctas_per_sm = 0;
     std::map<TuneKey, Layout> tune;
 };
@@ -249,9 +251,21 @@ int smem_for_cap(int device, int cap) {
     return std::max(0, per_sm / cap - reserved) & ~255;
 }
 
-// Candidate layouts: every lanes-per-orbit, the register-capped variant where
-// one exists, and CTA-per-SM caps below the natural occupancy (waves shaped so
-// the last one is not mostly idle).
+int64_t cta_groups(const sdb_desc& d, int lanes) {
+    return (d.orbits * lanes + sdeb::kBlock - 1) / sdeb::kBlock;
+}
+
+// Persistent mode: slabs sized so the resident grid sees >= 32 rounds of
+// work items (the end-of-run imbalance is then < ~3%), and >= 16 steps each.
+int64_t slab_steps_for(int64_t total_steps, int64_t groups, int64_t grid) {
+    const int64_t rounds = 32;
+    const int64_t nslabs = std::max<int64_t>(1, (rounds * grid + groups - 1) / groups);
+    return std::max<int64_t>(16, (total_steps + nslabs - 1) / nslabs);
+}
+
+// Candidate layouts per lanes-per-orbit: natural occupancy; CTA-per-SM caps
+// below it that turn a ragged last wave into full ones; and the persistent
+// work-pulling grid (when there are enough CTA-groups to feed it).
 sdb_status candidate_layouts(sdb_ctx* ctx, const Slot& s, const sdb_desc& d, int kind_solver,
                              int kind_stream, std::vector<Layout>* out) {
     const int P = next_pow2(d.nequat);
@@ -269,9 +283,9 @@ sdb_status candidate_layouts(sdb_ctx* ctx, const Slot& s, const sdb_desc& d, int
         int occ = 0;
         SDB_CUDA(ctx, occupancy_run(J, kind_solver, kind_stream, d.coupling, padded, 0, &occ));
         if (occ < 1) continue;
-        const int64_t ctas = (d.orbits * L + sdeb::kBlock - 1) / sdeb::kBlock;
+        const int64_t ctas = cta_groups(d, L);
         out->push_back(Layout{L, 0, 0, occ});
-        // caps that turn a ragged last wave into full ones
+        if (ctas >= 2 * int64_t(sms) * occ) out->push_back(Layout{L, 1, 0, occ});
         for (int cap = occ - 1; cap >= 1 && cap >= occ - 4; --cap) {
             const double waves_cap = double(ctas) / (double(sms) * cap);
             const double waves_occ = double(ctas) / (double(sms) * occ);
@@ -288,9 +302,33 @@ sdb_status candidate_layouts(sdb_ctx* ctx, const Slot& s, const sdb_desc& d, int
     return SDB_OK;
 }
 
-// Pick the launch layout: cached, single candidate, or timed on a short probe
-// into scratch buffers.  Every layout gives bit-identical results (canonical
-// summation tree), so this only affects speed.
+// Fill the layout-dependent launch arguments; zeroes the persistent-mode
+// counters on `st` (one memset) when needed.
+sdb_status configure_layout(sdb_ctx* ctx, const Slot& s, DevBuf& work, const sdb_desc& d,
+                            const Layout& lay, int64_t total_steps, cudaStream_t st,
+                            sdeb::RunArgs* a) {
+    a->smem_pad = lay.smem;
+    a->groups = cta_groups(d, lay.lanes);
+    a->persistent = 0;
+    if (lay.persistent) {
+        int sms = 0;
+        SDB_CUDA(ctx, cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s.device));
+        const int64_t grid = int64_t(sms) * lay.ctas_per_sm;
+        const size_t bytes = sizeof(uint64_t) + size_t(a->groups) * sizeof(unsigned);
+        SDB_CUDA(ctx, work.ensure(bytes));
+        SDB_CUDA(ctx, cudaMemsetAsync(work.ptr, 0, bytes, st));
+        a->persistent = int(grid);
+        a->slab_steps = slab_steps_for(total_steps, a->groups, grid);
+        a->work_counter = work.as<uint64_t>();
+        a->slab_done = reinterpret_cast<unsigned*>(work.as<char>() + sizeof(uint64_t));
+    }
+    return SDB_OK;
+}
+
+// Pick the launch layout: cached, pinned (SDEB200_LAYOUT), single candidate,
+// or timed on a short probe into scratch buffers.  Every layout gives
+// bit-identical results (canonical summation tree, exact slab hand-off), so
+// this only affects speed.
 sdb_status choose_layout(sdb_ctx* ctx, Slot& s, const sdb_desc& d, const double* d_init,
                          const double* d_params, cudaStream_t st, Layout* out) {
     int kind_solver, kind_stream;
@@ -303,12 +341,17 @@ sdb_status choose_layout(sdb_ctx* ctx, Slot& s, const sdb_desc& d, const double*
         *out = it->second;
         return SDB_OK;
     }
-    // SDEB200_LAYOUT="lanes,tight,ctas_per_sm" pins the layout (profiling runs
-    // must not capture autotune probes); ctas_per_sm 0 = natural occupancy.
+    // SDEB200_LAYOUT="lanes,persistent,ctas_per_sm" pins the layout (profiling
+    // runs must not capture autotune probes); ctas_per_sm 0 = natural occupancy.
     if (const char* env = std::getenv("SDEB200_LAYOUT")) {
-        int L = 0, t = 0, cap = 0;
-        if (std::sscanf(env, "%d,%d,%d", &L, &t, &cap) >= 1 && L > 0) {
-            Layout lay{L, t, cap > 0 ? smem_for_cap(s.device, cap) : 0, cap};
+        int L = 0, pers = 0, cap = 0;
+        if (std::sscanf(env, "%d,%d,%d", &L, &pers, &cap) >= 1 && L > 0) {
+            const int P = next_pow2(d.nequat);
+            int occ = 0;
+            SDB_CUDA(ctx, occupancy_run(P / L, kind_solver, kind_stream, d.coupling,
+                                        d.nequat < P ? 1 : 0, 0, &occ));
+            Layout lay{L, pers, (cap > 0 && !pers) ? smem_for_cap(s.device, cap) : 0,
+                       cap > 0 ? cap : occ};
             ctx->tune[key] = lay;
             *out = lay;
             return SDB_OK;
@@ -345,24 +388,25 @@ sdb_status choose_layout(sdb_ctx* ctx, Slot& s, const sdb_desc& d, const double*
         a.rng_state = s.t_rng.as<uint64_t>();
         a.ksteps = probe;
         a.chunk_end = 1;
-        a.smem_pad = lay.smem;
         float ms_best = 1e30f;
         for (int rep = 0; rep < 2; ++rep) {
+            rc = configure_layout(ctx, s, s.t_work, d, lay, probe, st, &a);
+            if (rc != SDB_OK) break;
             cudaEventRecord(e0, st);
             cudaError_t e = launch_run(a, P / lay.lanes, kind_solver, kind_stream, d.coupling,
                                        d.nequat < P ? 1 : 0, st);
             cudaEventRecord(e1, st);
             if (e == cudaSuccess) e = cudaEventSynchronize(e1);
             if (e != cudaSuccess) {
-                cudaEventDestroy(e0);
-                cudaEventDestroy(e1);
-                return cuda_fail(ctx, e, "autotune launch");
+                rc = cuda_fail(ctx, e, "autotune launch");
+                break;
             }
             float ms = 0.f;
             cudaEventElapsedTime(&ms, e0, e1);
             ms_best = std::min(ms_best, ms);
             s.launches += 1;
         }
+        if (rc != SDB_OK) break;
         if (ms_best < best) {
             best = ms_best;
             best_l = lay;
@@ -370,6 +414,7 @@ sdb_status choose_layout(sdb_ctx* ctx, Slot& s, const sdb_desc& d, const double*
     }
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
+    if (rc != SDB_OK) return rc;
     ctx->tune[key] = best_l;
     *out = best_l;
     return SDB_OK;
@@ -393,14 +438,15 @@ sdb_status launch_device(sdb_ctx* ctx, Slot& s, const sdb_desc& d, const double*
     a.values = d_values;
     a.fail_step = d_fail;
     a.rng_state = s.rng.as<uint64_t>();
-    a.smem_pad = lay.smem;
+    rc = configure_layout(ctx, s, s.work, d, lay, d.chunks * d.ksteps, st, &a);
+    if (rc != SDB_OK) return rc;
     const int P = next_pow2(d.nequat);
     cudaError_t e = launch_run(a, P / lay.lanes, kind_solver, kind_stream, d.coupling,
                                d.nequat < P ? 1 : 0, st);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "kuramoto_run_kernel launch");
     s.launches += 1;
     s.lanes = lay.lanes;
-    s.tight = lay.tight;
+    s.persistent = lay.persistent;
     s.ctas_per_sm = lay.ctas_per_sm;
     return SDB_OK;
 }
@@ -501,8 +547,8 @@ void sdb_close(sdb_ctx* ctx) {
     if (!ctx) return;
     for (Slot& s : ctx->slots) {
         cudaSetDevice(s.device);
-        for (DevBuf* b : {&s.init, &s.params, &s.values, &s.state, &s.fail, &s.rng, &s.t_values,
-                          &s.t_state, &s.t_fail, &s.t_rng})
+        for (DevBuf* b : {&s.init, &s.params, &s.values, &s.state, &s.fail, &s.rng, &s.work,
+                          &s.t_values, &s.t_state, &s.t_fail, &s.t_rng, &s.t_work})
             b->release();
         if (s.stream) cudaStreamDestroy(s.stream);
     }
@@ -517,9 +563,10 @@ const char* sdb_last_error(const sdb_ctx* ctx) {
 int64_t sdb_last_launch_count(const sdb_ctx* ctx) { return ctx ? ctx->launches : 0; }
 int32_t sdb_last_lanes(const sdb_ctx* ctx) { return ctx ? ctx->last_lanes : 0; }
 
-void sdb_last_layout(const sdb_ctx* ctx, int32_t* lanes, int32_t* tight, int32_t* ctas_per_sm) {
+void sdb_last_layout(const sdb_ctx* ctx, int32_t* lanes, int32_t* persistent,
+                     int32_t* ctas_per_sm) {
     if (lanes) *lanes = ctx ? ctx->last_lanes : 0;
-    if (tight) *tight = ctx ? ctx->last_tight : 0;
+    if (persistent) *persistent = ctx ? ctx->last_persistent : 0;
     if (ctas_per_sm) *ctas_per_sm = ctx ? ctx->last_ctas_per_sm : 0;
 }
 
@@ -558,7 +605,7 @@ sdb_status sdb_run(sdb_ctx* ctx, const sdb_desc* desc, const double* init, const
     ctx->launches = 0;
     for (int64_t g = 0; g < used; ++g) ctx->launches += ctx->slots[g].launches;
     ctx->last_lanes = ctx->slots[0].lanes;
-    ctx->last_tight = ctx->slots[0].tight;
+    ctx->last_persistent = ctx->slots[0].persistent;
     ctx->last_ctas_per_sm = ctx->slots[0].ctas_per_sm;
     for (int64_t g = 0; g < used; ++g)
         if (status[g] != SDB_OK) return status[g];
@@ -581,7 +628,7 @@ sdb_status sdb_run_device(sdb_ctx* ctx, const sdb_desc* desc, const double* d_in
                        static_cast<cudaStream_t>(stream));
     ctx->launches = s.launches;
     ctx->last_lanes = s.lanes;
-    ctx->last_tight = s.tight;
+    ctx->last_persistent = s.persistent;
     ctx->last_ctas_per_sm = s.ctas_per_sm;
     return rc;
 }

@@ -47,6 +47,11 @@ struct RunArgs {
     int fresh;                // 1: fail=-1 and seed stateful streams in-kernel
     int check_finite;         // 1: run_batch failure semantics; 0: raw per-step API
     int smem_pad;             // dynamic shared memory per CTA (caps CTAs/SM; 0 = none)
+    int persistent;           // > 0: grid size of the work-pulling (slab, CTA-group) mode
+    int64_t groups;           // CTA-groups = ceil(orbits * lanes / kBlock)
+    int64_t slab_steps;       // steps per work item (persistent mode)
+    uint64_t* work_counter;   // persistent: zeroed item counter
+    unsigned* slab_done;      // persistent: [groups] published slabs, zeroed
 };
 
 __device__ __forceinline__ bool finite_bits(double x) {
@@ -251,17 +256,19 @@ __device__ __forceinline__ void step_noise_apply(const RunArgs& a, int64_t row, 
 
 // ---- the fused run kernel ----------------------------------------------------
 
-// PADDED = (n < lanes * J): instantiated with and without padding handling.
+// One work item: CTA-group `cg` (kBlock/L orbits) advanced over the absolute
+// steps [s0, s1).  first = this item starts the run (state from state_in,
+// rng seeded / loaded per a.fresh); otherwise the state saved by the previous
+// slab is resumed from state_out / rng_state / fail_step.  Saving and resuming
+// are exact, so any slab split gives bit-identical results.
 template <int J, int SOLVER, int STREAM, int COUPLING, bool PADDED>
-__global__ void __launch_bounds__(kBlock) kuramoto_run_kernel(const RunArgs a) {
+__device__ __forceinline__ void run_item(const RunArgs& a, int64_t cg, uint64_t s0, uint64_t s1,
+                                         bool first, double* sh, double* shs) {
     constexpr bool kStochastic = (SOLVER == KS_EM) && (STREAM != KS_NONE);
     constexpr bool kStateful = kStochastic && (STREAM == KS_SFC64 || STREAM == KS_XOSHIRO);
     constexpr int NB = blocks_per_lane<J>();
-    extern __shared__ double smem[];
-    double* sh = smem;                  // pairwise: [J][kBlock]
-    double* shs = smem + J * kBlock;    // pairwise L==1: [J][kBlock]
 
-    const int64_t gtid = int64_t(blockIdx.x) * kBlock + threadIdx.x;
+    const int64_t gtid = cg * kBlock + threadIdx.x;
     const int lanes = a.lanes;
     const int64_t group = gtid >> a.log2lanes;
     const int lane = int(gtid & (lanes - 1));
@@ -274,11 +281,12 @@ __global__ void __launch_bounds__(kBlock) kuramoto_run_kernel(const RunArgs a) {
     double y[J], om[J], sg[J];
     const double* prow = a.params + row * a.nparams;
     const double kn = __ddiv_rn(__ldg(prow), double(n));  // np.divide(p[...,0:1], float(n))
+    const double* src = first ? a.state_in : a.state_out;
 #pragma unroll
     for (int q = 0; q < J; ++q) {
         const int i = base + q;
         const bool valid = i < n;
-        y[q] = valid ? a.state_in[row * n + i] : 0.0;
+        y[q] = valid ? src[row * n + i] : 0.0;
         om[q] = valid ? __ldg(prow + 1 + i) : 0.0;
         sg[q] = (kStochastic && valid) ? __ldg(prow + 1 + n + i) : 0.0;
     }
@@ -293,7 +301,8 @@ __global__ void __launch_bounds__(kBlock) kuramoto_run_kernel(const RunArgs a) {
         }
         return;
     } else {
-        int64_t fail = (a.fresh || a.fail_step == nullptr) ? -1 : a.fail_step[row];
+        const bool fresh = first && a.fresh;
+        int64_t fail = (fresh || a.fail_step == nullptr) ? -1 : a.fail_step[row];
         const int nblocks = (a.nnoise + 3) / 4;
 
         StreamState rs[NB];
@@ -302,7 +311,7 @@ __global__ void __launch_bounds__(kBlock) kuramoto_run_kernel(const RunArgs a) {
             for (int t = 0; t < NB; ++t) {
                 const int b = base / 4 + t;
                 if (b < nblocks) {
-                    if (a.fresh) {
+                    if (fresh) {
                         rs[t] = stream_init<STREAM>(a.seed, uint64_t(orbit_g), uint64_t(b));
                     } else {
                         const uint64_t* p = a.rng_state + (row * nblocks + b) * 4;
@@ -314,77 +323,80 @@ __global__ void __launch_bounds__(kBlock) kuramoto_run_kernel(const RunArgs a) {
             }
         }
 
-        uint64_t step = uint64_t(a.chunk_begin) * uint64_t(a.ksteps);
         const double dt = a.dt;
-        for (int64_t c = a.chunk_begin; c < a.chunk_end; ++c) {
-            for (int64_t ls = 0; ls < a.ksteps; ++ls, ++step) {
-                if constexpr (SOLVER == KS_EM) {
-                    double f[J];
-                    if constexpr (kStochastic) {
-                        drift<J, COUPLING, PADDED>(y, om, kn, base, n, lanes, sh, shs, f);
-                        // (y + f*dt) + sqrt(dt) * (s_i * N_i)   (solvers.py:70-71, model.py:201)
-                        step_noise_apply<J, STREAM, PADDED>(
-                            a, row, orbit_g, step, base, rs, [&](int q, double z) {
-                                const double g = __dmul_rn(sg[q], z);
-                                y[q] = __dadd_rn(__dadd_rn(y[q], __dmul_rn(f[q], dt)),
-                                                 __dmul_rn(a.sqrt_dt, g));
-                            });
-                    } else {
-                        drift<J, COUPLING, PADDED>(y, om, kn, base, n, lanes, sh, shs, f);
+        const uint64_t ks = uint64_t(a.ksteps);
+        uint64_t to_sample = ks - s0 % ks;  // steps until the next chunk end
+        for (uint64_t step = s0; step < s1; ++step) {
+            if constexpr (SOLVER == KS_EM) {
+                double f[J];
+                if constexpr (kStochastic) {
+                    drift<J, COUPLING, PADDED>(y, om, kn, base, n, lanes, sh, shs, f);
+                    // (y + f*dt) + sqrt(dt) * (s_i * N_i)   (solvers.py:70-71, model.py:201)
+                    step_noise_apply<J, STREAM, PADDED>(
+                        a, row, orbit_g, step, base, rs, [&](int q, double z) {
+                            const double g = __dmul_rn(sg[q], z);
+                            y[q] = __dadd_rn(__dadd_rn(y[q], __dmul_rn(f[q], dt)),
+                                             __dmul_rn(a.sqrt_dt, g));
+                        });
+                } else {
+                    drift<J, COUPLING, PADDED>(y, om, kn, base, n, lanes, sh, shs, f);
 #pragma unroll
-                        for (int q = 0; q < J; ++q) y[q] = __dadd_rn(y[q], __dmul_rn(f[q], dt));
-                    }
-                } else {  // KS_RK4 (solvers.py:80-88)
-                    double k[J], acc[J], ys[J];
-                    drift<J, COUPLING, PADDED>(y, om, kn, base, n, lanes, sh, shs, k);  // k1
-#pragma unroll
-                    for (int q = 0; q < J; ++q) {
-                        acc[q] = k[q];
-                        ys[q] = __dadd_rn(y[q], __dmul_rn(a.half_dt, k[q]));
-                    }
-                    drift<J, COUPLING, PADDED>(ys, om, kn, base, n, lanes, sh, shs, k);  // k2
-#pragma unroll
-                    for (int q = 0; q < J; ++q) {
-                        acc[q] = __dadd_rn(acc[q], __dmul_rn(2.0, k[q]));
-                        ys[q] = __dadd_rn(y[q], __dmul_rn(a.half_dt, k[q]));
-                    }
-                    drift<J, COUPLING, PADDED>(ys, om, kn, base, n, lanes, sh, shs, k);  // k3
-#pragma unroll
-                    for (int q = 0; q < J; ++q) {
-                        acc[q] = __dadd_rn(acc[q], __dmul_rn(2.0, k[q]));
-                        ys[q] = __dadd_rn(y[q], __dmul_rn(dt, k[q]));
-                    }
-                    drift<J, COUPLING, PADDED>(ys, om, kn, base, n, lanes, sh, shs, k);  // k4
-#pragma unroll
-                    for (int q = 0; q < J; ++q) {
-                        acc[q] = __dadd_rn(acc[q], k[q]);
-                        y[q] = __dadd_rn(y[q], __dmul_rn(a.dt6, acc[q]));
-                    }
+                    for (int q = 0; q < J; ++q) y[q] = __dadd_rn(y[q], __dmul_rn(f[q], dt));
                 }
-                // isfinite(y).all(-1) per orbit; first failure recorded, row -> NaN
-                // (engine.py:281-298).  Lanes record independently; the group
-                // minimum is the orbit's first failing step.
-                bool bad = false;
+            } else {  // KS_RK4 (solvers.py:80-88)
+                double k[J], acc[J], ys[J];
+                drift<J, COUPLING, PADDED>(y, om, kn, base, n, lanes, sh, shs, k);  // k1
 #pragma unroll
-                // (padding oscillators stay 0: no validity predicate needed)
-                for (int q = 0; q < J; ++q) bad |= !finite_bits(y[q]);
-                if (bad && a.check_finite) {
-                    if (fail < 0) fail = int64_t(step);
+                for (int q = 0; q < J; ++q) {
+                    acc[q] = k[q];
+                    ys[q] = __dadd_rn(y[q], __dmul_rn(a.half_dt, k[q]));
+                }
+                drift<J, COUPLING, PADDED>(ys, om, kn, base, n, lanes, sh, shs, k);  // k2
 #pragma unroll
-                    for (int q = 0; q < J; ++q) y[q] = CUDART_NAN;
+                for (int q = 0; q < J; ++q) {
+                    acc[q] = __dadd_rn(acc[q], __dmul_rn(2.0, k[q]));
+                    ys[q] = __dadd_rn(y[q], __dmul_rn(a.half_dt, k[q]));
+                }
+                drift<J, COUPLING, PADDED>(ys, om, kn, base, n, lanes, sh, shs, k);  // k3
+#pragma unroll
+                for (int q = 0; q < J; ++q) {
+                    acc[q] = __dadd_rn(acc[q], __dmul_rn(2.0, k[q]));
+                    ys[q] = __dadd_rn(y[q], __dmul_rn(dt, k[q]));
+                }
+                drift<J, COUPLING, PADDED>(ys, om, kn, base, n, lanes, sh, shs, k);  // k4
+#pragma unroll
+                for (int q = 0; q < J; ++q) {
+                    acc[q] = __dadd_rn(acc[q], k[q]);
+                    y[q] = __dadd_rn(y[q], __dmul_rn(a.dt6, acc[q]));
                 }
             }
-            // one sample per chunk (engine.py:299)
-            const int64_t gf = group_fail(fail, lanes);
-            if (gf >= 0 && a.check_finite) {
+            // isfinite(y).all(-1) per orbit; first failure recorded, row -> NaN
+            // (engine.py:281-298).  Lanes record independently; the group
+            // minimum is the orbit's first failing step.  Padding oscillators
+            // stay 0, so no validity predicate is needed.
+            bool bad = false;
+#pragma unroll
+            for (int q = 0; q < J; ++q) bad |= !finite_bits(y[q]);
+            if (bad && a.check_finite) {
+                if (fail < 0) fail = int64_t(step);
 #pragma unroll
                 for (int q = 0; q < J; ++q) y[q] = CUDART_NAN;
             }
-            if (active) {
-                double* out = a.values + (row * a.vstride + (c - a.chunk_begin)) * n + base;
+            if (--to_sample == 0) {
+                // one sample per chunk (engine.py:299)
+                to_sample = ks;
+                const int64_t gf = group_fail(fail, lanes);
+                if (gf >= 0 && a.check_finite) {
 #pragma unroll
-                for (int q = 0; q < J; ++q)
-                    if (base + q < n) out[q] = y[q];
+                    for (int q = 0; q < J; ++q) y[q] = CUDART_NAN;
+                }
+                if (active) {
+                    const int64_t c = int64_t((step + 1) / ks) - 1;
+                    double* out = a.values + (row * a.vstride + (c - a.chunk_begin)) * n + base;
+#pragma unroll
+                    for (int q = 0; q < J; ++q)
+                        if (base + q < n) out[q] = y[q];
+                }
             }
         }
 
@@ -412,6 +424,60 @@ __global__ void __launch_bounds__(kBlock) kuramoto_run_kernel(const RunArgs a) {
                 }
             }
         }
+    }
+}
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" : : "l"(p), "r"(v) : "memory");
+}
+
+// Non-persistent: CTA b advances CTA-group b over the whole launch range.
+// Persistent (a.persistent): a grid of exactly the resident CTAs pulls work
+// items w = slab * groups + cg from a global counter; slab k of a group waits
+// (acquire) for slab k-1 to be published (release).  The smallest in-flight
+// item's predecessor is always complete, so this cannot deadlock, and the
+// run ends within one slab of perfectly balanced: no partially-filled last
+// wave (the v3 profile lost ~13-23% to wave quantisation).
+// PADDED = (n < lanes * J): instantiated with and without padding handling.
+template <int J, int SOLVER, int STREAM, int COUPLING, bool PADDED>
+__global__ void __launch_bounds__(kBlock) kuramoto_run_kernel(const RunArgs a) {
+    extern __shared__ double smem[];
+    double* sh = smem;                  // pairwise: [J][kBlock]
+    double* shs = smem + J * kBlock;    // pairwise L==1: [J][kBlock]
+    const uint64_t begin = uint64_t(a.chunk_begin) * uint64_t(a.ksteps);
+    const uint64_t end = uint64_t(a.chunk_end) * uint64_t(a.ksteps);
+    if (!a.persistent) {
+        run_item<J, SOLVER, STREAM, COUPLING, PADDED>(a, blockIdx.x, begin, end, true, sh, shs);
+        return;
+    }
+    __shared__ int64_t item;
+    const uint64_t slab = uint64_t(a.slab_steps);
+    const int64_t nslabs = int64_t((end - begin + slab - 1) / slab);
+    const int64_t total = nslabs * a.groups;
+    for (;;) {
+        if (threadIdx.x == 0) item = int64_t(atomicAdd(reinterpret_cast<unsigned long long*>(a.work_counter), 1ull));
+        __syncthreads();
+        const int64_t w = item;
+        __syncthreads();
+        if (w >= total) break;
+        const int64_t cg = w % a.groups;
+        const int64_t k = w / a.groups;
+        if (k > 0 && threadIdx.x == 0) {
+            while (ld_acquire(a.slab_done + cg) < unsigned(k)) __nanosleep(256);
+        }
+        __syncthreads();
+        const uint64_t s0 = begin + uint64_t(k) * slab;
+        const uint64_t s1 = s0 + slab < end ? s0 + slab : end;
+        run_item<J, SOLVER, STREAM, COUPLING, PADDED>(a, cg, s0, s1, k == 0, sh, shs);
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) st_release(a.slab_done + cg, unsigned(k + 1));
     }
 }
 

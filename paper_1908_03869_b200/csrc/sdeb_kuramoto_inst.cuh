@@ -8,7 +8,8 @@ namespace sdeb {
 template <int J, int S, int R, int C, bool P>
 static cudaError_t launch_one(const RunArgs& a, cudaStream_t st) {
     const int64_t threads = a.orbits * int64_t(a.lanes);
-    const unsigned grid = unsigned((threads + kBlock - 1) / kBlock);
+    const unsigned grid = a.persistent > 0 ? unsigned(a.persistent)
+                                           : unsigned((threads + kBlock - 1) / kBlock);
     const size_t need = pairwise_smem_bytes(J, C);
     const size_t smem = need > size_t(a.smem_pad) ? need : size_t(a.smem_pad);
     if (smem > 48 * 1024) {

@@ -320,3 +320,49 @@ def test_launch_accounting():
                                                   lanes=2), b)
     info = last_launch_info()
     assert info["launches"] == 1 and info["lanes"] == 2
+
+
+def _run_pinned(layout, n, batch, cfg):
+    """run_batch through a fresh context with SDEB200_LAYOUT pinned."""
+    import ctypes
+    import os
+
+    from paper_1908_03869_b200 import _native as nat
+    from paper_1908_03869_b200.engine import make_desc
+    os.environ["SDEB200_LAYOUT"] = layout
+    try:
+        ctx = ctypes.c_void_p()
+        nat.check(nat.lib().sdb_open(None, 0, ctypes.byref(ctx)))
+        chunks = sdb.iteration_count(cfg.tspan, cfg.dt, cfg.ksteps)
+        desc = make_desc(sdb.kuramoto_model(n), cfg, chunks, batch.orbits)
+        values = np.empty((batch.orbits, chunks + 1, n))
+        fail = np.empty(batch.orbits, np.int64)
+        init, params = nat.f64(batch.init), nat.f64(batch.params)
+        nat.check(nat.lib().sdb_run(ctx, desc, nat.dptr(init), nat.dptr(params),
+                                    nat.dptr(values), nat.i64ptr(fail)), ctx)
+        nat.lib().sdb_close(ctx)
+        return values, fail
+    finally:
+        del os.environ["SDEB200_LAYOUT"]
+
+
+@pytest.mark.parametrize("stream", ["philox", "sfc64"])
+@pytest.mark.parametrize("n", [16, 12])
+def test_persistent_slab_schedule_bit_identical(n, stream):
+    # the work-pulling grid hands each orbit group over between CTAs every
+    # 16-step slab (samples every 50 steps fall mid-slab): must be bitwise
+    # identical to one CTA per group, for padded and unpadded n
+    m = 2000
+    batch = sdb.sample_kuramoto_batch(n, m, (0.2, 0.4), (0.01, 0.1), 0.3, seed=4)
+    params = batch.params.copy()
+    params[7, 1 + 3] = 1e308  # orbit 7 fails mid-run: failure + NaN fill across slabs
+    params[7, 0] = 0.0
+    batch = OrbitBatch(init=batch.init, params=params)
+    cfg = EngineConfig(dt=1e-2, tspan=3.0, ksteps=50, orbits=m, seed=9, stream=stream)
+    lanes = 4
+    ref, ref_fail = _run_pinned("%d,0,0" % lanes, n, batch, cfg)
+    got, got_fail = _run_pinned("%d,1,0" % lanes, n, batch, cfg)
+    assert np.array_equal(ref, got, equal_nan=True)
+    assert np.array_equal(ref_fail, got_fail) and ref_fail[7] >= 0
+    capped, _ = _run_pinned("%d,0,2" % lanes, n, batch, cfg)
+    assert np.array_equal(ref, capped, equal_nan=True)

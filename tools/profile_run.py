@@ -31,11 +31,11 @@ def main():
     ap.add_argument("--lanes", type=int, default=0)
     ap.add_argument("--coupling", default="meanfield")
     ap.add_argument("--repeat", type=int, default=1)
-    ap.add_argument("--tight", type=int, default=0)
+    ap.add_argument("--persistent", type=int, default=0)
     ap.add_argument("--ctas", type=int, default=0)
     args = ap.parse_args()
     if args.lanes:
-        os.environ["SDEB200_LAYOUT"] = "%d,%d,%d" % (args.lanes, args.tight, args.ctas)
+        os.environ["SDEB200_LAYOUT"] = "%d,%d,%d" % (args.lanes, args.persistent, args.ctas)
     w = dict(bench.WORKLOADS[args.workload])
     if args.steps:
         w["steps"] = args.steps
