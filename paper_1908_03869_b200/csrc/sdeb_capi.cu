@@ -293,9 +293,15 @@ sdb_status candidate_layouts(sdb_ctx* ctx, const Slot& s, const sdb_desc& d, int
             const double eff_occ = waves_occ / std::ceil(waves_occ);
             if (eff_cap <= eff_occ + 0.02) continue;
             const int smem = smem_for_cap(s.device, cap);
+            int optin = 0;
+            cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, s.device);
+            if (smem <= 0 || smem > optin) continue;
             int got = 0;
-            SDB_CUDA(ctx, occupancy_run(J, kind_solver, kind_stream, d.coupling, padded,
-                                        size_t(smem), &got));
+            if (occupancy_run(J, kind_solver, kind_stream, d.coupling, padded, size_t(smem),
+                              &got) != cudaSuccess) {
+                cudaGetLastError();  // not sticky: drop it so later launches see a clean slate
+                continue;
+            }
             if (got == cap) out->push_back(Layout{L, 0, smem, cap});
         }
     }

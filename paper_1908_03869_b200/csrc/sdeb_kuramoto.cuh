@@ -325,8 +325,13 @@ __device__ __forceinline__ void run_item(const RunArgs& a, int64_t cg, uint64_t 
 
         const double dt = a.dt;
         const uint64_t ks = uint64_t(a.ksteps);
-        uint64_t to_sample = ks - s0 % ks;  // steps until the next chunk end
-        for (uint64_t step = s0; step < s1; ++step) {
+        // Segments between chunk ends: the sample write sits outside the hot
+        // inner loop (a branch inside it cost ~40 registers of scheduling).
+        uint64_t next_sample = (s0 / ks + 1) * ks;  // exclusive end of s0's chunk
+        uint64_t step = s0;
+        while (step < s1) {
+          const uint64_t seg_end = next_sample < s1 ? next_sample : s1;
+          for (; step < seg_end; ++step) {
             if constexpr (SOLVER == KS_EM) {
                 double f[J];
                 if constexpr (kStochastic) {
@@ -382,16 +387,17 @@ __device__ __forceinline__ void run_item(const RunArgs& a, int64_t cg, uint64_t 
 #pragma unroll
                 for (int q = 0; q < J; ++q) y[q] = CUDART_NAN;
             }
-            if (--to_sample == 0) {
+            }
+            if (step == next_sample) {
                 // one sample per chunk (engine.py:299)
-                to_sample = ks;
+                next_sample += ks;
                 const int64_t gf = group_fail(fail, lanes);
                 if (gf >= 0 && a.check_finite) {
 #pragma unroll
                     for (int q = 0; q < J; ++q) y[q] = CUDART_NAN;
                 }
                 if (active) {
-                    const int64_t c = int64_t((step + 1) / ks) - 1;
+                    const int64_t c = int64_t(step / ks) - 1;
                     double* out = a.values + (row * a.vstride + (c - a.chunk_begin)) * n + base;
 #pragma unroll
                     for (int q = 0; q < J; ++q)
@@ -452,29 +458,33 @@ __global__ void __launch_bounds__(kBlock) kuramoto_run_kernel(const RunArgs a) {
     double* shs = smem + J * kBlock;    // pairwise L==1: [J][kBlock]
     const uint64_t begin = uint64_t(a.chunk_begin) * uint64_t(a.ksteps);
     const uint64_t end = uint64_t(a.chunk_end) * uint64_t(a.ksteps);
-    if (!a.persistent) {
-        run_item<J, SOLVER, STREAM, COUPLING, PADDED>(a, blockIdx.x, begin, end, true, sh, shs);
-        return;
-    }
+    // One run_item call site for both modes (two inlined copies cost ~40
+    // registers): the non-persistent mode is the one-item-per-CTA special case.
     __shared__ int64_t item;
-    const uint64_t slab = uint64_t(a.slab_steps);
-    const int64_t nslabs = int64_t((end - begin + slab - 1) / slab);
+    const bool persistent = a.persistent > 0;
+    const uint64_t slab = persistent ? uint64_t(a.slab_steps) : end - begin;
+    const int64_t nslabs = persistent ? int64_t((end - begin + slab - 1) / slab) : 1;
     const int64_t total = nslabs * a.groups;
+    int64_t w = blockIdx.x;
     for (;;) {
-        if (threadIdx.x == 0) item = int64_t(atomicAdd(reinterpret_cast<unsigned long long*>(a.work_counter), 1ull));
-        __syncthreads();
-        const int64_t w = item;
-        __syncthreads();
+        if (persistent) {
+            if (threadIdx.x == 0)
+                item = int64_t(atomicAdd(reinterpret_cast<unsigned long long*>(a.work_counter), 1ull));
+            __syncthreads();
+            w = item;
+            __syncthreads();
+        }
         if (w >= total) break;
         const int64_t cg = w % a.groups;
         const int64_t k = w / a.groups;
         if (k > 0 && threadIdx.x == 0) {
             while (ld_acquire(a.slab_done + cg) < unsigned(k)) __nanosleep(256);
         }
-        __syncthreads();
+        if (persistent) __syncthreads();
         const uint64_t s0 = begin + uint64_t(k) * slab;
         const uint64_t s1 = s0 + slab < end ? s0 + slab : end;
         run_item<J, SOLVER, STREAM, COUPLING, PADDED>(a, cg, s0, s1, k == 0, sh, shs);
+        if (!persistent) break;
         __threadfence();
         __syncthreads();
         if (threadIdx.x == 0) st_release(a.slab_done + cg, unsigned(k + 1));
