@@ -234,6 +234,7 @@ sdeb::RunArgs make_args(const sdb_desc& d, int lanes) {
     a.vstride = d.chunks;
     a.fresh = 1;
     a.check_finite = 1;
+    a.groups = (d.orbits * lanes + sdeb::kBlock - 1) / sdeb::kBlock;  // one CTA per group
     return a;
 }
 
