@@ -135,3 +135,55 @@ def test_emulated_log_within_1ulp_on_box_muller_uniforms():
 @pytest.mark.parametrize("x", [0.5, 0.75, 0.99999, 1.0, 1.5, 2.0, 44.0])
 def test_emulated_log_general_points(x):
     assert ulps(emu_log(x), math.log(x)) <= 1.0
+
+
+def _sincos_table():
+    text = open(os.path.join(CSRC, "sdeb_sincos_table.cuh")).read()
+    return [(_dbl(int(a, 16)), _dbl(int(b, 16)))
+            for a, b in re.findall(r"\{0x([0-9A-F]+)ULL, 0x([0-9A-F]+)ULL\}", text)]
+
+
+SCT = _sincos_table()
+
+
+def emu_sincos_tab(x):
+    t = fma(x, C["MC_128_OVER_PI"], MAGIC)
+    k = _bits(t) & 0xFFFFFFFF
+    kd = t - MAGIC
+    r = fma(-kd, C["MC_PI128_1"], x)
+    r = fma(-kd, C["MC_PI128_2"], r)
+    r = fma(-kd, C["MC_PI128_3"], r)
+    sa, ca = SCT[k & 255]
+    r2 = r * r
+    ps = fma(r2, C["MC_T_S7"], C["MC_T_S5"])
+    ps = fma(r2, ps, C["MC_T_S3"])
+    sr = fma(r2 * r, ps, r)
+    pc = fma(r2, C["MC_T_C6"], C["MC_T_C4"])
+    pc = fma(r2, pc, -0.5)
+    cr = fma(r2, pc, 1.0)
+    return fma(sa, cr, ca * sr), fma(ca, cr, -(sa * sr))
+
+
+def test_table_sincos_constants():
+    from decimal import Decimal, getcontext
+    getcontext().prec = 50
+    pi = Decimal("3.14159265358979323846264338327950288419716939937510582097494")
+    split = Decimal(C["MC_PI128_1"]) + Decimal(C["MC_PI128_2"]) + Decimal(C["MC_PI128_3"])
+    assert abs(split - pi / 128) < Decimal(10) ** -45
+    assert C["MC_PI128_1"] == math.pi / 128
+    assert len(SCT) == 256 and SCT[0] == (0.0, 1.0) and SCT[64] == (1.0, 0.0)
+    for k in range(1, 256):
+        assert SCT[256 - k][0] == -SCT[k][0] and SCT[256 - k][1] == SCT[k][1]
+
+
+def test_emulated_table_sincos_within_2ulp_and_odd():
+    g = np.random.default_rng(7)
+    xs = list(g.uniform(-np.pi, np.pi, 1500)) + list(g.uniform(-2e3, 2e3, 1500)) + \
+        list(g.uniform(0, 2 * np.pi, 500)) + [k * math.pi / 128 for k in range(-300, 301, 7)] + \
+        [0.0, 1e-300, 3.0e8, 2 * math.pi]
+    for x in xs:
+        s, c = emu_sincos_tab(float(x))
+        assert ulps(s, math.sin(x)) <= 2 or abs(s - math.sin(x)) <= 2.3e-16, x
+        assert ulps(c, math.cos(x)) <= 2 or abs(c - math.cos(x)) <= 2.3e-16, x
+        ns, nc = emu_sincos_tab(-float(x))
+        assert ns == -s and nc == c, x
