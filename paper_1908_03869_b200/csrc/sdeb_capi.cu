@@ -373,7 +373,9 @@ sdb_status choose_layout(sdb_ctx* ctx, Slot& s, const sdb_desc& d, const double*
         ctx->tune[key] = cands[0];
         return SDB_OK;
     }
-    const int64_t probe = std::min<int64_t>(total, 128);
+    // Probe ~5% of the run (128..512 steps): long enough that wave effects and
+    // the persistent grid's balance show as they will in the real run.
+    const int64_t probe = std::min<int64_t>(total, std::max<int64_t>(128, std::min<int64_t>(512, total / 20)));
     SDB_CUDA(ctx, s.t_values.ensure(size_t(d.orbits) * d.nequat * sizeof(double)));
     SDB_CUDA(ctx, s.t_state.ensure(size_t(d.orbits) * d.nequat * sizeof(double)));
     SDB_CUDA(ctx, s.t_fail.ensure(size_t(d.orbits) * sizeof(int64_t)));
@@ -398,6 +400,8 @@ sdb_status choose_layout(sdb_ctx* ctx, Slot& s, const sdb_desc& d, const double*
         float ms_best = 1e30f;
         for (int rep = 0; rep < 2; ++rep) {
             rc = configure_layout(ctx, s, s.t_work, d, lay, probe, st, &a);
+            // probe slabs: >= 32 steps so per-item overhead is not overstated
+            if (a.persistent) a.slab_steps = std::max<int64_t>(32, probe / 8);
             if (rc != SDB_OK) break;
             cudaEventRecord(e0, st);
             cudaError_t e = launch_run(a, P / lay.lanes, kind_solver, kind_stream, d.coupling,
