@@ -67,20 +67,24 @@ WORKLOADS = {
 }
 
 
+SINCOS_OPS = 17      # csrc/sdeb_math.cuh sincos_tab: 5 reduction + 8 poly + 4 rotation
+BOX_MULLER_PAIR = 44  # 2 uniforms, log 13, -2*log 1, sqrt 8, angle 1, sincos 17, 2 products
+
+
 def algorithmic_fp64_ops(n: int, solver: str, coupling: str) -> float:
-    """FP64 lane-ops per orbit-step of the algorithm the kernel runs
-    (per-function costs = libdevice fast paths on
-    sm_100a as counted in SURVEY.md 8d): sincos 22, sin 15, Box-Muller 35 per
-    normal, EM update 5 per oscillator, coupling accumulate 2 per term."""
+    """FP64 lane-ops (DFMA/DMUL/DADD/DSETP) per orbit-step of the algorithm the
+    kernel runs, counted from the device code:
+    meanfield drift 24/oscillator (sincos 17, sums 2, S_i 3, f_i 2); pairwise
+    drift 20 per unordered pair (difference, sincos, 2 accumulates) + 2/osc;
+    Box-Muller 44 per pair of normals; EM update 5/osc; RK4 4 drifts + 13/osc."""
     if coupling == "meanfield":
-        drift = n * (22 + 2 + 2 + 2)           # sincos, 2 sums, S_i, f_i
+        drift = n * (SINCOS_OPS + 2 + 3 + 2)
     else:
-        pairs = n * (n - 1) / 2
-        drift = pairs * 18 + n * 2             # diff + sin + 2 accumulates; f_i
+        drift = n * (n - 1) / 2 * (SINCOS_OPS + 3) + n * 2
     if solver == "rk4":
-        return 4 * drift + n * 9               # 4 stages + stage/accumulate updates
+        return 4 * drift + n * 13
     if solver == "em":
-        return drift + n * (35 + 5)
+        return drift + n * (BOX_MULLER_PAIR / 2 + 5)
     return drift + n * 2
 
 

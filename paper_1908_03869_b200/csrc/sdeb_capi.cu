@@ -60,6 +60,7 @@ struct Slot {
     int32_t lanes = 0;
     int32_t persistent = 0;
     int32_t ctas_per_sm = 0;
+    int32_t tight = 0;
     std::string error;
 };
 
@@ -71,6 +72,7 @@ struct Layout {
     int persistent = 0;
     int smem = 0;
     int ctas_per_sm = 0;
+    int tight = 0;  // register-capped kernel variant (unpadded meanfield, J in {4, 8})
 };
 
 using TuneKey = std::tuple<int, int, int, int, int, int64_t, int, int>;
@@ -252,6 +254,13 @@ int smem_for_cap(int device, int cap) {
     return std::max(0, per_sm / cap - reserved) & ~255;
 }
 
+// Kernel instantiation variant: 1 padded (n < next_pow2(n)), else 0, or 2
+// for the register-capped unpadded form.
+int kernel_variant(const sdb_desc& d, int tight) {
+    if (d.nequat < next_pow2(d.nequat)) return 1;
+    return tight ? 2 : 0;
+}
+
 int64_t cta_groups(const sdb_desc& d, int lanes) {
     return (d.orbits * lanes + sdeb::kBlock - 1) / sdeb::kBlock;
 }
@@ -279,14 +288,18 @@ sdb_status candidate_layouts(sdb_ctx* ctx, const Slot& s, const sdb_desc& d, int
         for (int L : candidate_lanes(d.nequat)) lanes_list.push_back(L);
     }
     for (int L : lanes_list) {
-        const int J = P / L;
-        const int padded = d.nequat < P ? 1 : 0;
+      const int J = P / L;
+      const bool can_tight = d.nequat == P && d.coupling == SDB_COUPLING_MEANFIELD &&
+                             (J == 4 || J == 8);
+      for (int tight = 0; tight <= (can_tight ? 1 : 0); ++tight) {
+        const int padded = kernel_variant(d, tight);
         int occ = 0;
         SDB_CUDA(ctx, occupancy_run(J, kind_solver, kind_stream, d.coupling, padded, 0, &occ));
         if (occ < 1) continue;
         const int64_t ctas = cta_groups(d, L);
-        out->push_back(Layout{L, 0, 0, occ});
-        if (ctas >= 2 * int64_t(sms) * occ) out->push_back(Layout{L, 1, 0, occ});
+        out->push_back(Layout{L, 0, 0, occ, tight});
+        if (ctas >= 2 * int64_t(sms) * occ) out->push_back(Layout{L, 1, 0, occ, tight});
+        if (tight) continue;
         for (int cap = occ - 1; cap >= 1 && cap >= occ - 4; --cap) {
             const double waves_cap = double(ctas) / (double(sms) * cap);
             const double waves_occ = double(ctas) / (double(sms) * occ);
@@ -303,8 +316,9 @@ sdb_status candidate_layouts(sdb_ctx* ctx, const Slot& s, const sdb_desc& d, int
                 cudaGetLastError();  // not sticky: drop it so later launches see a clean slate
                 continue;
             }
-            if (got == cap) out->push_back(Layout{L, 0, smem, cap});
+            if (got == cap) out->push_back(Layout{L, 0, smem, cap, 0});
         }
+      }
     }
     return SDB_OK;
 }
@@ -348,17 +362,18 @@ sdb_status choose_layout(sdb_ctx* ctx, Slot& s, const sdb_desc& d, const double*
         *out = it->second;
         return SDB_OK;
     }
-    // SDEB200_LAYOUT="lanes,persistent,ctas_per_sm" pins the layout (profiling
-    // runs must not capture autotune probes); ctas_per_sm 0 = natural occupancy.
+    // SDEB200_LAYOUT="lanes,persistent,ctas_per_sm[,tight]" pins the layout
+    // (profiling runs must not capture autotune probes); ctas_per_sm 0 =
+    // natural occupancy.
     if (const char* env = std::getenv("SDEB200_LAYOUT")) {
-        int L = 0, pers = 0, cap = 0;
-        if (std::sscanf(env, "%d,%d,%d", &L, &pers, &cap) >= 1 && L > 0) {
+        int L = 0, pers = 0, cap = 0, tight = 0;
+        if (std::sscanf(env, "%d,%d,%d,%d", &L, &pers, &cap, &tight) >= 1 && L > 0) {
             const int P = next_pow2(d.nequat);
             int occ = 0;
             SDB_CUDA(ctx, occupancy_run(P / L, kind_solver, kind_stream, d.coupling,
-                                        d.nequat < P ? 1 : 0, 0, &occ));
+                                        kernel_variant(d, tight), 0, &occ));
             Layout lay{L, pers, (cap > 0 && !pers) ? smem_for_cap(s.device, cap) : 0,
-                       cap > 0 ? cap : occ};
+                       cap > 0 ? cap : occ, tight};
             ctx->tune[key] = lay;
             *out = lay;
             return SDB_OK;
@@ -405,7 +420,7 @@ sdb_status choose_layout(sdb_ctx* ctx, Slot& s, const sdb_desc& d, const double*
             if (rc != SDB_OK) break;
             cudaEventRecord(e0, st);
             cudaError_t e = launch_run(a, P / lay.lanes, kind_solver, kind_stream, d.coupling,
-                                       d.nequat < P ? 1 : 0, st);
+                                       kernel_variant(d, lay.tight), st);
             cudaEventRecord(e1, st);
             if (e == cudaSuccess) e = cudaEventSynchronize(e1);
             if (e != cudaSuccess) {
@@ -453,12 +468,13 @@ sdb_status launch_device(sdb_ctx* ctx, Slot& s, const sdb_desc& d, const double*
     if (rc != SDB_OK) return rc;
     const int P = next_pow2(d.nequat);
     cudaError_t e = launch_run(a, P / lay.lanes, kind_solver, kind_stream, d.coupling,
-                               d.nequat < P ? 1 : 0, st);
+                               kernel_variant(d, lay.tight), st);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "kuramoto_run_kernel launch");
     s.launches += 1;
     s.lanes = lay.lanes;
     s.persistent = lay.persistent;
     s.ctas_per_sm = lay.ctas_per_sm;
+    s.tight = lay.tight;
     return SDB_OK;
 }
 

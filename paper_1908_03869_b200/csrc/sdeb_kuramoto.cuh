@@ -450,9 +450,18 @@ __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
 // item's predecessor is always complete, so this cannot deadlock, and the
 // run ends within one slab of perfectly balanced: no partially-filled last
 // wave (the v3 profile lost ~13-23% to wave quantisation).
-// PADDED = (n < lanes * J): instantiated with and without padding handling.
-template <int J, int SOLVER, int STREAM, int COUPLING, bool PADDED>
-__global__ void __launch_bounds__(kBlock) kuramoto_run_kernel(const RunArgs a) {
+// VAR: 0 = unpadded (n == lanes * J, no per-oscillator predicates),
+// 1 = padded, 2 = unpadded with registers capped (tight_minb<J>() CTAs/SM):
+// more resident warps against fewer registers; the autotuner decides.
+template <int J>
+__host__ __device__ constexpr int tight_minb() {
+    return J == 4 ? 6 : (J == 8 ? 4 : 1);
+}
+
+template <int J, int SOLVER, int STREAM, int COUPLING, int VAR>
+__global__ void __launch_bounds__(kBlock, (VAR == 2 ? tight_minb<J>() : 0))
+    kuramoto_run_kernel(const RunArgs a) {
+    constexpr bool PADDED = VAR == 1;
     extern __shared__ double smem[];
     double* sh = smem;                  // pairwise: [J][kBlock]
     double* shs = smem + J * kBlock;    // pairwise L==1: [J][kBlock]

@@ -5,7 +5,7 @@
 
 namespace sdeb {
 
-template <int J, int S, int R, int C, bool P>
+template <int J, int S, int R, int C, int P>
 static cudaError_t launch_one(const RunArgs& a, cudaStream_t st) {
     const int64_t threads = a.orbits * int64_t(a.lanes);
     const unsigned grid = a.persistent > 0 ? unsigned(a.persistent)
@@ -22,7 +22,7 @@ static cudaError_t launch_one(const RunArgs& a, cudaStream_t st) {
     return cudaGetLastError();
 }
 
-template <int J, int S, int R, int C, bool P>
+template <int J, int S, int R, int C, int P>
 static cudaError_t occupancy_one(size_t smem, int* blocks) {
     const size_t need = pairwise_smem_bytes(J, C);
     if (smem < need) smem = need;
@@ -36,35 +36,39 @@ static cudaError_t occupancy_one(size_t smem, int* blocks) {
                                                          kBlock, smem);
 }
 
-// Visits the kernel instantiation for (solver, stream, coupling, padded) with
-// op.template run<J, S, R, C, P>().  The predicate-free (P = false) variants
-// exist for the meanfield paths; pairwise and the explicit-noise / drift
-// entry points always use the padded form.
+// Visits the kernel instantiation for (solver, stream, coupling, variant)
+// with op.template run<J, S, R, C, V>() (V: 0 unpadded, 1 padded, 2 unpadded
+// register-capped).  Pairwise and the explicit-noise / drift entry points
+// always use the padded form; capped variants exist where tight_minb<J>() > 1.
 template <int J, class Op>
-static cudaError_t dispatch(int solver, int stream, int coupling, int padded, Op&& op) {
-    const bool p = padded != 0;
-#define SDEB_PICK(S, R) \
-    return p ? op.template run<J, S, R, KC_MEANFIELD, true>() : op.template run<J, S, R, KC_MEANFIELD, false>()
+static cudaError_t dispatch(int solver, int stream, int coupling, int variant, Op&& op) {
+    if (variant == 2 && tight_minb<J>() == 1) variant = 0;
+#define SDEB_PICK(S, R)                                                          \
+    switch (variant) {                                                           \
+        case 0: return op.template run<J, S, R, KC_MEANFIELD, 0>();              \
+        case 1: return op.template run<J, S, R, KC_MEANFIELD, 1>();              \
+        default: return op.template run<J, S, R, KC_MEANFIELD, (tight_minb<J>() > 1 ? 2 : 0)>(); \
+    }
     if (coupling == KC_PAIRWISE) {
-        if (solver == KS_RK4) return op.template run<J, KS_RK4, KS_NONE, KC_PAIRWISE, true>();
-        if (solver == KS_DRIFT) return op.template run<J, KS_DRIFT, KS_NONE, KC_PAIRWISE, true>();
+        if (solver == KS_RK4) return op.template run<J, KS_RK4, KS_NONE, KC_PAIRWISE, 1>();
+        if (solver == KS_DRIFT) return op.template run<J, KS_DRIFT, KS_NONE, KC_PAIRWISE, 1>();
         switch (stream) {
-            case KS_PHILOX: return op.template run<J, KS_EM, KS_PHILOX, KC_PAIRWISE, true>();
-            case KS_SFC64: return op.template run<J, KS_EM, KS_SFC64, KC_PAIRWISE, true>();
-            case KS_XOSHIRO: return op.template run<J, KS_EM, KS_XOSHIRO, KC_PAIRWISE, true>();
-            case KS_NONE: return op.template run<J, KS_EM, KS_NONE, KC_PAIRWISE, true>();
-            case KS_EXPLICIT: return op.template run<J, KS_EM, KS_EXPLICIT, KC_PAIRWISE, true>();
+            case KS_PHILOX: return op.template run<J, KS_EM, KS_PHILOX, KC_PAIRWISE, 1>();
+            case KS_SFC64: return op.template run<J, KS_EM, KS_SFC64, KC_PAIRWISE, 1>();
+            case KS_XOSHIRO: return op.template run<J, KS_EM, KS_XOSHIRO, KC_PAIRWISE, 1>();
+            case KS_NONE: return op.template run<J, KS_EM, KS_NONE, KC_PAIRWISE, 1>();
+            case KS_EXPLICIT: return op.template run<J, KS_EM, KS_EXPLICIT, KC_PAIRWISE, 1>();
             default: return cudaErrorInvalidValue;
         }
     }
     if (solver == KS_RK4) SDEB_PICK(KS_RK4, KS_NONE);
-    if (solver == KS_DRIFT) return op.template run<J, KS_DRIFT, KS_NONE, KC_MEANFIELD, true>();
+    if (solver == KS_DRIFT) return op.template run<J, KS_DRIFT, KS_NONE, KC_MEANFIELD, 1>();
     switch (stream) {
         case KS_PHILOX: SDEB_PICK(KS_EM, KS_PHILOX);
         case KS_SFC64: SDEB_PICK(KS_EM, KS_SFC64);
         case KS_XOSHIRO: SDEB_PICK(KS_EM, KS_XOSHIRO);
         case KS_NONE: SDEB_PICK(KS_EM, KS_NONE);
-        case KS_EXPLICIT: return op.template run<J, KS_EM, KS_EXPLICIT, KC_MEANFIELD, true>();
+        case KS_EXPLICIT: return op.template run<J, KS_EM, KS_EXPLICIT, KC_MEANFIELD, 1>();
         default: return cudaErrorInvalidValue;
     }
 #undef SDEB_PICK
@@ -73,7 +77,7 @@ static cudaError_t dispatch(int solver, int stream, int coupling, int padded, Op
 struct LaunchOp {
     const RunArgs& a;
     cudaStream_t st;
-    template <int J, int S, int R, int C, bool P>
+    template <int J, int S, int R, int C, int P>
     cudaError_t run() const {
         return launch_one<J, S, R, C, P>(a, st);
     }
@@ -82,7 +86,7 @@ struct LaunchOp {
 struct OccupancyOp {
     size_t smem;
     int* blocks;
-    template <int J, int S, int R, int C, bool P>
+    template <int J, int S, int R, int C, int P>
     cudaError_t run() const {
         return occupancy_one<J, S, R, C, P>(smem, blocks);
     }

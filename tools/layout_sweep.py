@@ -42,7 +42,8 @@ def main():
     lanes_opts = [L for L in (1, 2, 4, 8, 16, 32) if L <= p and p // L <= 16]
     layouts = ([tuple(int(x) for x in s.split(",")) for s in args.layouts.split(";")]
                if args.layouts else
-               [(L, pers, 0) for L in lanes_opts for pers in (0, 1)])
+               [(L, pers, 0, tight) for L in lanes_opts for pers in (0, 1)
+                for tight in ((0, 1) if (p // L) in (4, 8) and p == n else (0,))])
     model = bench.make_model(sdb, w)
     batch = bench.make_batch(sdb, w, 0)
     cfg = sdb.EngineConfig(dt=w["dt"], tspan=w["dt"] * steps, ksteps=w["ksteps"], orbits=m,
@@ -57,7 +58,7 @@ def main():
     lib = nat.lib()
     ref = None
     for lay in layouts:
-        os.environ["SDEB200_LAYOUT"] = "%d,%d,%d" % lay
+        os.environ["SDEB200_LAYOUT"] = ",".join(str(v) for v in lay)
         ctx = ctypes.c_void_p()
         nat.check(lib.sdb_open(None, 0, ctypes.byref(ctx)))
         times = []

@@ -33,9 +33,11 @@ def main():
     ap.add_argument("--repeat", type=int, default=1)
     ap.add_argument("--persistent", type=int, default=0)
     ap.add_argument("--ctas", type=int, default=0)
+    ap.add_argument("--tight", type=int, default=0)
     args = ap.parse_args()
     if args.lanes:
-        os.environ["SDEB200_LAYOUT"] = "%d,%d,%d" % (args.lanes, args.persistent, args.ctas)
+        os.environ["SDEB200_LAYOUT"] = "%d,%d,%d,%d" % (args.lanes, args.persistent, args.ctas,
+                                                        args.tight)
     w = dict(bench.WORKLOADS[args.workload])
     if args.steps:
         w["steps"] = args.steps

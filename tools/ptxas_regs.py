@@ -23,6 +23,6 @@ for ln in out.splitlines():
 pat = sys.argv[1] if len(sys.argv) > 1 else "kuramoto_run"
 for name, regs, spill in rows:
     if pat in name:
-        t = re.search(r"ILi(\d+)ELi(\d+)ELi(\d+)ELi(\d+)ELb(\d)E", name)
-        tag = ("J=%s solver=%s stream=%s coupling=%s padded=%s" % t.groups()) if t else name
+        t = re.search(r"ILi(\d+)ELi(\d+)ELi(\d+)ELi(\d+)EL[ib](\d)E", name)
+        tag = ("J=%s solver=%s stream=%s coupling=%s variant=%s" % t.groups()) if t else name
         print("%-45s regs %3d spill %s" % (tag, regs, spill))
