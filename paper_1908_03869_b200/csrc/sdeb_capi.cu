@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -388,9 +389,13 @@ sdb_status choose_layout(sdb_ctx* ctx, Slot& s, const sdb_desc& d, const double*
         ctx->tune[key] = cands[0];
         return SDB_OK;
     }
-    // Probe ~5% of the run (128..512 steps): long enough that wave effects and
-    // the persistent grid's balance show as they will in the real run.
-    const int64_t probe = std::min<int64_t>(total, std::max<int64_t>(128, std::min<int64_t>(512, total / 20)));
+    // Differential probe: time P1 and P2 = 2*P1 steps and rank layouts by
+    // t(P2) - t(P1), the steady-state cost of P1 more steps.  Launch and
+    // end-of-run costs cancel; a one-CTA-per-group layout keeps its wave
+    // quantisation (every wave gets longer), a persistent grid does not
+    // (its drain tail cancels), so both are compared as they scale.
+    const int64_t p1 = std::min<int64_t>(total, std::max<int64_t>(64, std::min<int64_t>(256, total / 40)));
+    const int64_t p2 = std::min<int64_t>(total, 2 * p1);
     SDB_CUDA(ctx, s.t_values.ensure(size_t(d.orbits) * d.nequat * sizeof(double)));
     SDB_CUDA(ctx, s.t_state.ensure(size_t(d.orbits) * d.nequat * sizeof(double)));
     SDB_CUDA(ctx, s.t_fail.ensure(size_t(d.orbits) * sizeof(int64_t)));
@@ -401,7 +406,7 @@ sdb_status choose_layout(sdb_ctx* ctx, Slot& s, const sdb_desc& d, const double*
     float best = 1e30f;
     Layout best_l = cands[0];
     const int P = next_pow2(d.nequat);
-    for (const Layout& lay : cands) {
+    auto timed = [&](const Layout& lay, int64_t steps, float* ms_out) -> sdb_status {
         sdeb::RunArgs a = make_args(d, lay.lanes);
         a.state_in = d_init;
         a.params = d_params;
@@ -410,31 +415,39 @@ sdb_status choose_layout(sdb_ctx* ctx, Slot& s, const sdb_desc& d, const double*
         a.vstride = 1;
         a.fail_step = s.t_fail.as<int64_t>();
         a.rng_state = s.t_rng.as<uint64_t>();
-        a.ksteps = probe;
+        a.ksteps = steps;
         a.chunk_end = 1;
         float ms_best = 1e30f;
         for (int rep = 0; rep < 2; ++rep) {
-            rc = configure_layout(ctx, s, s.t_work, d, lay, probe, st, &a);
-            // probe slabs: >= 32 steps so per-item overhead is not overstated
-            if (a.persistent) a.slab_steps = std::max<int64_t>(32, probe / 8);
-            if (rc != SDB_OK) break;
+            sdb_status r2 = configure_layout(ctx, s, s.t_work, d, lay, steps, st, &a);
+            if (r2 != SDB_OK) return r2;
+            if (a.persistent) a.slab_steps = std::max<int64_t>(16, p1 / 2);
             cudaEventRecord(e0, st);
             cudaError_t e = launch_run(a, P / lay.lanes, kind_solver, kind_stream, d.coupling,
                                        kernel_variant(d, lay.tight), st);
             cudaEventRecord(e1, st);
             if (e == cudaSuccess) e = cudaEventSynchronize(e1);
-            if (e != cudaSuccess) {
-                rc = cuda_fail(ctx, e, "autotune launch");
-                break;
-            }
+            if (e != cudaSuccess) return cuda_fail(ctx, e, "autotune launch");
             float ms = 0.f;
             cudaEventElapsedTime(&ms, e0, e1);
             ms_best = std::min(ms_best, ms);
             s.launches += 1;
         }
+        *ms_out = ms_best;
+        return SDB_OK;
+    };
+    for (const Layout& lay : cands) {
+        float t1 = 0.f, t2 = 0.f;
+        rc = timed(lay, p1, &t1);
         if (rc != SDB_OK) break;
-        if (ms_best < best) {
-            best = ms_best;
+        float score = t1;
+        if (p2 > p1) {
+            rc = timed(lay, p2, &t2);
+            if (rc != SDB_OK) break;
+            score = t2 - t1;
+        }
+        if (score < best) {
+            best = score;
             best_l = lay;
         }
     }
@@ -479,9 +492,27 @@ sdb_status launch_device(sdb_ctx* ctx, Slot& s, const sdb_desc& d, const double*
 }
 
 // One device's contiguous shard [r0, r0+rows) of a host-buffer run.
+// SDEB200_TRACE=1: per-phase wall-clock of host-buffer runs on stderr (adds
+// stream synchronisations between phases; for diagnosis only).
+bool trace_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("SDEB200_TRACE");
+        return e && *e && *e != '0';
+    }();
+    return on;
+}
+
+double now_ms() {
+    return std::chrono::duration<double, std::milli>(
+               std::chrono::steady_clock::now().time_since_epoch())
+        .count();
+}
+
 sdb_status run_shard(sdb_ctx* ctx, Slot& s, sdb_desc d, int64_t r0, int64_t rows,
                      const double* init, const double* params, double* values, int64_t* fail) {
     SDB_CUDA(ctx, cudaSetDevice(s.device));
+    const bool tr = trace_enabled();
+    const double t0 = tr ? now_ms() : 0.0;
     const int n = d.nequat;
     d.orbit_offset += r0;
     d.orbits = rows;
@@ -494,9 +525,13 @@ sdb_status run_shard(sdb_ctx* ctx, Slot& s, sdb_desc d, int64_t r0, int64_t rows
     SDB_CUDA(ctx, cudaMemcpyAsync(s.params.ptr, params + r0 * d.nparams,
                                   size_t(rows) * d.nparams * sizeof(double),
                                   cudaMemcpyHostToDevice, s.stream));
+    if (tr) SDB_CUDA(ctx, cudaStreamSynchronize(s.stream));
+    const double t1 = tr ? now_ms() : 0.0;
     sdb_status rc = launch_device(ctx, s, d, s.init.as<double>(), s.params.as<double>(),
                                   s.values.as<double>(), s.fail.as<int64_t>(), s.stream);
     if (rc != SDB_OK) return rc;
+    if (tr) SDB_CUDA(ctx, cudaStreamSynchronize(s.stream));
+    const double t2 = tr ? now_ms() : 0.0;
     const size_t row_bytes = size_t(d.chunks) * n * sizeof(double);
     // samples 1..k of each row land after the verbatim sample 0 (engine.py:250-251)
     SDB_CUDA(ctx, cudaMemcpy2DAsync(values + (r0 * (d.chunks + 1) + 1) * n,
@@ -506,6 +541,15 @@ sdb_status run_shard(sdb_ctx* ctx, Slot& s, sdb_desc d, int64_t r0, int64_t rows
     SDB_CUDA(ctx, cudaMemcpyAsync(fail + r0, s.fail.ptr, size_t(rows) * sizeof(int64_t),
                                   cudaMemcpyDeviceToHost, s.stream));
     SDB_CUDA(ctx, cudaStreamSynchronize(s.stream));
+    if (tr) {
+        const double t3 = now_ms();
+        std::fprintf(stderr,
+                     "[sdeb200] dev %d rows %lld: H2D %.3f ms (%.1f MB), kernel %.3f ms, "
+                     "D2H %.3f ms (%.1f MB)\n",
+                     s.device, (long long)rows, t1 - t0,
+                     double(rows) * (n + d.nparams) * 8 / 1e6, t2 - t1, t3 - t2,
+                     double(rows) * (d.chunks * n + 1) * 8 / 1e6);
+    }
     return SDB_OK;
 }
 
@@ -608,8 +652,11 @@ sdb_status sdb_run(sdb_ctx* ctx, const sdb_desc* desc, const double* init, const
     const sdb_desc d = *desc;
     const int n = d.nequat;
     // sample 0 is the initial state verbatim (engine.py:251)
+    const double tc0 = trace_enabled() ? now_ms() : 0.0;
     for (int64_t r = 0; r < d.orbits; ++r)
         std::memcpy(values + r * (d.chunks + 1) * n, init + r * n, size_t(n) * sizeof(double));
+    if (trace_enabled())
+        std::fprintf(stderr, "[sdeb200] sample-0 copy %.3f ms\n", now_ms() - tc0);
     const int64_t nslots = int64_t(ctx->slots.size());
     const int64_t used = std::min<int64_t>(nslots, d.orbits);
     std::vector<sdb_status> status(used, SDB_OK);
