@@ -88,6 +88,15 @@ def algorithmic_fp64_ops(n: int, solver: str, coupling: str) -> float:
     return drift + n * 2
 
 
+def measured_traffic(workload: str):
+    """DRAM bytes per launch from the committed ncu capture (profiles/traffic.json)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            return json.load(f).get(workload, {}).get("dram_bytes")
+    except (OSError, ValueError):
+        return None
+
+
 def pairwise_equivalent_ops(n: int) -> float:
     """SURVEY.md 8d W_EM(n) = 9 n(n-1) + 41 n (the reference algorithm's work)."""
     return 9.0 * n * (n - 1) + 41.0 * n
@@ -336,9 +345,9 @@ def run_ours(args, w, world, rank, local, dist):
         launch()
     torch.cuda.synchronize()
     import ctypes
-    lay = [ctypes.c_int32() for _ in range(3)]
+    lay = [ctypes.c_int32() for _ in range(5)]
     lib.sdb_last_layout(ctx, *(ctypes.byref(v) for v in lay))
-    lanes, persistent, ctas_per_sm = (int(v.value) for v in lay)
+    lanes, persistent, ctas_per_sm, variant, _ = (int(v.value) for v in lay)
     launches_per_step = int(lib.sdb_last_launch_count(ctx))
 
     clocks = ClockSampler(local)
@@ -389,7 +398,7 @@ def run_ours(args, w, world, rank, local, dist):
         "bound": "fp64", "unit": "TFLOP/s",
         "achieved": 2 * achieved / 1e12, "peak": 2 * peak_ops / 1e12,
         "frac": achieved / peak_ops,
-        "traffic": None,
+        "traffic": measured_traffic(args.workload),
         "algorithmic_fp64_ops_per_orbit_step": ops,
         "peak_source": "measured live: sdb_fp64_peak DFMA-throughput kernel (FLOP = 2 x DFMA)",
         "pairwise_equivalent_frac": pairwise_equivalent_ops(n) * orbit_steps
@@ -410,7 +419,8 @@ def run_ours(args, w, world, rank, local, dist):
                        "orbits_per_gpu": m, "sde_steps": steps, "ksteps": w["ksteps"],
                        "solver": w["solver"], "stream": w["stream"], "coupling": args.coupling,
                        "lanes_per_orbit": lanes, "persistent_grid": bool(persistent),
-                       "ctas_per_sm": ctas_per_sm, "parallelism": "orbit-shard x%d" % world,
+                       "ctas_per_sm": ctas_per_sm, "register_capped": bool(variant),
+                       "parallelism": "orbit-shard x%d" % world,
                        "l2": "flushed (512 MiB memset) between timed steps, outside the "
                              "event pairs"},
             "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu,

@@ -25,7 +25,7 @@
 extern "C" {
 #endif
 
-#define SDB_ABI_VERSION 1
+#define SDB_ABI_VERSION 2
 
 typedef enum sdb_status {
     SDB_OK = 0,
@@ -97,10 +97,14 @@ int64_t sdb_last_launch_count(const sdb_ctx* ctx);
 /* Lanes-per-orbit layout chosen by the last run (after autotune). */
 int32_t sdb_last_lanes(const sdb_ctx* ctx);
 /* Full layout of the last run: lanes per orbit, persistent work-pulling grid
- * (0/1), resident CTAs per SM it ran at.  SDEB200_LAYOUT="lanes,persistent,ctas"
- * in the environment pins it (profiling). */
+ * (0/1), resident CTAs per SM it ran at, register-capped kernel variant (0/1),
+ * and the orbit tiles the host-buffer pipeline used (0 for sdb_run_device).
+ * SDEB200_LAYOUT="lanes,persistent,ctas,variant" in the environment pins the
+ * layout (profiling); SDEB200_TILES / SDEB200_PIECE_KB / SDEB200_HOST_THREADS
+ * override the host pipeline's tiling, transfer piece size and copy threads.
+ * Any pointer may be NULL. */
 void sdb_last_layout(const sdb_ctx* ctx, int32_t* lanes, int32_t* persistent,
-                     int32_t* ctas_per_sm);
+                     int32_t* ctas_per_sm, int32_t* variant, int32_t* tiles);
 
 /* ---- noise streams (rng.py) ------------------------------------------------ */
 

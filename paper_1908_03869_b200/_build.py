@@ -24,7 +24,12 @@ SOURCES = ["sdeb_capi.cu", "sdeb_misc.cu"] + ["sdeb_kuramoto_j%d.cu" % j for j i
 HEADERS = sorted(f for f in os.listdir(CSRC) if f.endswith((".cuh", ".h")))
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+# -fmad=false: every FP64 op on the stepper path is an explicit __d*_rn /
+# __fma_rn intrinsic already; the flag pins the rest (libdevice's huge-argument
+# trig reduction multiplies by 2/pi with a plain `*`), which ptxas would
+# otherwise fuse differently per kernel instantiation -- breaking the
+# bit-identity of lane layouts for |theta| >= 2^29.
+NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-Xcompiler", "-fPIC",
                      "-Xptxas", "-v", "-I", os.path.join(ROOT, "include")]
 
 

@@ -40,6 +40,8 @@ class SdbDesc(ctypes.Structure):
 
 
 # name -> (restype, argtypes); mirrors include/sdeb200.h one to one
+ABI_VERSION = 2  # include/sdeb200.h SDB_ABI_VERSION
+
 SIGNATURES = {
     "sdb_abi_version": (ctypes.c_int, []),
     "sdb_device_count": (ctypes.c_int, []),
@@ -54,8 +56,7 @@ SIGNATURES = {
                                       ctypes.c_void_p]),
     "sdb_last_launch_count": (ctypes.c_int64, [ctypes.c_void_p]),
     "sdb_last_lanes": (ctypes.c_int32, [ctypes.c_void_p]),
-    "sdb_last_layout": (None, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int32),
-                               ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32)]),
+    "sdb_last_layout": (None, [ctypes.c_void_p] + [ctypes.POINTER(ctypes.c_int32)] * 5),
     "sdb_philox_words": (ctypes.c_int, [ctypes.c_void_p, _c_u32_p, ctypes.c_int64, _c_u32_p]),
     "sdb_normals": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_uint64, _c_u32_p,
                                    ctypes.c_int64, ctypes.c_uint32, ctypes.c_uint32,
@@ -103,7 +104,7 @@ def lib():
                     fn = getattr(handle, name)
                     fn.restype = res
                     fn.argtypes = args
-                if handle.sdb_abi_version() != 1:
+                if handle.sdb_abi_version() != ABI_VERSION:
                     raise RuntimeError("libsdeb200.so ABI mismatch")
                 _lib = handle
     return _lib

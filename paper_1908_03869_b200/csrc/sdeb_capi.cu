@@ -51,9 +51,53 @@ struct DevBuf {
     }
 };
 
+// Pinned host staging slot (grow-only) + the event of the last DMA that used it.
+struct PinBuf {
+    void* ptr = nullptr;
+    size_t cap = 0;
+    cudaEvent_t ev = nullptr;
+    cudaError_t ensure(size_t bytes) {
+        if (!ev) {
+            cudaError_t e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+            if (e != cudaSuccess) return e;
+        }
+        if (bytes <= cap) return cudaSuccess;
+        if (ptr) {
+            cudaError_t e = cudaEventSynchronize(ev);
+            if (e != cudaSuccess) return e;
+            cudaFreeHost(ptr);
+        }
+        ptr = nullptr;
+        cap = 0;
+        const size_t want = std::max<size_t>(bytes, 1 << 20);
+        cudaError_t e = cudaHostAlloc(&ptr, want, cudaHostAllocPortable);
+        if (e == cudaSuccess) cap = want;
+        return e;
+    }
+    void release() {
+        if (ev) cudaEventSynchronize(ev);
+        if (ptr) cudaFreeHost(ptr);
+        if (ev) cudaEventDestroy(ev);
+        ptr = nullptr;
+        ev = nullptr;
+        cap = 0;
+    }
+    template <class T>
+    T* as() const {
+        return static_cast<T*>(ptr);
+    }
+};
+
+constexpr int kPinSlots = 2;
+
 struct Slot {
     int device = 0;
-    cudaStream_t stream = nullptr;
+    cudaStream_t stream = nullptr;  // kernels
+    cudaStream_t h2d = nullptr;     // host-buffer runs: input DMA
+    cudaStream_t d2h = nullptr;     // host-buffer runs: output DMA
+    cudaEvent_t ev_in = nullptr;
+    std::vector<cudaEvent_t> ev_tile;  // end of each tile's kernel
+    PinBuf pin_in[kPinSlots], pin_out[kPinSlots];
     DevBuf init, params, values, state, fail, rng;
     DevBuf t_values, t_state, t_fail, t_rng, t_work;  // autotune scratch
     DevBuf work;  // persistent mode: item counter + per-group slab counters
@@ -62,6 +106,7 @@ struct Slot {
     int32_t persistent = 0;
     int32_t ctas_per_sm = 0;
     int32_t tight = 0;
+    int32_t tiles = 0;  // orbit tiles of the last host-buffer run
     std::string error;
 };
 
@@ -87,6 +132,8 @@ struct sdb_ctx {
     int32_t last_lanes = 0;
     int32_t last_persistent = 0;
     int32_t last_ctas_per_sm = 0;
+    int32_t last_tight = 0;
+    int32_t last_tiles = 0;
     std::map<TuneKey, Layout> tune;
 };
 
@@ -508,49 +555,223 @@ double now_ms() {
         .count();
 }
 
+int env_int(const char* name, int dflt) {
+    const char* e = std::getenv(name);
+    return (e && *e) ? std::atoi(e) : dflt;
+}
+
+// Host copy of rows [0, rows) split over `threads` std::threads (the calling
+// thread takes the first range).  Pageable numpy destinations fault their
+// pages in on first touch; spreading the copy spreads the faults too.
+template <class F>
+void parallel_rows(int64_t rows, size_t bytes, int threads, F&& fn) {
+    const int64_t want = std::min<int64_t>(threads, int64_t(bytes >> 20));  // >= 1 MiB each
+    const int nt = int(std::max<int64_t>(1, std::min<int64_t>(want, rows)));
+    if (nt == 1) {
+        fn(int64_t(0), rows);
+        return;
+    }
+    std::vector<std::thread> pool;
+    pool.reserve(nt - 1);
+    for (int t = 1; t < nt; ++t)
+        pool.emplace_back([&, t] { fn(rows * t / nt, rows * (t + 1) / nt); });
+    fn(int64_t(0), rows / nt);
+    for (auto& th : pool) th.join();
+}
+
+int host_copy_threads(int shards) {
+    const int hw = int(std::max(1u, std::thread::hardware_concurrency()));
+    return std::max(1, env_int("SDEB200_HOST_THREADS", std::min(8, hw / std::max(1, shards))));
+}
+
+// Orbit tiles of a host-buffer shard: copies of tile t+1 / t-1 overlap the
+// kernel of tile t.  A tile must keep the kernel well fed (>= ~8 waves of
+// resident threads at a typical lanes-per-orbit) and be worth a pipeline
+// stage (>= 32 MB of transfers); at most 8.  SDEB200_TILES overrides.
+int64_t shard_tiles(const sdb_desc& d, int64_t rows, int device) {
+    const int forced = env_int("SDEB200_TILES", 0);
+    if (forced > 0) return std::min<int64_t>(forced, rows);
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    const int64_t lanes_est = std::min(32, std::max(1, next_pow2(d.nequat) / 4));
+    const int64_t min_rows = int64_t(8) * sms * 768 / lanes_est;
+    const double io = double(rows) * double(d.nequat + d.nparams + d.chunks * d.nequat) * 8.0;
+    int64_t t = std::min<int64_t>(rows / std::max<int64_t>(1, min_rows), int64_t(io / 32e6));
+    return std::max<int64_t>(1, std::min<int64_t>(8, t));
+}
+
+// One device's contiguous shard [r0, r0+rows) of a host-buffer run, as a
+// pipeline over orbit tiles and transfer pieces (<= SDEB200_PIECE_KB, 64 MiB):
+//   inputs  host rows -> pinned slot (parallel memcpy) -> DMA on s.h2d
+//   kernel  tile t on s.stream after its inputs landed
+//   outputs DMA on s.d2h after the tile's kernel -> pinned slot -> host rows,
+//           written as [init row | samples 1..k] (engine.py:250-251)
+// Pinned slots alternate (kPinSlots each way); a slot is refilled only after
+// the DMA that last used it completed.  Input staging of tile t+1 is issued
+// before the outputs of tile t are drained, so host copies, both DMA
+// directions and the kernels overlap.  Results are identical for any tiling:
+// noise is keyed by global orbit id and orbits are independent.
 sdb_status run_shard(sdb_ctx* ctx, Slot& s, sdb_desc d, int64_t r0, int64_t rows,
-                     const double* init, const double* params, double* values, int64_t* fail) {
+                     const double* init, const double* params, double* values, int64_t* fail,
+                     int shards) {
     SDB_CUDA(ctx, cudaSetDevice(s.device));
     const bool tr = trace_enabled();
     const double t0 = tr ? now_ms() : 0.0;
     const int n = d.nequat;
+    const int64_t np_ = d.nparams;
+    const int64_t k = d.chunks;
+    const int threads = host_copy_threads(shards);
     d.orbit_offset += r0;
     d.orbits = rows;
     SDB_CUDA(ctx, s.init.ensure(size_t(rows) * n * sizeof(double)));
-    SDB_CUDA(ctx, s.params.ensure(size_t(rows) * d.nparams * sizeof(double)));
-    SDB_CUDA(ctx, s.values.ensure(size_t(rows) * d.chunks * n * sizeof(double)));
+    SDB_CUDA(ctx, s.params.ensure(size_t(rows) * np_ * sizeof(double)));
+    SDB_CUDA(ctx, s.values.ensure(size_t(rows) * k * n * sizeof(double)));
     SDB_CUDA(ctx, s.fail.ensure(size_t(rows) * sizeof(int64_t)));
-    SDB_CUDA(ctx, cudaMemcpyAsync(s.init.ptr, init + r0 * n, size_t(rows) * n * sizeof(double),
-                                  cudaMemcpyHostToDevice, s.stream));
-    SDB_CUDA(ctx, cudaMemcpyAsync(s.params.ptr, params + r0 * d.nparams,
-                                  size_t(rows) * d.nparams * sizeof(double),
-                                  cudaMemcpyHostToDevice, s.stream));
-    if (tr) SDB_CUDA(ctx, cudaStreamSynchronize(s.stream));
-    const double t1 = tr ? now_ms() : 0.0;
-    sdb_status rc = launch_device(ctx, s, d, s.init.as<double>(), s.params.as<double>(),
-                                  s.values.as<double>(), s.fail.as<int64_t>(), s.stream);
-    if (rc != SDB_OK) return rc;
-    if (tr) SDB_CUDA(ctx, cudaStreamSynchronize(s.stream));
-    const double t2 = tr ? now_ms() : 0.0;
-    const size_t row_bytes = size_t(d.chunks) * n * sizeof(double);
-    // samples 1..k of each row land after the verbatim sample 0 (engine.py:250-251)
-    SDB_CUDA(ctx, cudaMemcpy2DAsync(values + (r0 * (d.chunks + 1) + 1) * n,
-                                    size_t(d.chunks + 1) * n * sizeof(double), s.values.ptr,
-                                    row_bytes, row_bytes, size_t(rows), cudaMemcpyDeviceToHost,
-                                    s.stream));
-    SDB_CUDA(ctx, cudaMemcpyAsync(fail + r0, s.fail.ptr, size_t(rows) * sizeof(int64_t),
-                                  cudaMemcpyDeviceToHost, s.stream));
-    SDB_CUDA(ctx, cudaStreamSynchronize(s.stream));
-    if (tr) {
-        const double t3 = now_ms();
-        std::fprintf(stderr,
-                     "[sdeb200] dev %d rows %lld: H2D %.3f ms (%.1f MB), kernel %.3f ms, "
-                     "D2H %.3f ms (%.1f MB)\n",
-                     s.device, (long long)rows, t1 - t0,
-                     double(rows) * (n + d.nparams) * 8 / 1e6, t2 - t1, t3 - t2,
-                     double(rows) * (d.chunks * n + 1) * 8 / 1e6);
+    if (!s.ev_in) SDB_CUDA(ctx, cudaEventCreateWithFlags(&s.ev_in, cudaEventDisableTiming));
+
+    const int64_t tiles = shard_tiles(d, rows, s.device);
+    const size_t piece_cap = size_t(std::max(1, env_int("SDEB200_PIECE_KB", 65536))) << 10;
+    const size_t in_row = size_t(n + np_) * sizeof(double);
+    const size_t out_row = size_t(k * n + 1) * sizeof(double);  // samples + fail word
+    const int64_t in_piece = std::max<int64_t>(1, int64_t(piece_cap / in_row));
+    const int64_t out_piece = std::max<int64_t>(1, int64_t(piece_cap / out_row));
+    double* d_init = s.init.as<double>();
+    double* d_params = s.params.as<double>();
+    double* d_values = s.values.as<double>();
+    int64_t* d_fail = s.fail.as<int64_t>();
+    int in_next = 0, out_next = 0;
+    double host_in_ms = 0.0, host_out_ms = 0.0, wait_ms = 0.0;
+
+    struct Pending {
+        int slot;
+        int64_t a, rows;  // shard-local rows
+    };
+    std::vector<Pending> pending;  // FIFO of issued output pieces
+    size_t head = 0;
+
+    auto drain_one = [&]() -> sdb_status {
+        const Pending p = pending[head++];
+        PinBuf& pb = s.pin_out[p.slot];
+        const double w0 = now_ms();
+        SDB_CUDA(ctx, cudaEventSynchronize(pb.ev));
+        const double w1 = now_ms();
+        const double* src = pb.as<double>();
+        const int64_t* fsrc = reinterpret_cast<const int64_t*>(src + p.rows * k * n);
+        parallel_rows(p.rows, size_t(p.rows) * out_row, threads, [&](int64_t a, int64_t b) {
+            for (int64_t r = a; r < b; ++r) {
+                const int64_t g = r0 + p.a + r;
+                double* dst = values + g * (k + 1) * n;
+                std::memcpy(dst, init + g * n, size_t(n) * sizeof(double));
+                std::memcpy(dst + n, src + r * k * n, size_t(k) * n * sizeof(double));
+            }
+        });
+        std::memcpy(fail + r0 + p.a, fsrc, size_t(p.rows) * sizeof(int64_t));
+        wait_ms += w1 - w0;
+        host_out_ms += now_ms() - w1;
+        return SDB_OK;
+    };
+
+    auto stage_inputs = [&](int64_t a, int64_t b) -> sdb_status {
+        for (int64_t p0 = a; p0 < b; p0 += in_piece) {
+            const int64_t pr = std::min(in_piece, b - p0);
+            PinBuf& pb = s.pin_in[in_next];
+            in_next = (in_next + 1) % kPinSlots;
+            SDB_CUDA(ctx, pb.ensure(size_t(pr) * in_row));
+            const double w0 = now_ms();
+            SDB_CUDA(ctx, cudaEventSynchronize(pb.ev));  // the slot's previous DMA is done
+            const double w1 = now_ms();
+            double* pin_init = pb.as<double>();
+            double* pin_par = pin_init + pr * n;
+            const double* h_init = init + (r0 + p0) * n;
+            const double* h_par = params + (r0 + p0) * np_;
+            parallel_rows(pr, size_t(pr) * in_row, threads, [&](int64_t x, int64_t y) {
+                std::memcpy(pin_init + x * n, h_init + x * n, size_t(y - x) * n * sizeof(double));
+                std::memcpy(pin_par + x * np_, h_par + x * np_, size_t(y - x) * np_ * sizeof(double));
+            });
+            wait_ms += w1 - w0;
+            host_in_ms += now_ms() - w1;
+            SDB_CUDA(ctx, cudaMemcpyAsync(d_init + p0 * n, pin_init, size_t(pr) * n * sizeof(double),
+                                          cudaMemcpyHostToDevice, s.h2d));
+            SDB_CUDA(ctx, cudaMemcpyAsync(d_params + p0 * np_, pin_par,
+                                          size_t(pr) * np_ * sizeof(double),
+                                          cudaMemcpyHostToDevice, s.h2d));
+            SDB_CUDA(ctx, cudaEventRecord(pb.ev, s.h2d));
+        }
+        return SDB_OK;
+    };
+
+    while (s.ev_tile.size() < size_t(tiles)) {
+        cudaEvent_t e;
+        SDB_CUDA(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        s.ev_tile.push_back(e);
     }
-    return SDB_OK;
+
+    auto launch_tile = [&](int64_t t, int64_t a, int64_t b) -> sdb_status {
+        SDB_CUDA(ctx, cudaEventRecord(s.ev_in, s.h2d));
+        SDB_CUDA(ctx, cudaStreamWaitEvent(s.stream, s.ev_in, 0));
+        sdb_desc td = d;
+        td.orbit_offset = d.orbit_offset + a;
+        td.orbits = b - a;
+        sdb_status rc = launch_device(ctx, s, td, d_init + a * n, d_params + a * np_,
+                                      d_values + a * k * n, d_fail + a, s.stream);
+        if (rc != SDB_OK) return rc;
+        SDB_CUDA(ctx, cudaEventRecord(s.ev_tile[t], s.stream));
+        return SDB_OK;
+    };
+
+    auto issue_outputs = [&](int64_t t, int64_t a, int64_t b) -> sdb_status {
+        SDB_CUDA(ctx, cudaStreamWaitEvent(s.d2h, s.ev_tile[t], 0));
+        for (int64_t p0 = a; p0 < b; p0 += out_piece) {
+            const int64_t pr = std::min(out_piece, b - p0);
+            // a slot is free once the piece that used it has been drained
+            while (pending.size() - head >= size_t(kPinSlots)) {
+                sdb_status rc = drain_one();
+                if (rc != SDB_OK) return rc;
+            }
+            const int slot = out_next;
+            out_next = (out_next + 1) % kPinSlots;
+            PinBuf& pb = s.pin_out[slot];
+            SDB_CUDA(ctx, pb.ensure(size_t(pr) * out_row));
+            double* dst = pb.as<double>();
+            SDB_CUDA(ctx, cudaMemcpyAsync(dst, d_values + p0 * k * n,
+                                          size_t(pr) * k * n * sizeof(double),
+                                          cudaMemcpyDeviceToHost, s.d2h));
+            SDB_CUDA(ctx, cudaMemcpyAsync(dst + pr * k * n, d_fail + p0,
+                                          size_t(pr) * sizeof(int64_t), cudaMemcpyDeviceToHost,
+                                          s.d2h));
+            SDB_CUDA(ctx, cudaEventRecord(pb.ev, s.d2h));
+            pending.push_back(Pending{slot, p0, pr});
+        }
+        return SDB_OK;
+    };
+
+    auto lo = [&](int64_t t) { return rows * t / tiles; };
+    sdb_status rc = stage_inputs(lo(0), lo(1));
+    if (rc == SDB_OK) rc = launch_tile(0, lo(0), lo(1));
+    for (int64_t t = 0; t < tiles && rc == SDB_OK; ++t) {
+        if (t + 1 < tiles) {  // queue tile t+1 before draining tile t
+            rc = stage_inputs(lo(t + 1), lo(t + 2));
+            if (rc == SDB_OK) rc = launch_tile(t + 1, lo(t + 1), lo(t + 2));
+        }
+        if (rc == SDB_OK) rc = issue_outputs(t, lo(t), lo(t + 1));
+    }
+    while (rc == SDB_OK && head < pending.size()) rc = drain_one();
+    if (rc != SDB_OK) {
+        cudaStreamSynchronize(s.h2d);  // leave no DMA in flight into pinned slots
+        cudaStreamSynchronize(s.stream);
+        cudaStreamSynchronize(s.d2h);
+        return rc;
+    }
+    s.tiles = int32_t(tiles);
+    if (tr) {
+        std::fprintf(stderr,
+                     "[sdeb200] dev %d rows %lld tiles %lld: total %.3f ms, host-in %.3f ms, "
+                     "host-out %.3f ms, waits %.3f ms (%.1f MB in, %.1f MB out)\n",
+                     s.device, (long long)rows, (long long)tiles, now_ms() - t0, host_in_ms,
+                     host_out_ms, wait_ms, double(rows) * in_row / 1e6,
+                     double(rows) * out_row / 1e6);
+    }
+    return rc;
 }
 
 // Scoped device buffer for the context-free utility entry points.
@@ -604,6 +825,8 @@ sdb_status sdb_open(const int* devices, int ndevices, sdb_ctx** out) {
         s.device = dev;
         cudaError_t e = cudaSetDevice(dev);
         if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&s.h2d, cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&s.d2h, cudaStreamNonBlocking);
         if (e != cudaSuccess) {
             delete ctx;
             return cuda_fail(nullptr, e, "sdb_open");
@@ -621,7 +844,11 @@ void sdb_close(sdb_ctx* ctx) {
         for (DevBuf* b : {&s.init, &s.params, &s.values, &s.state, &s.fail, &s.rng, &s.work,
                           &s.t_values, &s.t_state, &s.t_fail, &s.t_rng, &s.t_work})
             b->release();
-        if (s.stream) cudaStreamDestroy(s.stream);
+        for (PinBuf* b : {&s.pin_in[0], &s.pin_in[1], &s.pin_out[0], &s.pin_out[1]}) b->release();
+        if (s.ev_in) cudaEventDestroy(s.ev_in);
+        for (cudaEvent_t e : s.ev_tile) cudaEventDestroy(e);
+        for (cudaStream_t st : {s.stream, s.h2d, s.d2h})
+            if (st) cudaStreamDestroy(st);
     }
     delete ctx;
 }
@@ -635,7 +862,9 @@ int64_t sdb_last_launch_count(const sdb_ctx* ctx) { return ctx ? ctx->launches :
 int32_t sdb_last_lanes(const sdb_ctx* ctx) { return ctx ? ctx->last_lanes : 0; }
 
 void sdb_last_layout(const sdb_ctx* ctx, int32_t* lanes, int32_t* persistent,
-                     int32_t* ctas_per_sm) {
+                     int32_t* ctas_per_sm, int32_t* variant, int32_t* tiles) {
+    if (variant) *variant = ctx ? ctx->last_tight : 0;
+    if (tiles) *tiles = ctx ? ctx->last_tiles : 0;
     if (lanes) *lanes = ctx ? ctx->last_lanes : 0;
     if (persistent) *persistent = ctx ? ctx->last_persistent : 0;
     if (ctas_per_sm) *ctas_per_sm = ctx ? ctx->last_ctas_per_sm : 0;
@@ -651,12 +880,6 @@ sdb_status sdb_run(sdb_ctx* ctx, const sdb_desc* desc, const double* init, const
         return fail_with(ctx, SDB_ERR_ARGUMENT, "null host buffer");
     const sdb_desc d = *desc;
     const int n = d.nequat;
-    // sample 0 is the initial state verbatim (engine.py:251)
-    const double tc0 = trace_enabled() ? now_ms() : 0.0;
-    for (int64_t r = 0; r < d.orbits; ++r)
-        std::memcpy(values + r * (d.chunks + 1) * n, init + r * n, size_t(n) * sizeof(double));
-    if (trace_enabled())
-        std::fprintf(stderr, "[sdeb200] sample-0 copy %.3f ms\n", now_ms() - tc0);
     const int64_t nslots = int64_t(ctx->slots.size());
     const int64_t used = std::min<int64_t>(nslots, d.orbits);
     std::vector<sdb_status> status(used, SDB_OK);
@@ -668,7 +891,8 @@ sdb_status sdb_run(sdb_ctx* ctx, const sdb_desc* desc, const double* init, const
     // contiguous shards [g*M/G, (g+1)*M/G)
     auto shard = [&](int64_t g) {
         const int64_t r0 = g * d.orbits / used, r1 = (g + 1) * d.orbits / used;
-        status[g] = run_shard(ctx, ctx->slots[g], d, r0, r1 - r0, init, params, values, fail_step);
+        status[g] = run_shard(ctx, ctx->slots[g], d, r0, r1 - r0, init, params, values, fail_step,
+                              int(used));
     };
     if (used == 1) {
         shard(0);
@@ -681,6 +905,8 @@ sdb_status sdb_run(sdb_ctx* ctx, const sdb_desc* desc, const double* init, const
     ctx->last_lanes = ctx->slots[0].lanes;
     ctx->last_persistent = ctx->slots[0].persistent;
     ctx->last_ctas_per_sm = ctx->slots[0].ctas_per_sm;
+    ctx->last_tight = ctx->slots[0].tight;
+    ctx->last_tiles = ctx->slots[0].tiles;
     for (int64_t g = 0; g < used; ++g)
         if (status[g] != SDB_OK) return status[g];
     return SDB_OK;
@@ -704,6 +930,8 @@ sdb_status sdb_run_device(sdb_ctx* ctx, const sdb_desc* desc, const double* d_in
     ctx->last_lanes = s.lanes;
     ctx->last_persistent = s.persistent;
     ctx->last_ctas_per_sm = s.ctas_per_sm;
+    ctx->last_tight = s.tight;
+    ctx->last_tiles = 0;
     return rc;
 }
 

@@ -162,13 +162,17 @@ template <int J>
 __device__ __forceinline__ void sincos_vec(const double (&x)[J], double (&s)[J], double (&c)[J]) {
     bool big = false;
 #pragma unroll
-    for (int q = 0; q < J; ++q) big |= big_arg(x[q]);
-    if (!big) {
+    for (int q = 0; q < J; ++q) {
+        big |= big_arg(x[q]);
+        sincos_small(x[q], s[q], c[q]);
+    }
+    if (big) {
+        // rare: only the huge elements are redone with the exact reduction, so
+        // a value's bits never depend on its J-vector neighbours (lane
+        // layouts stay bit-identical)
 #pragma unroll
-        for (int q = 0; q < J; ++q) sincos_small(x[q], s[q], c[q]);
-    } else {
-#pragma unroll
-        for (int q = 0; q < J; ++q) sincos(x[q], &s[q], &c[q]);
+        for (int q = 0; q < J; ++q)
+            if (big_arg(x[q])) sincos(x[q], &s[q], &c[q]);
     }
 }
 

@@ -22,6 +22,7 @@ New, optional fields on EngineConfig (defaults keep reference behaviour):
 
 from __future__ import annotations
 
+import ctypes
 import dataclasses
 import math
 import os
@@ -291,5 +292,9 @@ def last_launch_info(devices=None) -> dict:
     """Kernel launches and lane layout of the most recent run on a context."""
     ctx = nat.context(devices)
     lib = nat.lib()
-    return {"launches": int(lib.sdb_last_launch_count(ctx)),
-            "lanes": int(lib.sdb_last_lanes(ctx))}
+    lay = [ctypes.c_int32() for _ in range(5)]
+    lib.sdb_last_layout(ctx, *(ctypes.byref(v) for v in lay))
+    lanes, persistent, ctas, variant, tiles = (int(v.value) for v in lay)
+    return {"launches": int(lib.sdb_last_launch_count(ctx)), "lanes": lanes,
+            "persistent_grid": bool(persistent), "ctas_per_sm": ctas,
+            "register_capped": bool(variant), "tiles": tiles}

@@ -366,3 +366,45 @@ def test_persistent_slab_schedule_bit_identical(n, stream):
     assert np.array_equal(ref_fail, got_fail) and ref_fail[7] >= 0
     capped, _ = _run_pinned("%d,0,2" % lanes, n, batch, cfg)
     assert np.array_equal(ref, capped, equal_nan=True)
+
+
+@pytest.mark.parametrize("stream", ["philox", "sfc64"])
+def test_host_pipeline_tiling_bit_identical(stream, monkeypatch):
+    # sdb_run's host pipeline (orbit tiles x pinned transfer pieces x host copy
+    # threads) must not change a single bit, failures and sample 0 included
+    from paper_1908_03869_b200.engine import last_launch_info
+    n, m = 16, 1501
+    batch = sdb.sample_kuramoto_batch(n, m, (0.2, 0.4), (0.01, 0.1), 0.3, seed=11)
+    params = batch.params.copy()
+    params[1000, 1 + 5] = 1e308  # a failing orbit inside a later tile
+    params[1200, 1 + 2] = 1e12   # |theta| >> 2^29: the exact-reduction trig path
+    batch = OrbitBatch(init=batch.init, params=params)
+    cfg = EngineConfig(dt=1e-2, tspan=2.0, ksteps=20, orbits=m, seed=2, stream=stream)
+    ref = run_batch(sdb.kuramoto_model(n), cfg, batch)
+    assert ref.failures and ref.failures[0].orbit == 1000
+    for tiles, piece_kb, threads in [(3, 100, 4), (7, 40, 1), (2, 65536, 8), (1, 1, 2)]:
+        monkeypatch.setenv("SDEB200_TILES", str(tiles))
+        monkeypatch.setenv("SDEB200_PIECE_KB", str(piece_kb))
+        monkeypatch.setenv("SDEB200_HOST_THREADS", str(threads))
+        got = run_batch(sdb.kuramoto_model(n), cfg, batch)
+        assert last_launch_info()["tiles"] == tiles
+        assert sdb.store_hash(got) == sdb.store_hash(ref)
+        assert got.failures == ref.failures
+        assert np.array_equal(got.values[:, 0], batch.init)
+
+
+@pytest.mark.parametrize("stream", ["philox", "sfc64"])
+def test_lane_layouts_bit_identical_huge_phases(stream):
+    # phases beyond 2^29 take the exact (Payne-Hanek) reduction branch; it must
+    # give the same bits in every kernel instantiation (lanes x J)
+    n, m = 16, 64
+    batch = sdb.sample_kuramoto_batch(n, m, (0.2, 0.4), (0.01, 0.1), 0.3, seed=3)
+    params = batch.params.copy()
+    params[::3, 1 + 4] = 1e12
+    params[1::5, 1:1 + n] = 1e308  # grows through 2^1000 to overflow (fails)
+    batch = OrbitBatch(init=batch.init, params=params)
+    base = EngineConfig(dt=1e-2, tspan=2.0, ksteps=10, orbits=m, seed=8, stream=stream)
+    stores = [run_batch(sdb.kuramoto_model(n), dataclasses.replace(base, lanes=L), batch)
+              for L in _lane_options(n)]
+    assert len({sdb.store_hash(s) for s in stores}) == 1
+    assert {f.orbit for f in stores[0].failures} == set(range(1, m, 5))

@@ -36,7 +36,7 @@ def test_library_exports_every_header_symbol():
 
 def test_library_loads_without_gpu():
     lib = nat.lib()
-    assert lib.sdb_abi_version() == 1
+    assert lib.sdb_abi_version() == 2
     assert lib.sdb_device_count() >= 0
 
 

@@ -77,7 +77,7 @@ def main():
         same = ref is None or np.array_equal(out, ref, equal_nan=True)
         if ref is None:
             ref = out
-        got = [ctypes.c_int32() for _ in range(3)]
+        got = [ctypes.c_int32() for _ in range(5)]
         lib.sdb_last_layout(ctx, *(ctypes.byref(v) for v in got))
         print(json.dumps({"layout": lay, "ran": [v.value for v in got], "ms": min(times),
                           "orbit_steps_per_s": m * steps / (min(times) * 1e-3),
