@@ -35,7 +35,8 @@ typedef enum sdb_status {
     SDB_ERR_ARGUMENT = 4     /* maps to ValueError */
 } sdb_status;
 
-enum { SDB_MODEL_KURAMOTO = 1 };                 /* model.py:188-220 */
+enum { SDB_MODEL_KURAMOTO = 1,                   /* model.py:188-220 */
+       SDB_MODEL_EXPRESSION = 2 };               /* model_from_dsl, model.py:291-309 */
 enum { SDB_SOLVER_EM = 0, SDB_SOLVER_EULER = 1, SDB_SOLVER_RK4 = 2 }; /* solvers.py:369-375 */
 enum { SDB_STREAM_PHILOX = 0, SDB_STREAM_SFC64 = 1, SDB_STREAM_XOSHIRO256PP = 2 };
 /* How the coupling sum S_i = sum_j sin(y_j - y_i) (model.py:193-195) is evaluated:
@@ -44,12 +45,13 @@ enum { SDB_STREAM_PHILOX = 0, SDB_STREAM_SFC64 = 1, SDB_STREAM_XOSHIRO256PP = 2 
 enum { SDB_COUPLING_MEANFIELD = 0, SDB_COUPLING_PAIRWISE = 1 };
 
 typedef struct sdb_ctx sdb_ctx;
+typedef struct sdb_model sdb_model;
 
 /* One integration run: the fields of EngineConfig (engine.py:81-101) that the
  * device needs, after the host has validated them (engine.py:103-117,
  * 229-245) and computed chunks = iteration_count(...) (engine.py:163-179). */
 typedef struct sdb_desc {
-    int32_t model;        /* SDB_MODEL_KURAMOTO */
+    int32_t model;        /* SDB_MODEL_KURAMOTO, or SDB_MODEL_EXPRESSION for sdb_run_model */
     int32_t nequat;       /* n oscillators */
     int32_t nparams;      /* row length of params: (K, omega_1..n[, s_1..n, ...]) */
     int32_t nnoise;       /* n (stochastic) or 0 (ODE) */
@@ -162,6 +164,55 @@ sdb_status sdb_fp64_peak(sdb_ctx* ctx, double* ops_per_s, double* ms);
  * tests): func 0 = sin, 1 = cos (the stepper's sincos), 2 = log (Box-Muller
  * radius), 3 = sqrt, 4 = sin / 5 = cos / 6 = log of libdevice for comparison. */
 sdb_status sdb_math_probe(sdb_ctx* ctx, int32_t func, const double* x, int64_t count,
+                          double* out);
+
+/* ---- expression-template models (dsl.py / model.py:291-323) -----------------
+ *
+ * The reference evaluates a model's drift and diffusion templates with a numpy
+ * interpreter (dsl.py:441-571, via drift_eval/diffusion_eval, model.py:142-182).
+ * Here the template text is compiled: parsed, turned into CUDA device functions
+ * and built by NVRTC for sm_100a into a one-thread-per-orbit stepper with the
+ * same fused noise streams (the paper's runtime kernel generation,
+ * PAPER.md:88-113).  Grammar: dsl.py:12-19 (numbers; t, N, i; y[.], p[.], n[.];
+ * + - * / ^; sin cos tan exp ln sqrt abs; sum(j, body)).  The caller validates
+ * the templates against the dimensions first (dsl.validate, dsl.py:353-408) and
+ * checks that every index stays in range (the reference raises DomainError at
+ * evaluation time, dsl.py:516-531); the device does not bounds-check. */
+
+/* Parse both templates and generate their device code (no GPU needed).
+ * Errors: SDB_ERR_ARGUMENT with "drift|diffusion: line L, column C: ..." in
+ * sdb_last_error(NULL).  Programs are compiled lazily on first use. */
+sdb_status sdb_model_create(int32_t nequat, int32_t nparams, int32_t nnoise, const char* drift,
+                            const char* diffusion, sdb_model** out);
+void sdb_model_free(sdb_model* model);
+/* Generated CUDA source of program `kind` (0..9, see sdeb_dsl_args.h DslKind):
+ * copies at most cap-1 bytes + NUL into buf (may be NULL) and returns the full
+ * length, or -1. */
+int64_t sdb_model_source(const sdb_model* model, int32_t kind, char* buf, int64_t cap);
+/* NVRTC-compile program `kind` without loading it (no GPU needed); the compile
+ * log / error is in sdb_last_error(NULL) on failure. */
+sdb_status sdb_model_build(sdb_model* model, int32_t kind);
+
+/* run_batch (engine.py:184-277) for an expression-template model: desc->model
+ * = SDB_MODEL_EXPRESSION, dimensions equal to the model's; buffers as sdb_run. */
+sdb_status sdb_run_model(sdb_ctx* ctx, sdb_model* model, const sdb_desc* desc,
+                         const double* init, const double* params, double* values,
+                         int64_t* fail_step);
+/* The same on device buffers (first device, asynchronous on `stream`), as
+ * sdb_run_device. */
+sdb_status sdb_run_model_device(sdb_ctx* ctx, sdb_model* model, const sdb_desc* desc,
+                                const double* d_init, const double* d_params, double* d_values,
+                                int64_t* d_fail_step, void* stream);
+/* drift_eval (which=0) / diffusion_eval (which=1) at time t over `count` rows
+ * (model.py:142-182; strict=False semantics: domain errors give inf/NaN).
+ * y [count][nequat], p [count][nparams], noise [count][nnoise] (diffusion),
+ * out [count][nequat]. */
+sdb_status sdb_model_eval(sdb_ctx* ctx, sdb_model* model, int32_t which, double t, int64_t count,
+                          const double* y, const double* p, const double* noise, double* out);
+/* One em / euler / rk4 step at time t (solvers.py:63-88) with caller-given
+ * noise for em on a noisy model. */
+sdb_status sdb_model_step(sdb_ctx* ctx, sdb_model* model, int32_t solver, double t, double dt,
+                          int64_t count, const double* y, const double* p, const double* noise,
                           double* out);
 
 #ifdef __cplusplus

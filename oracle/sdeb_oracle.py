@@ -317,15 +317,21 @@ def iteration_count(tspan, dt, ksteps, pad=False):
 # The restated run loop (engine.py:221-314)
 
 def integrate(init, params, *, dt, ksteps, chunks, seed=0, solver="em", nnoise=None,
-              stream="philox", orbit_ids=None, threads=1, group=None):
+              stream="philox", orbit_ids=None, threads=1, group=None, drift=None,
+              diffusion=None):
     """Restated ``run_batch`` inner loop for global ``orbit_ids``.
 
     engine.py:260-300 (integrate_group) with the stepper of engine.py:190-218.
     Returns (times, values, failures) where failures are
     (orbit, chunk, step, time, reason) tuples sorted by orbit (engine.py:312).
     ``threads``/``group`` mirror the reference's pool over contiguous orbit
-    groups (engine.py:302-311); they never change the result.
+    groups (engine.py:302-311); they never change the result.  ``drift(t, y,
+    p)`` / ``diffusion(t, y, p, noise)`` default to the Kuramoto system; pass
+    :func:`expression_model` functions for a template model.
     """
+    f_drift = drift if drift is not None else (lambda t, y, p: kuramoto_drift(y, p))
+    f_diff = diffusion if diffusion is not None else (
+        lambda t, y, p, noise: kuramoto_diffusion(y, p, noise))
     init = np.asarray(init, dtype=np.float64)
     params = np.asarray(params, dtype=np.float64)
     m_orbits, n = init.shape
@@ -362,11 +368,16 @@ def integrate(init, params, *, dt, ksteps, chunks, seed=0, solver="em", nnoise=N
                                                        (s >> 32) & MASK32, s & MASK32, nnoise)
                         else:
                             noise = gaussian_from_words(*stream_block_words(stream, st), nnoise)
-                        y = (y + kuramoto_drift(y, p) * dt) + sqrt_dt * kuramoto_diffusion(y, p, noise)
+                        y = (y + f_drift(t, y, p) * dt) + sqrt_dt * f_diff(t, y, p, noise)
                     elif solver in ("em", "euler"):
-                        y = euler_step(y, p, dt)
+                        y = y + f_drift(t, y, p) * dt
                     elif solver == "rk4":
-                        y = rk4_step(y, p, dt)
+                        half = 0.5 * dt
+                        k1 = f_drift(t, y, p)
+                        k2 = f_drift(t + half, y + half * k1, p)
+                        k3 = f_drift(t + half, y + half * k2, p)
+                        k4 = f_drift(t + dt, y + dt * k3, p)
+                        y = y + (dt / 6.0) * (k1 + 2.0 * k2 + 2.0 * k3 + k4)
                     else:
                         raise ValueError("unsupported solver %r" % (solver,))
                     ok = np.isfinite(y).all(axis=-1)
@@ -392,6 +403,107 @@ def integrate(init, params, *, dt, ksteps, chunks, seed=0, solver="em", nnoise=N
                 failures.extend(res)
     failures.sort(key=lambda f: f[0])
     return times, values, failures
+
+
+# ---------------------------------------------------------------------------
+# Expression templates (dsl.py:1-27 grammar; interpreter dsl.py:441-571)
+#
+# Parsing goes through Python's own expression parser: with '^' spelled '**'
+# the template grammar is a subset of Python's with the same precedences
+# (unary minus looser than '**', '**' right-associative and taking a signed
+# right operand).  Evaluation restates the reference interpreter: numpy
+# float64 ufuncs, equation index i and sum indices as int64 arrays on their
+# own broadcast axes, indexing through np.take, sums as np.sum over the last
+# axis (numpy pairwise order).
+
+_EXPR_FUNCS = {"sin": np.sin, "cos": np.cos, "tan": np.tan, "exp": np.exp, "ln": np.log,
+               "sqrt": np.sqrt, "abs": np.abs}
+_EXPR_BIN = {"Add": np.add, "Sub": np.subtract, "Mult": np.multiply, "Div": np.divide,
+             "Pow": np.power}
+
+
+def _expr_tree(text):
+    import ast
+    return ast.parse(text.replace("^", "**"), mode="eval").body
+
+
+def _expr_index(node, axes):
+    """dsl.py:472-496: integer index arithmetic."""
+    import ast
+    if isinstance(node, ast.Constant):
+        return int(node.value)
+    if isinstance(node, ast.Name):
+        if node.id == "N":
+            return axes["N"]
+        return axes[node.id]
+    if isinstance(node, ast.UnaryOp):
+        return -_expr_index(node.operand, axes)
+    a, b = _expr_index(node.left, axes), _expr_index(node.right, axes)
+    op = type(node.op).__name__
+    return a + b if op == "Add" else a - b if op == "Sub" else a * b
+
+
+def _expr_eval(node, env, axes, depth):
+    """dsl.py:441-551 (_Evaluator.eval) for one expression node."""
+    import ast
+    if isinstance(node, ast.Constant):
+        return float(node.value)
+    if isinstance(node, ast.Name):
+        if node.id == "t":
+            return env["t"]
+        if node.id == "N":
+            return float(env["N"])
+        return axes[node.id]
+    if isinstance(node, ast.UnaryOp):
+        return np.negative(_expr_eval(node.operand, env, axes, depth))
+    if isinstance(node, ast.BinOp):
+        left = _expr_eval(node.left, env, axes, depth)
+        right = _expr_eval(node.right, env, axes, depth)
+        return _EXPR_BIN[type(node.op).__name__](left, right)
+    if isinstance(node, ast.Subscript):
+        arr = env[node.value.id]
+        idx = _expr_index(node.slice, axes)
+        taken = np.take(arr, idx, axis=-1)
+        if not isinstance(idx, np.ndarray) and depth:
+            taken = np.reshape(taken, np.shape(taken) + (1,) * depth)
+        return taken
+    if isinstance(node, ast.Call):
+        name = node.func.id
+        if name == "sum":  # dsl.py:533-551
+            var = node.args[0].id
+            n = env["N"]
+            inner = {k: (v.reshape(v.shape + (1,)) if isinstance(v, np.ndarray) else v)
+                     for k, v in axes.items()}
+            inner[var] = np.arange(n, dtype=np.int64).reshape((1,) * depth + (n,))
+            body = np.asarray(_expr_eval(node.args[1], env, inner, depth + 1))
+            full = np.broadcast_shapes(body.shape, (1,) * depth + (n,))
+            if body.shape != full:
+                body = np.broadcast_to(body, full)
+            return np.sum(body, axis=-1)
+        return _EXPR_FUNCS[name](_expr_eval(node.args[0], env, axes, depth))
+    raise ValueError("unsupported expression node %r" % (node,))
+
+
+def evaluate_expression(text, t, y, p, noise=None):
+    """All equations of a template at once (dsl.evaluate with i=None)."""
+    y = np.asarray(y, dtype=np.float64)
+    n = y.shape[-1]
+    env = {"t": float(t), "N": n, "y": y, "p": np.asarray(p, dtype=np.float64), "n": noise}
+    axes = {"i": np.arange(n, dtype=np.int64), "N": n}
+    with np.errstate(all="ignore"):
+        out = _expr_eval(_expr_tree(text), env, axes, 1)
+    return np.broadcast_to(np.asarray(out, dtype=np.float64), y.shape)
+
+
+def expression_model(drift_text, diffusion_text=None):
+    """(drift, diffusion) callables for :func:`integrate` from template text
+    (model.py:142-182: results broadcast to the state's shape)."""
+    def drift(t, y, p):
+        return evaluate_expression(drift_text, t, y, p)
+
+    def diffusion(t, y, p, noise):
+        return evaluate_expression(diffusion_text, t, y, p, noise)
+    return drift, diffusion
 
 
 def mixed_error(got, ref):

@@ -17,7 +17,7 @@ from .engine import (EngineConfig, TrajectoryStore, OrbitFailure, ConfigError, r
 from .solvers import (euler_maruyama_step, euler_step, rk4_step, implicit_euler_step,
                       implicit_midpoint_step, get_solver, SOLVERS)
 from .storage import store_hash
-from . import rng
+from . import dsl, rng
 
 __all__ = [
     "__version__",
@@ -28,5 +28,5 @@ __all__ = [
     "iteration_count", "partition_orbits",
     "euler_maruyama_step", "euler_step", "rk4_step",
     "implicit_euler_step", "implicit_midpoint_step", "get_solver", "SOLVERS",
-    "store_hash", "rng",
+    "store_hash", "dsl", "rng",
 ]

@@ -20,8 +20,15 @@ CSRC = os.path.join(PKG, "csrc")
 OBJ = os.path.join(PKG, "_obj")
 LIB = os.path.join(PKG, "libsdeb200.so")
 
-SOURCES = ["sdeb_capi.cu", "sdeb_misc.cu"] + ["sdeb_kuramoto_j%d.cu" % j for j in (1, 2, 4, 8, 16)]
+SOURCES = (["sdeb_capi.cu", "sdeb_misc.cu", "sdeb_dsl.cu"]
+           + ["sdeb_kuramoto_j%d.cu" % j for j in (1, 2, 4, 8, 16)])
 HEADERS = sorted(f for f in os.listdir(CSRC) if f.endswith((".cuh", ".h")))
+# device headers the NVRTC-compiled expression-template programs include; they
+# are embedded into the library (no source tree needed at run time)
+RTC_HEADERS = ["sdeb_dsl_kernel.cuh", "sdeb_dsl_args.h", "sdeb_rng.cuh", "sdeb_math.cuh",
+               "sdeb_cstdint.cuh", "sdeb_log_table.cuh", "sdeb_sincos_table.cuh"]
+RTC_INC = os.path.join(OBJ, "sdeb_rtc_headers.inc")
+CUDA_LIB = "/usr/local/cuda/lib64"
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 # -fmad=false: every FP64 op on the stepper path is an explicit __d*_rn /
@@ -30,7 +37,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 # otherwise fuse differently per kernel instantiation -- breaking the
 # bit-identity of lane layouts for |theta| >= 2^29.
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-Xcompiler", "-fPIC",
-                     "-Xptxas", "-v", "-I", os.path.join(ROOT, "include")]
+                     "-Xptxas", "-v", "-I", os.path.join(ROOT, "include"), "-I", OBJ]
 
 
 def nvcc() -> str:
@@ -44,9 +51,33 @@ def _mtime(path: str) -> float:
     return os.path.getmtime(path) if os.path.exists(path) else -1.0
 
 
+def _write_rtc_headers() -> None:
+    """sdeb_rtc_headers.inc: {name, raw text} of every header a generated
+    program includes (rewritten only when a header changed)."""
+    if os.path.exists(RTC_INC) and _mtime(RTC_INC) >= max(
+            _mtime(os.path.join(CSRC, h)) for h in RTC_HEADERS):
+        return
+    parts = ["const RtcHeader kRtcHeaders[] = {"]
+    for h in RTC_HEADERS:
+        with open(os.path.join(CSRC, h)) as f:
+            text = f.read()
+        assert ")SDEBRTC\"" not in text
+        # split into <= 60 KB raw-string pieces (adjacent literals concatenate)
+        chunks = [text[i:i + 60000] for i in range(0, len(text), 60000)] or [""]
+        body = "\n".join('R"SDEBRTC(%s)SDEBRTC"' % c for c in chunks)
+        parts.append('    {"%s",\n%s},' % (h, body))
+    parts.append("};")
+    tmp = RTC_INC + ".tmp"
+    with open(tmp, "w") as f:
+        f.write("\n".join(parts) + "\n")
+    os.replace(tmp, RTC_INC)
+
+
 def _compile(src: str, log: list) -> str:
     obj = os.path.join(OBJ, os.path.basename(src).replace(".cu", ".o"))
     deps = [os.path.join(CSRC, src)] + [os.path.join(CSRC, h) for h in HEADERS]
+    if src == "sdeb_dsl.cu":
+        deps.append(RTC_INC)
     deps.append(os.path.join(ROOT, "include", "sdeb200.h"))
     if _mtime(obj) >= max(_mtime(d) for d in deps):
         return obj
@@ -63,11 +94,13 @@ def build(verbose: bool = False, force: bool = False) -> str:
     if force:
         for f in os.listdir(OBJ):
             os.remove(os.path.join(OBJ, f))
+    _write_rtc_headers()
     log: list = []
     with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as pool:
         objs = list(pool.map(lambda s: _compile(s, log), SOURCES))
     if force or _mtime(LIB) < max(_mtime(o) for o in objs):
-        cmd = [nvcc()] + ARCH + ["-shared", "-cudart", "static", "-o", LIB] + objs
+        cmd = ([nvcc()] + ARCH + ["-shared", "-cudart", "static", "-o", LIB] + objs
+               + ["-L", CUDA_LIB, "-lnvrtc", "-Xlinker", "-rpath=" + CUDA_LIB])
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
             raise RuntimeError("link failed:\n" + res.stdout + res.stderr)

@@ -19,6 +19,7 @@ LIB_PATH = os.environ.get("SDEB200_LIB", os.path.join(_HERE, "libsdeb200.so"))
 
 SDB_OK, SDB_ERR_CONFIG, SDB_ERR_UNSUPPORTED, SDB_ERR_CUDA, SDB_ERR_ARGUMENT = range(5)
 SDB_MODEL_KURAMOTO = 1
+SDB_MODEL_EXPRESSION = 2
 SOLVER_IDS = {"em": 0, "euler": 1, "rk4": 2}
 STREAM_IDS = {"philox": 0, "sfc64": 1, "xoshiro256pp": 2}
 COUPLING_IDS = {"meanfield": 0, "pairwise": 1}
@@ -58,6 +59,23 @@ SIGNATURES = {
     "sdb_last_lanes": (ctypes.c_int32, [ctypes.c_void_p]),
     "sdb_last_layout": (None, [ctypes.c_void_p] + [ctypes.POINTER(ctypes.c_int32)] * 5),
     "sdb_philox_words": (ctypes.c_int, [ctypes.c_void_p, _c_u32_p, ctypes.c_int64, _c_u32_p]),
+    "sdb_model_create": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                        ctypes.c_char_p, ctypes.c_char_p,
+                                        ctypes.POINTER(ctypes.c_void_p)]),
+    "sdb_model_free": (None, [ctypes.c_void_p]),
+    "sdb_model_source": (ctypes.c_int64, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_char_p,
+                                          ctypes.c_int64]),
+    "sdb_model_build": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32]),
+    "sdb_run_model": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(SdbDesc),
+                                     _c_double_p, _c_double_p, _c_double_p, _c_i64_p]),
+    "sdb_run_model_device": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p,
+                                            ctypes.POINTER(SdbDesc)] + [ctypes.c_void_p] * 5),
+    "sdb_model_eval": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32,
+                                      ctypes.c_double, ctypes.c_int64, _c_double_p, _c_double_p,
+                                      _c_double_p, _c_double_p]),
+    "sdb_model_step": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32,
+                                      ctypes.c_double, ctypes.c_double, ctypes.c_int64,
+                                      _c_double_p, _c_double_p, _c_double_p, _c_double_p]),
     "sdb_normals": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_uint64, _c_u32_p,
                                    ctypes.c_int64, ctypes.c_uint32, ctypes.c_uint32,
                                    ctypes.c_int32, _c_double_p]),

@@ -20,6 +20,7 @@
 #include <vector>
 
 #include "../../include/sdeb200.h"
+#include "sdeb_dsl.h"
 #include "sdeb_kuramoto.cuh"
 #include "sdeb_misc.h"
 
@@ -101,6 +102,7 @@ struct Slot {
     DevBuf init, params, values, state, fail, rng;
     DevBuf t_values, t_state, t_fail, t_rng, t_work;  // autotune scratch
     DevBuf work;  // persistent mode: item counter + per-group slab counters
+    DevBuf scratch;  // expression-template programs with global state columns
     int64_t launches = 0;
     int32_t lanes = 0;
     int32_t persistent = 0;
@@ -506,9 +508,58 @@ sdb_status choose_layout(sdb_ctx* ctx, Slot& s, const sdb_desc& d, const double*
     return SDB_OK;
 }
 
-sdb_status launch_device(sdb_ctx* ctx, Slot& s, const sdb_desc& d, const double* d_init,
-                         const double* d_params, double* d_values, int64_t* d_fail,
-                         cudaStream_t st) {
+// One launch of an expression-template program over d.orbits rows (one
+// thread per orbit; no layout autotune).
+sdb_status launch_model(sdb_ctx* ctx, Slot& s, const sdb_desc& d, sdb_model* m,
+                        const double* d_init, const double* d_params, double* d_values,
+                        int64_t* d_fail, cudaStream_t st) {
+    const int nb = std::max(1, (m->nnoise + 3) / 4);
+    SDB_CUDA(ctx, s.state.ensure(size_t(d.orbits) * d.nequat * sizeof(double)));
+    int kind = sdeb::DK_RUN_EULER;
+    if (d.solver == SDB_SOLVER_RK4) {
+        kind = sdeb::DK_RUN_RK4;
+    } else if (d.solver == SDB_SOLVER_EM && m->nnoise > 0) {
+        kind = d.stream == SDB_STREAM_SFC64 ? sdeb::DK_RUN_SFC64
+             : d.stream == SDB_STREAM_XOSHIRO256PP ? sdeb::DK_RUN_XOSHIRO : sdeb::DK_RUN_PHILOX;
+        if (kind != sdeb::DK_RUN_PHILOX)
+            SDB_CUDA(ctx, s.rng.ensure(size_t(d.orbits) * nb * 4 * sizeof(uint64_t)));
+    }
+    sdeb::DslArgs a{};
+    a.state_in = d_init;
+    a.params = d_params;
+    a.state_out = s.state.as<double>();
+    a.values = d_values;
+    a.fail_step = d_fail;
+    a.rng_state = s.rng.as<uint64_t>();
+    a.rows = d.orbits;
+    a.orbit_offset = d.orbit_offset;
+    a.vstride = d.chunks;
+    a.ksteps = d.ksteps;
+    a.chunk_begin = 0;
+    a.chunk_end = d.chunks;
+    a.seed = d.seed;
+    a.dt = d.dt;
+    a.sqrt_dt = std::sqrt(d.dt);
+    a.fresh = 1;
+    if (sdeb_dsl::global_state(m)) {
+        SDB_CUDA(ctx, s.scratch.ensure(size_t(d.orbits) * sdeb_dsl::state_words(m) * sizeof(double)));
+        a.scratch = s.scratch.as<double>();
+    }
+    std::string err;
+    cudaError_t e = sdeb_dsl::launch(m, kind, a, st, &err);
+    if (e != cudaSuccess) return fail_with(ctx, SDB_ERR_CUDA, "%s", err.c_str());
+    s.launches += 1;
+    s.lanes = 1;
+    s.persistent = 0;
+    s.ctas_per_sm = 0;
+    s.tight = 0;
+    return SDB_OK;
+}
+
+sdb_status launch_device(sdb_ctx* ctx, Slot& s, const sdb_desc& d, sdb_model* m,
+                         const double* d_init, const double* d_params, double* d_values,
+                         int64_t* d_fail, cudaStream_t st) {
+    if (m) return launch_model(ctx, s, d, m, d_init, d_params, d_values, d_fail, st);
     Layout lay;
     sdb_status rc = choose_layout(ctx, s, d, d_init, d_params, st, &lay);
     if (rc != SDB_OK) return rc;
@@ -611,7 +662,7 @@ int64_t shard_tiles(const sdb_desc& d, int64_t rows, int device) {
 // before the outputs of tile t are drained, so host copies, both DMA
 // directions and the kernels overlap.  Results are identical for any tiling:
 // noise is keyed by global orbit id and orbits are independent.
-sdb_status run_shard(sdb_ctx* ctx, Slot& s, sdb_desc d, int64_t r0, int64_t rows,
+sdb_status run_shard(sdb_ctx* ctx, Slot& s, sdb_desc d, sdb_model* m, int64_t r0, int64_t rows,
                      const double* init, const double* params, double* values, int64_t* fail,
                      int shards) {
     SDB_CUDA(ctx, cudaSetDevice(s.device));
@@ -712,7 +763,7 @@ sdb_status run_shard(sdb_ctx* ctx, Slot& s, sdb_desc d, int64_t r0, int64_t rows
         sdb_desc td = d;
         td.orbit_offset = d.orbit_offset + a;
         td.orbits = b - a;
-        sdb_status rc = launch_device(ctx, s, td, d_init + a * n, d_params + a * np_,
+        sdb_status rc = launch_device(ctx, s, td, m, d_init + a * n, d_params + a * np_,
                                       d_values + a * k * n, d_fail + a, s.stream);
         if (rc != SDB_OK) return rc;
         SDB_CUDA(ctx, cudaEventRecord(s.ev_tile[t], s.stream));
@@ -788,6 +839,132 @@ sdb_status utility_prologue(sdb_ctx* ctx) {
     return SDB_OK;
 }
 
+
+sdb_status validate_model(sdb_ctx* ctx, const sdb_desc* d, const sdb_model* m) {
+    if (!d) return fail_with(ctx, SDB_ERR_ARGUMENT, "null descriptor");
+    if (!m) return fail_with(ctx, SDB_ERR_ARGUMENT, "null model");
+    if (d->model != SDB_MODEL_EXPRESSION)
+        return fail_with(ctx, SDB_ERR_ARGUMENT, "descriptor model must be SDB_MODEL_EXPRESSION");
+    if (d->nequat != m->nequat || d->nparams != m->nparams || d->nnoise != m->nnoise)
+        return fail_with(ctx, SDB_ERR_ARGUMENT, "descriptor dimensions (%d, %d, %d) do not match "
+                         "the model (%d, %d, %d)", d->nequat, d->nparams, d->nnoise, m->nequat,
+                         m->nparams, m->nnoise);
+    if (d->solver != SDB_SOLVER_EM && d->solver != SDB_SOLVER_EULER && d->solver != SDB_SOLVER_RK4)
+        return fail_with(ctx, SDB_ERR_ARGUMENT, "unknown solver %d", d->solver);
+    if (d->solver != SDB_SOLVER_EM && d->nnoise > 0)
+        return fail_with(ctx, SDB_ERR_CONFIG,
+                         "solver is deterministic but the model has %d noise terms", d->nnoise);
+    if (d->stream < SDB_STREAM_PHILOX || d->stream > SDB_STREAM_XOSHIRO256PP)
+        return fail_with(ctx, SDB_ERR_ARGUMENT, "unknown stream %d", d->stream);
+    if (!(d->dt > 0.0)) return fail_with(ctx, SDB_ERR_CONFIG, "dt must be positive");
+    if (d->ksteps < 1) return fail_with(ctx, SDB_ERR_CONFIG, "ksteps must be >= 1");
+    if (d->chunks < 1) return fail_with(ctx, SDB_ERR_CONFIG, "chunks must be >= 1");
+    if (d->orbits < 1) return fail_with(ctx, SDB_ERR_CONFIG, "orbits must be >= 1");
+    if (d->orbit_offset < 0 || d->orbit_offset + d->orbits > (int64_t(1) << 32))
+        return fail_with(ctx, SDB_ERR_CONFIG, "global orbit ids must fit in 32 bits");
+    if (d->chunks > INT64_MAX / d->ksteps)
+        return fail_with(ctx, SDB_ERR_CONFIG, "total step count does not fit in 63 bits");
+    return SDB_OK;
+}
+
+// Host-buffer run over all of the context's devices (validated descriptor).
+sdb_status run_host(sdb_ctx* ctx, const sdb_desc& d, sdb_model* m, const double* init,
+                    const double* params, double* values, int64_t* fail_step) {
+    if (!init || !params || !values || !fail_step)
+        return fail_with(ctx, SDB_ERR_ARGUMENT, "null host buffer");
+    const int64_t nslots = int64_t(ctx->slots.size());
+    const int64_t used = std::min<int64_t>(nslots, d.orbits);
+    std::vector<sdb_status> status(used, SDB_OK);
+    std::vector<std::thread> threads;
+    for (Slot& s : ctx->slots) {
+        s.launches = 0;
+        s.error.clear();
+    }
+    // contiguous shards [g*M/G, (g+1)*M/G) (SURVEY.md 8e)
+    auto shard = [&](int64_t g) {
+        const int64_t r0 = g * d.orbits / used, r1 = (g + 1) * d.orbits / used;
+        status[g] = run_shard(ctx, ctx->slots[g], d, m, r0, r1 - r0, init, params, values,
+                              fail_step, int(used));
+    };
+    if (used == 1) {
+        shard(0);
+    } else {
+        for (int64_t g = 0; g < used; ++g) threads.emplace_back(shard, g);
+        for (auto& t : threads) t.join();
+    }
+    ctx->launches = 0;
+    for (int64_t g = 0; g < used; ++g) ctx->launches += ctx->slots[g].launches;
+    ctx->last_lanes = ctx->slots[0].lanes;
+    ctx->last_persistent = ctx->slots[0].persistent;
+    ctx->last_ctas_per_sm = ctx->slots[0].ctas_per_sm;
+    ctx->last_tight = ctx->slots[0].tight;
+    ctx->last_tiles = ctx->slots[0].tiles;
+    for (int64_t g = 0; g < used; ++g)
+        if (status[g] != SDB_OK) return status[g];
+    return SDB_OK;
+}
+
+// Device-buffer run on the first device (validated descriptor).
+sdb_status run_dev(sdb_ctx* ctx, const sdb_desc& d, sdb_model* m, const double* d_init,
+                   const double* d_params, double* d_values, int64_t* d_fail_step, void* stream) {
+    if (!d_init || !d_params || !d_values || !d_fail_step)
+        return fail_with(ctx, SDB_ERR_ARGUMENT, "null device buffer");
+    Slot& s = ctx->slots[0];
+    SDB_CUDA(ctx, cudaSetDevice(s.device));
+    s.launches = 0;
+    sdb_status rc = launch_device(ctx, s, d, m, d_init, d_params, d_values, d_fail_step,
+                                  static_cast<cudaStream_t>(stream));
+    ctx->launches = s.launches;
+    ctx->last_lanes = s.lanes;
+    ctx->last_persistent = s.persistent;
+    ctx->last_ctas_per_sm = s.ctas_per_sm;
+    ctx->last_tight = s.tight;
+    ctx->last_tiles = 0;
+    return rc;
+}
+
+// Row-wise program (eval / one step) over host arrays: y [count][N], p
+// [count][NP], noise [count][NN] or null, out [count][N].
+sdb_status model_rows(sdb_ctx* ctx, sdb_model* m, int kind, double t, double dt, int64_t count,
+                      const double* y, const double* p, const double* noise, double* out) {
+    sdb_status rc = utility_prologue(ctx);
+    if (rc != SDB_OK) return rc;
+    if (count < 0 || !y || !p || !out) return fail_with(ctx, SDB_ERR_ARGUMENT, "bad row arrays");
+    if (count == 0) return SDB_OK;
+    const size_t n = size_t(m->nequat), np_ = size_t(m->nparams), nn = size_t(m->nnoise);
+    TmpBuf dy, dp, dn, dout;
+    SDB_CUDA(ctx, cudaMalloc(&dy.p, count * n * sizeof(double)));
+    SDB_CUDA(ctx, cudaMalloc(&dp.p, count * std::max<size_t>(np_, 1) * sizeof(double)));
+    SDB_CUDA(ctx, cudaMalloc(&dout.p, count * n * sizeof(double)));
+    SDB_CUDA(ctx, cudaMemcpy(dy.p, y, count * n * sizeof(double), cudaMemcpyHostToDevice));
+    if (np_) SDB_CUDA(ctx, cudaMemcpy(dp.p, p, count * np_ * sizeof(double), cudaMemcpyHostToDevice));
+    if (noise && nn) {
+        SDB_CUDA(ctx, cudaMalloc(&dn.p, count * nn * sizeof(double)));
+        SDB_CUDA(ctx, cudaMemcpy(dn.p, noise, count * nn * sizeof(double), cudaMemcpyHostToDevice));
+    }
+    sdeb::DslArgs a{};
+    a.state_in = static_cast<const double*>(dy.p);
+    a.params = static_cast<const double*>(dp.p);
+    a.noise = static_cast<const double*>(dn.p);
+    a.state_out = static_cast<double*>(dout.p);
+    a.values = static_cast<double*>(dout.p);
+    a.rows = count;
+    a.t = t;
+    a.dt = dt;
+    a.sqrt_dt = dt > 0.0 ? std::sqrt(dt) : 0.0;
+    TmpBuf scratch;
+    if (sdeb_dsl::global_state(m)) {
+        SDB_CUDA(ctx, cudaMalloc(&scratch.p, count * sdeb_dsl::state_words(m) * sizeof(double)));
+        a.scratch = static_cast<double*>(scratch.p);
+    }
+    std::string err;
+    cudaError_t e = sdeb_dsl::launch(m, kind, a, nullptr, &err);
+    if (e != cudaSuccess) return fail_with(ctx, SDB_ERR_CUDA, "%s", err.c_str());
+    SDB_CUDA(ctx, cudaMemcpy(out, dout.p, count * n * sizeof(double), cudaMemcpyDeviceToHost));
+    ctx->launches = 1;
+    return SDB_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -841,7 +1018,7 @@ void sdb_close(sdb_ctx* ctx) {
     if (!ctx) return;
     for (Slot& s : ctx->slots) {
         cudaSetDevice(s.device);
-        for (DevBuf* b : {&s.init, &s.params, &s.values, &s.state, &s.fail, &s.rng, &s.work,
+        for (DevBuf* b : {&s.init, &s.params, &s.values, &s.state, &s.fail, &s.rng, &s.work, &s.scratch,
                           &s.t_values, &s.t_state, &s.t_fail, &s.t_rng, &s.t_work})
             b->release();
         for (PinBuf* b : {&s.pin_in[0], &s.pin_in[1], &s.pin_out[0], &s.pin_out[1]}) b->release();
@@ -876,40 +1053,7 @@ sdb_status sdb_run(sdb_ctx* ctx, const sdb_desc* desc, const double* init, const
     ctx->error.clear();
     sdb_status rc = validate(ctx, desc);
     if (rc != SDB_OK) return rc;
-    if (!init || !params || !values || !fail_step)
-        return fail_with(ctx, SDB_ERR_ARGUMENT, "null host buffer");
-    const sdb_desc d = *desc;
-    const int n = d.nequat;
-    const int64_t nslots = int64_t(ctx->slots.size());
-    const int64_t used = std::min<int64_t>(nslots, d.orbits);
-    std::vector<sdb_status> status(used, SDB_OK);
-    std::vector<std::thread> threads;
-    for (Slot& s : ctx->slots) {
-        s.launches = 0;
-        s.error.clear();
-    }
-    // contiguous shards [g*M/G, (g+1)*M/G) (SURVEY.md 8e)
-    auto shard = [&](int64_t g) {
-        const int64_t r0 = g * d.orbits / used, r1 = (g + 1) * d.orbits / used;
-        status[g] = run_shard(ctx, ctx->slots[g], d, r0, r1 - r0, init, params, values, fail_step,
-                              int(used));
-    };
-    if (used == 1) {
-        shard(0);
-    } else {
-        for (int64_t g = 0; g < used; ++g) threads.emplace_back(shard, g);
-        for (auto& t : threads) t.join();
-    }
-    ctx->launches = 0;
-    for (int64_t g = 0; g < used; ++g) ctx->launches += ctx->slots[g].launches;
-    ctx->last_lanes = ctx->slots[0].lanes;
-    ctx->last_persistent = ctx->slots[0].persistent;
-    ctx->last_ctas_per_sm = ctx->slots[0].ctas_per_sm;
-    ctx->last_tight = ctx->slots[0].tight;
-    ctx->last_tiles = ctx->slots[0].tiles;
-    for (int64_t g = 0; g < used; ++g)
-        if (status[g] != SDB_OK) return status[g];
-    return SDB_OK;
+    return run_host(ctx, *desc, nullptr, init, params, values, fail_step);
 }
 
 sdb_status sdb_run_device(sdb_ctx* ctx, const sdb_desc* desc, const double* d_init,
@@ -919,20 +1063,103 @@ sdb_status sdb_run_device(sdb_ctx* ctx, const sdb_desc* desc, const double* d_in
     ctx->error.clear();
     sdb_status rc = validate(ctx, desc);
     if (rc != SDB_OK) return rc;
-    if (!d_init || !d_params || !d_values || !d_fail_step)
-        return fail_with(ctx, SDB_ERR_ARGUMENT, "null device buffer");
-    Slot& s = ctx->slots[0];
-    SDB_CUDA(ctx, cudaSetDevice(s.device));
-    s.launches = 0;
-    rc = launch_device(ctx, s, *desc, d_init, d_params, d_values, d_fail_step,
-                       static_cast<cudaStream_t>(stream));
-    ctx->launches = s.launches;
-    ctx->last_lanes = s.lanes;
-    ctx->last_persistent = s.persistent;
-    ctx->last_ctas_per_sm = s.ctas_per_sm;
-    ctx->last_tight = s.tight;
-    ctx->last_tiles = 0;
-    return rc;
+    return run_dev(ctx, *desc, nullptr, d_init, d_params, d_values, d_fail_step, stream);
+}
+
+/* ---- expression-template models ------------------------------------------ */
+
+sdb_status sdb_model_create(int32_t nequat, int32_t nparams, int32_t nnoise, const char* drift,
+                            const char* diffusion, sdb_model** out) {
+    if (!out || !drift || !diffusion)
+        return fail_with(nullptr, SDB_ERR_ARGUMENT, "null model argument");
+    *out = nullptr;
+    if (nequat < 1 || nparams < 0 || nnoise < 0)
+        return fail_with(nullptr, SDB_ERR_ARGUMENT, "bad model dimensions (%d, %d, %d)", nequat,
+                         nparams, nnoise);
+    auto* m = new sdb_model();
+    m->nequat = nequat;
+    m->nparams = nparams;
+    m->nnoise = nnoise;
+    m->drift_text = drift;
+    m->diffusion_text = diffusion;
+    std::string err;
+    if (!sdeb_dsl::generate(m, &err)) {
+        delete m;
+        return fail_with(nullptr, SDB_ERR_ARGUMENT, "%s", err.c_str());
+    }
+    *out = m;
+    return SDB_OK;
+}
+
+void sdb_model_free(sdb_model* m) { delete m; }
+
+int64_t sdb_model_source(const sdb_model* m, int32_t kind, char* buf, int64_t cap) {
+    if (!m || kind < 0 || kind >= sdeb::DK_COUNT) return -1;
+    const std::string src = sdeb_dsl::program_source(m, kind);
+    if (buf && cap > 0) {
+        const size_t n = std::min<size_t>(src.size(), size_t(cap - 1));
+        std::memcpy(buf, src.data(), n);
+        buf[n] = '\0';
+    }
+    return int64_t(src.size());
+}
+
+sdb_status sdb_model_build(sdb_model* m, int32_t kind) {
+    if (!m || kind < 0 || kind >= sdeb::DK_COUNT)
+        return fail_with(nullptr, SDB_ERR_ARGUMENT, "bad model or program kind");
+    std::string err;
+    cudaError_t e = sdeb_dsl::compile_only(m, kind, &err);
+    if (e != cudaSuccess) return fail_with(nullptr, SDB_ERR_CUDA, "%s", err.c_str());
+    return SDB_OK;
+}
+
+sdb_status sdb_run_model(sdb_ctx* ctx, sdb_model* m, const sdb_desc* desc, const double* init,
+                         const double* params, double* values, int64_t* fail_step) {
+    if (!ctx) return fail_with(nullptr, SDB_ERR_ARGUMENT, "null context");
+    ctx->error.clear();
+    sdb_status rc = validate_model(ctx, desc, m);
+    if (rc != SDB_OK) return rc;
+    return run_host(ctx, *desc, m, init, params, values, fail_step);
+}
+
+sdb_status sdb_run_model_device(sdb_ctx* ctx, sdb_model* m, const sdb_desc* desc,
+                                const double* d_init, const double* d_params, double* d_values,
+                                int64_t* d_fail_step, void* stream) {
+    if (!ctx) return fail_with(nullptr, SDB_ERR_ARGUMENT, "null context");
+    ctx->error.clear();
+    sdb_status rc = validate_model(ctx, desc, m);
+    if (rc != SDB_OK) return rc;
+    return run_dev(ctx, *desc, m, d_init, d_params, d_values, d_fail_step, stream);
+}
+
+sdb_status sdb_model_eval(sdb_ctx* ctx, sdb_model* m, int32_t which, double t, int64_t count,
+                          const double* y, const double* p, const double* noise, double* out) {
+    if (!m) return fail_with(ctx, SDB_ERR_ARGUMENT, "null model");
+    if (which != 0 && which != 1) return fail_with(ctx, SDB_ERR_ARGUMENT, "which must be 0 or 1");
+    if (which == 1 && m->nnoise > 0 && !noise)
+        return fail_with(ctx, SDB_ERR_ARGUMENT, "diffusion needs a noise array");
+    return model_rows(ctx, m, which == 0 ? sdeb::DK_EVAL_DRIFT : sdeb::DK_EVAL_DIFFUSION, t, 0.0,
+                      count, y, p, which == 1 ? noise : nullptr, out);
+}
+
+sdb_status sdb_model_step(sdb_ctx* ctx, sdb_model* m, int32_t solver, double t, double dt,
+                          int64_t count, const double* y, const double* p, const double* noise,
+                          double* out) {
+    if (!m) return fail_with(ctx, SDB_ERR_ARGUMENT, "null model");
+    if (!(dt > 0.0)) return fail_with(ctx, SDB_ERR_ARGUMENT, "dt must be positive");
+    int kind;
+    if (solver == SDB_SOLVER_RK4) {
+        kind = sdeb::DK_STEP_RK4;
+    } else if (solver == SDB_SOLVER_EM && m->nnoise > 0) {
+        if (!noise) return fail_with(ctx, SDB_ERR_ARGUMENT, "em step needs a noise array");
+        kind = sdeb::DK_STEP_EM;
+    } else if (solver == SDB_SOLVER_EM || solver == SDB_SOLVER_EULER) {
+        kind = sdeb::DK_STEP_EULER;
+    } else {
+        return fail_with(ctx, SDB_ERR_ARGUMENT, "unknown solver %d", solver);
+    }
+    return model_rows(ctx, m, kind, t, dt, count, y, p, kind == sdeb::DK_STEP_EM ? noise : nullptr,
+                      out);
 }
 
 sdb_status sdb_philox_words(sdb_ctx* ctx, const uint32_t* in, int64_t count, uint32_t* out) {

@@ -1,0 +1,65 @@
+// Runtime code generation for expression-template models (host side).
+//
+// The reference evaluates drift/diffusion templates with a numpy tree-walking
+// interpreter (dsl.py:441-571).  Here the template text (the grammar of
+// dsl.py:12-19, in the canonical form dsl.to_source prints) is parsed once,
+// turned into CUDA device functions, spliced into sdeb_dsl_kernel.cuh and
+// compiled by NVRTC for sm_100a -- the paper's own mechanism of generating
+// the system's GPU source at run time.  Programs are cached
+// per (model, kind).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+
+#include "sdeb_dsl_args.h"
+
+struct sdb_model {
+    int32_t nequat = 0, nparams = 0, nnoise = 0;
+    std::string drift_text, diffusion_text;  // as given
+    std::string drift_cu, diffusion_cu;      // generated device functions
+    std::string error;                       // last compile / launch error
+    std::mutex mu;
+    struct Program {
+        cudaLibrary_t lib = nullptr;
+        cudaKernel_t kernel = nullptr;
+        std::string log;
+    };
+    std::map<int, Program> programs;  // by sdeb::DslKind
+    ~sdb_model();
+};
+
+namespace sdeb_dsl {
+
+// Parse both templates and generate their device code.  On failure returns
+// false with `err` = "drift: line L, column C: message" style text.
+bool generate(sdb_model* m, std::string* err);
+
+// Full CUDA source of one program kind (for inspection / tests).
+std::string program_source(const sdb_model* m, int kind);
+
+// NVRTC compile only (no device needed); the log lands in m->error.
+cudaError_t compile_only(sdb_model* m, int kind, std::string* err);
+
+// The compiled kernel of one kind (compiled on first use, thread-safe).
+cudaError_t kernel_for(sdb_model* m, int kind, cudaKernel_t* out, std::string* err);
+
+// Launch one program over `a.rows` rows (one thread per orbit).
+cudaError_t launch(sdb_model* m, int kind, const sdeb::DslArgs& a, cudaStream_t st,
+                   std::string* err);
+
+constexpr int kBlock = 128;      // threads per CTA (fewer when the state columns need it)
+constexpr int kSmemMax = 96 * 1024;
+constexpr int kUnrollWork = 32;  // unroll equation loops while N x evaluations <= this
+
+// Doubles per orbit in the strided state column: y + one step's normals.
+int state_words(const sdb_model* m);
+// True when the columns go to global scratch ([words][rows]) instead of shared memory.
+bool global_state(const sdb_model* m);
+// CTA width of a shared-memory program.
+int threads_for(const sdb_model* m);
+
+}  // namespace sdeb_dsl

@@ -19,7 +19,7 @@
 // and cos even, which the antisymmetric pairwise tiling relies on.
 // |x| >= 2^29 falls back to libdevice sincos (exact Payne-Hanek reduction).
 #pragma once
-#include <cstdint>
+#include "sdeb_cstdint.cuh"
 
 #include "sdeb_log_table.cuh"
 #include "sdeb_sincos_table.cuh"

@@ -7,7 +7,7 @@
 // SplitMix64 / sfc64 / xoshiro256++ are the extra per-(orbit, block) streams
 // DESIGN.md defines ("Noise streams"); they are not in the reference.
 #pragma once
-#include <cstdint>
+#include "sdeb_cstdint.cuh"
 
 #include "sdeb_math.cuh"
 

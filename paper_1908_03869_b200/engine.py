@@ -31,7 +31,8 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _native as nat
-from .model import ModelSpec, OrbitBatch, require_kuramoto
+from .model import (ModelSpec, OrbitBatch, expression_model, kuramoto_signature,
+                    require_device_model)
 from .solvers import get_solver
 
 __all__ = [
@@ -179,9 +180,11 @@ def _check_stepper(model: ModelSpec, config: EngineConfig):
 def make_desc(model: ModelSpec, config: EngineConfig, chunks: int, orbits: int,
               orbit_offset: int = 0) -> nat.SdbDesc:
     """Descriptor for the C ABI (include/sdeb200.h sdb_desc)."""
-    n, nnoise = require_kuramoto(model)
+    require_device_model(model)
+    sig = kuramoto_signature(model)
+    n, nnoise = sig if sig is not None else (model.nequat, model.nnoise)
     d = nat.SdbDesc()
-    d.model = nat.SDB_MODEL_KURAMOTO
+    d.model = nat.SDB_MODEL_KURAMOTO if sig is not None else nat.SDB_MODEL_EXPRESSION
     d.nequat = n
     d.nparams = model.nparams
     d.nnoise = nnoise
@@ -250,6 +253,10 @@ def run_batch(model: ModelSpec, config: EngineConfig, batch: OrbitBatch, *,
             % (store_bytes, batch.orbits, samples, model.nequat, config.max_store_bytes))
     _check_stepper(model, config)
     desc = make_desc(model, config, chunks, batch.orbits, orbit_offset)
+    if desc.model == nat.SDB_MODEL_EXPRESSION:
+        # indices are checked up front: the reference raises DomainError at step 0
+        from . import program
+        program.check_model_indices(model)
 
     sample_dt = config.ksteps * config.dt
     times = np.arange(samples, dtype=np.float64) * sample_dt
@@ -258,8 +265,14 @@ def run_batch(model: ModelSpec, config: EngineConfig, batch: OrbitBatch, *,
     init = nat.f64(batch.init)
     params = nat.f64(batch.params)
     ctx = nat.context(config.devices)
-    nat.check(nat.lib().sdb_run(ctx, desc, nat.dptr(init), nat.dptr(params), nat.dptr(values),
-                                nat.i64ptr(fail_step)), ctx, "sdb_run")
+    if desc.model == nat.SDB_MODEL_EXPRESSION:
+        cm = program.model_program(model)  # compiled expression-template program
+        nat.check(nat.lib().sdb_run_model(ctx, cm.handle, desc, nat.dptr(init), nat.dptr(params),
+                                          nat.dptr(values), nat.i64ptr(fail_step)),
+                  ctx, "sdb_run_model")
+    else:
+        nat.check(nat.lib().sdb_run(ctx, desc, nat.dptr(init), nat.dptr(params),
+                                    nat.dptr(values), nat.i64ptr(fail_step)), ctx, "sdb_run")
     failures = failures_from_steps(fail_step, config.ksteps, config.dt, orbit_offset)
     return TrajectoryStore(times=times, values=values, model_name=model.name,
                            config=config, failures=failures)

@@ -1,8 +1,9 @@
 """Single-step integrators (drop-in for ``sdebatch.solvers``,
 /root/reference/pkg/src/sdebatch/solvers.py).
 
-em / euler / rk4 run on the GPU (sdb_step) with the reference's operation
-order (solvers.py:63-88).  The implicit fixed-point steppers (ie, im;
+em / euler / rk4 run on the GPU with the reference's operation order
+(solvers.py:63-88): sdb_step for the Kuramoto system, the compiled program's
+step kernel (sdb_model_step) for expression-template models.  The implicit fixed-point steppers (ie, im;
 solvers.py:91-137) are registered with the same metadata so configuration
 validation behaves identically, but they are outside the device path this
 round and raise NotImplementedError when executed.
@@ -67,11 +68,22 @@ def get_solver(name: str) -> SolverInfo:
                          % (name, ", ".join(sorted(SOLVERS))))
 
 
-def _device_step(solver: str, model, y, p, dt, noise=None, coupling="meanfield"):
-    from .model import _check_dims, _rows, require_kuramoto
+def _device_step(solver: str, model, y, p, dt, noise=None, coupling="meanfield", t=0.0):
+    from .model import _check_dims, _rows, expression_model, require_kuramoto
     y = np.asarray(y, dtype=np.float64)
     p = np.asarray(p, dtype=np.float64)
     _check_dims(model, y, p)
+    if expression_model(model):
+        from . import program
+        program.check_model_indices(model)
+        if solver == "em" and model.nnoise > 0:
+            noise = np.asarray(noise, dtype=np.float64)
+            if noise.shape[-1] != model.nnoise:
+                raise ValueError("noise vector has length %d, model has nnoise=%d"
+                                 % (noise.shape[-1], model.nnoise))
+        else:
+            noise = None
+        return program.step_rows(program.model_program(model), solver, t, y, p, dt, noise)
     n, nnoise = require_kuramoto(model)
     lead, yy, pp = _rows(y, p)
     nz = None
@@ -95,17 +107,17 @@ def euler_maruyama_step(model, t: float, y, p, dt: float, noise, coupling="meanf
     """One Euler-Maruyama step (solvers.py:63-71); nnoise = 0 is exactly euler."""
     if model.nnoise == 0:
         return euler_step(model, t, y, p, dt, coupling=coupling)
-    return _device_step("em", model, y, p, dt, noise, coupling)
+    return _device_step("em", model, y, p, dt, noise, coupling, t)
 
 
 def euler_step(model, t: float, y, p, dt: float, coupling="meanfield"):
     """One explicit Euler step (solvers.py:74-77)."""
-    return _device_step("euler", model, y, p, dt, None, coupling)
+    return _device_step("euler", model, y, p, dt, None, coupling, t)
 
 
 def rk4_step(model, t: float, y, p, dt: float, coupling="meanfield"):
     """One classical RK4 step (solvers.py:80-88)."""
-    return _device_step("rk4", model, y, p, dt, None, coupling)
+    return _device_step("rk4", model, y, p, dt, None, coupling, t)
 
 
 def implicit_euler_step(model, t, y, p, dt, tol=DEFAULT_TOL, max_iter=DEFAULT_MAX_ITER,

@@ -52,3 +52,13 @@ def case_config(case):
     cfg = dict(case["config"])
     cfg["seed"] = int(cfg["seed"])
     return cfg
+
+
+@pytest.fixture(scope="session")
+def golden_dsl():
+    """Reference run_batch / drift_eval outputs for expression-template models
+    (tests/golden/make_golden_dsl.py)."""
+    data = np.load(os.path.join(GOLDEN_DIR, "golden_dsl_v1.npz"))
+    with open(os.path.join(GOLDEN_DIR, "cases_dsl.json")) as fh:
+        cases = json.load(fh)
+    return {k: data[k] for k in data.files}, cases

@@ -111,8 +111,8 @@ def test_unsupported_models_raise_not_implemented():
     cfg = EngineConfig(dt=0.1, tspan=1.0, ksteps=10, orbits=1)
     with pytest.raises(NotImplementedError):
         run_batch(lam, cfg, OrbitBatch(init=np.ones((1, 1)), params=np.empty((1, 0))))
-    with pytest.raises(NotImplementedError):
-        sdb.model_from_dsl("x", 1, 1, 0, "0 - p[0]*y[0]", "0")
+    # expression templates are compiled (program.py), not rejected
+    assert sdb.model.expression_model(sdb.model_from_dsl("x", 1, 1, 0, "0 - p[0]*y[0]", "0"))
     ode = ModelSpec(name="k0", nequat=2, nparams=5, nnoise=0, drift=sdb.model._kuramoto_drift)
     with pytest.raises(NotImplementedError):
         run_batch(ode, EngineConfig(dt=0.1, tspan=1.0, ksteps=10, orbits=1, solver="ie"),
