@@ -64,11 +64,38 @@ WORKLOADS = {
     "cfg5": dict(n=32, orbits=131072, dt=1e-3, steps=1000, ksteps=10, stream="philox",
                  solver="em", batch="resample",
                  desc="n=32, 512 parameter sets x 256 realisations, trajectory every 10 steps"),
+    # expression-template models through the NVRTC-generated program
+    "cfg2_codegen": dict(n=16, orbits=65536, dt=1e-3, steps=10000, ksteps=10000, stream="sfc64",
+                         solver="em", batch="kgrid", model="kuramoto_template",
+                         desc="cfg2 through the generated program of the Kuramoto templates "
+                              "(model_from_dsl, n^2 sin terms in the reference's order)"),
+    "ou_codegen": dict(n=16, orbits=65536, dt=1e-3, steps=10000, ksteps=1000, stream="philox",
+                       solver="em", batch="uniform", model="ou",
+                       desc="Ornstein-Uhlenbeck template model (drift p[0]*(p[1]-y[i]), "
+                            "diffusion p[2+i]*n[i]), n=16, 65,536 orbits, 10 samples"),
+}
+
+# expression-template workloads: (drift, diffusion, nparams(n))
+TEMPLATES = {
+    "kuramoto_template": ("p[i+1] + (p[0]/N) * sum(j, sin(y[j] - y[i]))", "p[1+N+i] * n[i]",
+                          lambda n: 2 * n + 1),
+    "ou": ("p[0]*(p[1] - y[i])", "p[2 + i]*n[i]", lambda n: n + 2),
 }
 
 
 SINCOS_OPS = 17      # csrc/sdeb_math.cuh sincos_tab: 5 reduction + 8 poly + 4 rotation
 BOX_MULLER_PAIR = 44  # 2 uniforms, log 13, -2*log 1, sqrt 8, angle 1, sincos 17, 2 products
+
+
+def template_fp64_ops(n: int, model: str) -> float:
+    """FP64 lane-ops per orbit-step of the generated program (counted from the
+    generated code): Kuramoto template n^2 terms x (difference 1, sin 15 --
+    the table sincos minus its cos-only ops --, sum 1) + per equation
+    (K/N 2, omega + 1) + noise 22 + update 5; OU 2 drift + 1 diffusion + noise
+    22 + update 5 per equation."""
+    if model == "kuramoto_template":
+        return n * n * 17 + n * (3 + 22 + 5 + 1)
+    return n * (2 + 1 + 22 + 5)
 
 
 def algorithmic_fp64_ops(n: int, solver: str, coupling: str) -> float:
@@ -131,11 +158,19 @@ def make_batch(sdb, w, orbit_offset: int, seed: int = 20260809):
         params[:, 0] = np.linspace(0.05, 0.8, 16)[np.arange(sets) % 16]
         return sdb.OrbitBatch(init=np.repeat(b.init, 256, axis=0),
                               params=np.repeat(params, 256, axis=0))
+    if w["batch"] == "uniform":  # generic template models: seeded uniform draws
+        g = np.random.default_rng(seed + orbit_offset)
+        nparams = TEMPLATES[w["model"]][2](n)
+        return sdb.OrbitBatch(init=g.uniform(-1.0, 1.0, (m, n)),
+                              params=g.uniform(0.05, 0.5, (m, nparams)))
     raise ValueError(w["batch"])
 
 
 def make_model(sdb, w):
     n = w["n"]
+    if "model" in w:
+        drift, diffusion, nparams = TEMPLATES[w["model"]]
+        return sdb.model_from_dsl(w["model"], n, nparams(n), n, drift, diffusion)
     if w["solver"] == "rk4":
         return sdb.ModelSpec(name="kuramoto-ode:%d" % n, nequat=n, nparams=2 * n + 1, nnoise=0,
                              drift=sdb.model._kuramoto_drift)
@@ -251,11 +286,18 @@ def cpu_sample_rate(w, seconds: float, threads: int, stream_override=None):
     stream = stream_override or w["stream"]
     group = max(1, m_cpu // threads)
     nnoise = 0 if w["solver"] == "rk4" else n
+    fns = {}
+    if "model" in w:  # the reference's interpreter, restated (oracle.expression_model)
+        drift_t, diffusion_t, nparams = TEMPLATES[w["model"]]
+        fns = dict(zip(("drift", "diffusion"), O.expression_model(drift_t, diffusion_t)))
+        g = np.random.default_rng(1)
+        params = g.uniform(0.05, 0.5, (m_cpu, nparams(n)))
 
     def run(steps):
         t0 = time.perf_counter()
         O.integrate(init, params, dt=w["dt"], ksteps=steps, chunks=1, seed=1,
-                    solver=w["solver"], nnoise=nnoise, stream=stream, threads=threads, group=group)
+                    solver=w["solver"], nnoise=nnoise, stream=stream, threads=threads, group=group,
+                    **fns)
         return time.perf_counter() - t0
 
     probe = 3
@@ -315,6 +357,8 @@ def run_ours(args, w, world, rank, local, dist):
     from paper_1908_03869_b200.engine import make_desc
 
     torch.cuda.set_device(local)
+    if w.get("model") == "kuramoto_template":
+        os.environ["SDEB200_NO_NATIVE_KURAMOTO"] = "1"  # the generated program, not the stepper
     n, m, steps = w["n"], w["orbits"], w["steps"]
     chunks = steps // w["ksteps"]
     model = make_model(sdb, w)
@@ -336,7 +380,18 @@ def run_ours(args, w, world, rank, local, dist):
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
     stream = torch.cuda.current_stream()
 
+    program_handle = None
+    if desc.model == nat.SDB_MODEL_EXPRESSION:
+        from paper_1908_03869_b200 import program
+        program_handle = program.model_program(model).handle
+
     def launch():
+        if program_handle is not None:
+            nat.check(lib.sdb_run_model_device(ctx, program_handle, desc, d_init.data_ptr(),
+                                               d_params.data_ptr(), d_values.data_ptr(),
+                                               d_fail.data_ptr(), stream.cuda_stream),
+                      ctx, "sdb_run_model_device")
+            return
         nat.check(lib.sdb_run_device(ctx, desc, d_init.data_ptr(), d_params.data_ptr(),
                                      d_values.data_ptr(), d_fail.data_ptr(), stream.cuda_stream),
                   ctx, "sdb_run_device")
@@ -392,7 +447,8 @@ def run_ours(args, w, world, rank, local, dist):
 
     # --- roofline (FP64 pipe) ---
     peak_ops = ctypes_peak(lib, ctx)
-    ops = algorithmic_fp64_ops(n, w["solver"], args.coupling)
+    ops = (template_fp64_ops(n, w["model"]) if "model" in w
+           else algorithmic_fp64_ops(n, w["solver"], args.coupling))
     achieved = ops * orbit_steps / (np.mean(kernel_ms) * 1e-3)
     roofline = {
         "bound": "fp64", "unit": "TFLOP/s",
@@ -420,6 +476,7 @@ def run_ours(args, w, world, rank, local, dist):
                        "solver": w["solver"], "stream": w["stream"], "coupling": args.coupling,
                        "lanes_per_orbit": lanes, "persistent_grid": bool(persistent),
                        "ctas_per_sm": ctas_per_sm, "register_capped": bool(variant),
+                       "template_model": w.get("model"),
                        "parallelism": "orbit-shard x%d" % world,
                        "l2": "flushed (512 MiB memset) between timed steps, outside the "
                              "event pairs"},

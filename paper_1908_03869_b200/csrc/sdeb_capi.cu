@@ -541,15 +541,15 @@ sdb_status launch_model(sdb_ctx* ctx, Slot& s, const sdb_desc& d, sdb_model* m,
     a.dt = d.dt;
     a.sqrt_dt = std::sqrt(d.dt);
     a.fresh = 1;
-    if (sdeb_dsl::global_state(m)) {
-        SDB_CUDA(ctx, s.scratch.ensure(size_t(d.orbits) * sdeb_dsl::state_words(m) * sizeof(double)));
+    if (const size_t words = sdeb_dsl::scratch_doubles(m, sdeb_dsl::lanes_for(m), d.orbits)) {
+        SDB_CUDA(ctx, s.scratch.ensure(words * sizeof(double)));
         a.scratch = s.scratch.as<double>();
     }
     std::string err;
     cudaError_t e = sdeb_dsl::launch(m, kind, a, st, &err);
     if (e != cudaSuccess) return fail_with(ctx, SDB_ERR_CUDA, "%s", err.c_str());
     s.launches += 1;
-    s.lanes = 1;
+    s.lanes = sdeb_dsl::lanes_for(m);
     s.persistent = 0;
     s.ctas_per_sm = 0;
     s.tight = 0;
@@ -953,8 +953,8 @@ sdb_status model_rows(sdb_ctx* ctx, sdb_model* m, int kind, double t, double dt,
     a.dt = dt;
     a.sqrt_dt = dt > 0.0 ? std::sqrt(dt) : 0.0;
     TmpBuf scratch;
-    if (sdeb_dsl::global_state(m)) {
-        SDB_CUDA(ctx, cudaMalloc(&scratch.p, count * sdeb_dsl::state_words(m) * sizeof(double)));
+    if (const size_t words = sdeb_dsl::scratch_doubles(m, sdeb_dsl::lanes_for(m), count)) {
+        SDB_CUDA(ctx, cudaMalloc(&scratch.p, words * sizeof(double)));
         a.scratch = static_cast<double*>(scratch.p);
     }
     std::string err;
@@ -1095,7 +1095,7 @@ void sdb_model_free(sdb_model* m) { delete m; }
 
 int64_t sdb_model_source(const sdb_model* m, int32_t kind, char* buf, int64_t cap) {
     if (!m || kind < 0 || kind >= sdeb::DK_COUNT) return -1;
-    const std::string src = sdeb_dsl::program_source(m, kind);
+    const std::string src = sdeb_dsl::program_source(m, kind, sdeb_dsl::lanes_for(m));
     if (buf && cap > 0) {
         const size_t n = std::min<size_t>(src.size(), size_t(cap - 1));
         std::memcpy(buf, src.data(), n);
@@ -1108,7 +1108,7 @@ sdb_status sdb_model_build(sdb_model* m, int32_t kind) {
     if (!m || kind < 0 || kind >= sdeb::DK_COUNT)
         return fail_with(nullptr, SDB_ERR_ARGUMENT, "bad model or program kind");
     std::string err;
-    cudaError_t e = sdeb_dsl::compile_only(m, kind, &err);
+    cudaError_t e = sdeb_dsl::compile_only(m, kind, sdeb_dsl::lanes_for(m), &err);
     if (e != cudaSuccess) return fail_with(nullptr, SDB_ERR_CUDA, "%s", err.c_str());
     return SDB_OK;
 }

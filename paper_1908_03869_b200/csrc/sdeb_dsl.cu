@@ -248,6 +248,7 @@ std::string literal(double v) {
 class Gen {
   public:
     explicit Gen(bool has_noise) : has_noise_(has_noise) {}
+    bool used_sum = false;
 
     // Double-valued expression (dsl.py _Evaluator.eval).
     std::string num(const Node& n) {
@@ -280,8 +281,8 @@ class Gen {
             }
             case Node::CALL: {
                 const std::string x = num(*n.a);
-                if (n.name == "sin") return "dsl_sin(" + x + ")";
-                if (n.name == "cos") return "dsl_cos(" + x + ")";
+                if (n.name == "sin") return "dsl_sin<EXACT>(" + x + ", big)";
+                if (n.name == "cos") return "dsl_cos<EXACT>(" + x + ", big)";
                 if (n.name == "tan") return "tan(" + x + ")";
                 if (n.name == "exp") return "exp(" + x + ")";
                 if (n.name == "ln") return "log(" + x + ")";
@@ -292,6 +293,7 @@ class Gen {
                 if (scope_.count(n.name) || n.name == "t" || n.name == "N" || n.name == "i")
                     throw GenError{"sum index '" + n.name + "' shadows a name in scope", n.line, n.col};
                 scope_.insert(n.name);
+                used_sum = true;
                 const std::string body = num(*n.a);
                 scope_.erase(n.name);
                 return "dsl_sum([&](int s_" + n.name + ") -> double { return " + body + "; })";
@@ -333,21 +335,25 @@ class Gen {
     std::set<std::string> scope_;
 };
 
-bool gen_function(const std::string& text, bool diffusion, std::string* out, std::string* err) {
+bool gen_function(const std::string& text, bool diffusion, std::string* out, std::string* err,
+                  bool* used_sum) {
     try {
         Parser ps(text);
         P root = ps.parse();
         Gen g(diffusion);
         const std::string body = g.num(*root);
+        *used_sum = *used_sum || g.used_sum;
         if (diffusion) {
-            *out = "__device__ __forceinline__ double sdeb::sdb_diffusion(int i, double t, "
-                   "const DVec& y, const double* __restrict__ p, const DVec& n) {\n"
-                   "    (void)i; (void)t; (void)y; (void)p; (void)n;\n"
+            *out = "template <bool EXACT>\n"
+                   "__device__ __forceinline__ double sdeb::sdb_diffusion(int i, double t, "
+                   "const DVec& y, const double* __restrict__ p, const DVec& n, bool& big) {\n"
+                   "    (void)i; (void)t; (void)y; (void)p; (void)n; (void)big;\n"
                    "    return " + body + ";\n}\n";
         } else {
-            *out = "__device__ __forceinline__ double sdeb::sdb_drift(int i, double t, "
-                   "const DVec& y, const double* __restrict__ p) {\n"
-                   "    (void)i; (void)t; (void)y; (void)p;\n    return " + body + ";\n}\n";
+            *out = "template <bool EXACT>\n"
+                   "__device__ __forceinline__ double sdeb::sdb_drift(int i, double t, "
+                   "const DVec& y, const double* __restrict__ p, bool& big) {\n"
+                   "    (void)i; (void)t; (void)y; (void)p; (void)big;\n    return " + body + ";\n}\n";
         }
         return true;
     } catch (const SyntaxError& e) {
@@ -384,31 +390,50 @@ int state_words(const sdb_model* m) {
     return m->nequat + (m->nnoise > 0 ? 4 * nb : 0);
 }
 
-// y + normals of 32 threads must fit the 96 KB shared-memory opt-in.
-bool global_state(const sdb_model* m) { return state_words(m) * 8 * 32 > kSmemMax; }
+int lanes_for(const sdb_model* m) {
+    if (const char* e = std::getenv("SDEB200_DSL_LANES")) {
+        const int v = std::atoi(e);
+        if (v >= 1 && v <= 32 && (v & (v - 1)) == 0) return v;
+    }
+    const int per_lane = m->uses_sum ? 4 : 16;
+    const int want = (m->nequat + per_lane - 1) / per_lane;
+    int l = 1;
+    while (l < want && l < 32) l <<= 1;
+    return l;
+}
 
-int threads_for(const sdb_model* m) {
-    const int fit = kSmemMax / (state_words(m) * 8);
-    return std::max(32, std::min(kBlock, fit / 32 * 32));
+// the columns of a CTA's 128 / lanes orbits must fit the 96 KB opt-in
+bool global_state(const sdb_model* m, int lanes) {
+    return size_t(state_words(m)) * 8 * size_t(kBlock / lanes) > size_t(kSmemMax);
+}
+
+size_t scratch_doubles(const sdb_model* m, int lanes, int64_t rows) {
+    if (!global_state(m, lanes)) return 0;
+    const int64_t slots = kBlock / lanes;
+    return size_t(state_words(m)) * size_t((rows + slots - 1) / slots * slots);
 }
 
 bool generate(sdb_model* m, std::string* err) {
-    return gen_function(m->drift_text, false, &m->drift_cu, err) &&
-           gen_function(m->diffusion_text, true, &m->diffusion_cu, err);
+    m->uses_sum = false;
+    return gen_function(m->drift_text, false, &m->drift_cu, err, &m->uses_sum) &&
+           gen_function(m->diffusion_text, true, &m->diffusion_cu, err, &m->uses_sum);
 }
 
-std::string program_source(const sdb_model* m, int kind) {
+std::string program_source(const sdb_model* m, int kind, int lanes) {
     // unrolled equation loops keep f / g / RK4 stages in registers; the
-    // unrolled model code grows as N x (drift evaluations per step), and ptxas
-    // time with it, so larger systems run the loops rolled (stack arrays)
+    // unrolled model code grows as (N / lanes) x (drift evaluations per
+    // step), and ptxas time with it, so larger systems run the loops rolled
+    // (stack arrays)
+    const int epl = (m->nequat + lanes - 1) / lanes;
     const int evals = (kind == sdeb::DK_RUN_RK4 || kind == sdeb::DK_STEP_RK4) ? 4
                       : (kind <= sdeb::DK_RUN_XOSHIRO || kind == sdeb::DK_STEP_EM) ? 2 : 1;
-    const int unroll = m->nequat * evals <= kUnrollWork ? m->nequat : 1;
-    char head[320];
+    const int unroll = epl * evals <= kUnrollWork ? epl : 1;
+    char head[360];
     std::snprintf(head, sizeof(head),
                   "#define SDB_N %d\n#define SDB_NP %d\n#define SDB_NN %d\n#define SDB_KIND %d\n"
-                  "#define SDB_UNROLL %d\n#define SDB_GLOBAL_STATE %d\n",
-                  m->nequat, m->nparams, m->nnoise, kind, unroll, global_state(m) ? 1 : 0);
+                  "#define SDB_LANES %d\n#define SDB_UNROLL %d\n#define SDB_GLOBAL_STATE %d\n",
+                  m->nequat, m->nparams, m->nnoise, kind, lanes, unroll,
+                  global_state(m, lanes) ? 1 : 0);
     return std::string("// generated by sdeb200 from expression templates\n") + head +
            "#include \"sdeb_dsl_kernel.cuh\"\n\n// drift: " + m->drift_text + "\n" + m->drift_cu +
            "\n// diffusion: " + m->diffusion_text + "\n" + m->diffusion_cu;
@@ -417,9 +442,9 @@ std::string program_source(const sdb_model* m, int kind) {
 namespace {
 
 // NVRTC: generated source -> sm_100a cubin.
-cudaError_t nvrtc_cubin(const sdb_model* m, int kind, std::vector<char>* cubin, std::string* log,
-                        std::string* err) {
-    const std::string src = program_source(m, kind);
+cudaError_t nvrtc_cubin(const sdb_model* m, int kind, int lanes, std::vector<char>* cubin,
+                        std::string* log, std::string* err) {
+    const std::string src = program_source(m, kind, lanes);
     nvrtcProgram prog;
     std::vector<const char*> names, texts;
     for (const RtcHeader& h : kRtcHeaders) {
@@ -452,9 +477,9 @@ cudaError_t nvrtc_cubin(const sdb_model* m, int kind, std::vector<char>* cubin, 
     return cudaSuccess;
 }
 
-cudaError_t compile(sdb_model* m, int kind, sdb_model::Program* out, std::string* err) {
+cudaError_t compile(sdb_model* m, int kind, int lanes, sdb_model::Program* out, std::string* err) {
     std::vector<char> cubin;
-    cudaError_t e = nvrtc_cubin(m, kind, &cubin, &out->log, err);
+    cudaError_t e = nvrtc_cubin(m, kind, lanes, &cubin, &out->log, err);
     if (e != cudaSuccess) return e;
     e = cudaLibraryLoadData(&out->lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
     if (e == cudaSuccess) e = cudaLibraryGetKernel(&out->kernel, out->lib, "sdb_dsl_main");
@@ -464,23 +489,24 @@ cudaError_t compile(sdb_model* m, int kind, sdb_model::Program* out, std::string
 
 }  // namespace
 
-cudaError_t compile_only(sdb_model* m, int kind, std::string* err) {
+cudaError_t compile_only(sdb_model* m, int kind, int lanes, std::string* err) {
     std::vector<char> cubin;
     std::string log;
-    cudaError_t e = nvrtc_cubin(m, kind, &cubin, &log, err);
+    cudaError_t e = nvrtc_cubin(m, kind, lanes, &cubin, &log, err);
     std::lock_guard<std::mutex> lock(m->mu);
     m->error = e == cudaSuccess ? log : *err;
     return e;
 }
 
-cudaError_t kernel_for(sdb_model* m, int kind, cudaKernel_t* out, std::string* err) {
+cudaError_t kernel_for(sdb_model* m, int kind, int lanes, cudaKernel_t* out, std::string* err) {
     std::lock_guard<std::mutex> lock(m->mu);
-    auto it = m->programs.find(kind);
+    const int key = kind + 64 * lanes;
+    auto it = m->programs.find(key);
     if (it == m->programs.end()) {
         sdb_model::Program prog;
-        cudaError_t e = compile(m, kind, &prog, err);
+        cudaError_t e = compile(m, kind, lanes, &prog, err);
         if (e != cudaSuccess) return e;
-        it = m->programs.emplace(kind, prog).first;
+        it = m->programs.emplace(key, prog).first;
     }
     *out = it->second.kernel;
     return cudaSuccess;
@@ -488,21 +514,20 @@ cudaError_t kernel_for(sdb_model* m, int kind, cudaKernel_t* out, std::string* e
 
 cudaError_t launch(sdb_model* m, int kind, const sdeb::DslArgs& a, cudaStream_t st,
                    std::string* err) {
+    const int lanes = lanes_for(m);
     cudaKernel_t k = nullptr;
-    cudaError_t e = kernel_for(m, kind, &k, err);
+    cudaError_t e = kernel_for(m, kind, lanes, &k, err);
     if (e != cudaSuccess) return e;
     if (a.rows <= 0) return cudaSuccess;
-    int threads = kBlock;
+    const int64_t slots = kBlock / lanes;
     size_t smem = 0;
-    sdeb::DslArgs copy = a;
-    if (global_state(m)) {
-        if (!copy.scratch) {
+    if (global_state(m, lanes)) {
+        if (!a.scratch) {
             *err = "expression-template program needs a global scratch buffer";
             return cudaErrorInvalidValue;
         }
     } else {
-        threads = threads_for(m);
-        smem = size_t(threads) * state_words(m) * sizeof(double);
+        smem = size_t(slots) * state_words(m) * sizeof(double);
         if (smem > 48 * 1024) {
             e = cudaFuncSetAttribute(reinterpret_cast<const void*>(k),
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
@@ -512,7 +537,8 @@ cudaError_t launch(sdb_model* m, int kind, const sdeb::DslArgs& a, cudaStream_t 
             }
         }
     }
-    const dim3 grid(unsigned((a.rows + threads - 1) / threads)), block(threads);
+    const dim3 grid(unsigned((a.rows + slots - 1) / slots)), block(kBlock);
+    sdeb::DslArgs copy = a;
     void* args[] = {&copy};
     e = cudaLaunchKernel(reinterpret_cast<const void*>(k), grid, block, args, smem, st);
     if (e != cudaSuccess) *err = std::string("expression-template kernel launch: ") + cudaGetErrorString(e);

@@ -22,13 +22,14 @@ struct sdb_model {
     std::string drift_text, diffusion_text;  // as given
     std::string drift_cu, diffusion_cu;      // generated device functions
     std::string error;                       // last compile / launch error
+    bool uses_sum = false;                   // O(N) work per equation (sets lanes_for)
     std::mutex mu;
     struct Program {
         cudaLibrary_t lib = nullptr;
         cudaKernel_t kernel = nullptr;
         std::string log;
     };
-    std::map<int, Program> programs;  // by sdeb::DslKind
+    std::map<int, Program> programs;  // by kind + 64 * lanes
     ~sdb_model();
 };
 
@@ -39,27 +40,32 @@ namespace sdeb_dsl {
 bool generate(sdb_model* m, std::string* err);
 
 // Full CUDA source of one program kind (for inspection / tests).
-std::string program_source(const sdb_model* m, int kind);
+std::string program_source(const sdb_model* m, int kind, int lanes);
 
 // NVRTC compile only (no device needed); the log lands in m->error.
-cudaError_t compile_only(sdb_model* m, int kind, std::string* err);
+cudaError_t compile_only(sdb_model* m, int kind, int lanes, std::string* err);
 
-// The compiled kernel of one kind (compiled on first use, thread-safe).
-cudaError_t kernel_for(sdb_model* m, int kind, cudaKernel_t* out, std::string* err);
+// The compiled kernel of one (kind, lanes) (compiled on first use, thread-safe).
+cudaError_t kernel_for(sdb_model* m, int kind, int lanes, cudaKernel_t* out, std::string* err);
 
-// Launch one program over `a.rows` rows (one thread per orbit).
+// Launch one program over `a.rows` orbits (lanes_for(m) threads each); the
+// caller provides a.scratch of scratch_doubles() when global_state().
 cudaError_t launch(sdb_model* m, int kind, const sdeb::DslArgs& a, cudaStream_t st,
                    std::string* err);
 
-constexpr int kBlock = 128;      // threads per CTA (fewer when the state columns need it)
+constexpr int kBlock = 128;      // threads per CTA = 128 / lanes orbit slots
 constexpr int kSmemMax = 96 * 1024;
-constexpr int kUnrollWork = 32;  // unroll equation loops while N x evaluations <= this
+constexpr int kUnrollWork = 32;  // unroll equation loops while (N / lanes) x evaluations <= this
 
-// Doubles per orbit in the strided state column: y + one step's normals.
+// Doubles per orbit in the shared column: y + one step's normals.
 int state_words(const sdb_model* m);
-// True when the columns go to global scratch ([words][rows]) instead of shared memory.
-bool global_state(const sdb_model* m);
-// CTA width of a shared-memory program.
-int threads_for(const sdb_model* m);
+// Lanes per orbit (power of two <= 32): ~4 equations per lane for templates
+// with sums (O(N) work per equation), ~16 without, or SDEB200_DSL_LANES.
+// Results do not depend on it.
+int lanes_for(const sdb_model* m);
+// True when the columns go to global scratch instead of shared memory.
+bool global_state(const sdb_model* m, int lanes);
+// Doubles of global scratch a launch over `rows` orbits needs (0 = none).
+size_t scratch_doubles(const sdb_model* m, int lanes, int64_t rows);
 
 }  // namespace sdeb_dsl

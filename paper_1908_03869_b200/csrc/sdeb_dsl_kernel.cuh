@@ -4,18 +4,18 @@
 //
 // sdeb_dsl.cu generates one translation unit per (model, kind):
 //
-//     #define SDB_N / SDB_NP / SDB_NN / SDB_KIND / SDB_UNROLL / SDB_GLOBAL_STATE
+//     #define SDB_N / SDB_NP / SDB_NN / SDB_KIND / SDB_LANES / SDB_UNROLL / SDB_GLOBAL_STATE
 //     #include "sdeb_dsl_kernel.cuh"
 //     __device__ double sdb_drift(int i, double t, const DVec& y, const double* p) {...}
 //     __device__ double sdb_diffusion(int i, double t, const DVec& y,
 //                                     const double* p, const DVec& n) {...}
 //
-// and NVRTC compiles it for sm_100a.  One thread integrates one orbit; N is a
-// compile-time constant.  The vector the templates index (y, and the step's
-// normals n) sits in a per-thread shared-memory column, since template
-// indices are runtime values (y[j] inside sum(j, .)); the per-equation
-// temporaries (f, g, RK4 stages) are indexed by the unrolled equation loop
-// only and live in registers for SDB_UNROLL = N.  Arithmetic is
+// and NVRTC compiles it for sm_100a.  A group of SDB_LANES threads integrates
+// one orbit (equations split across its lanes); N is a compile-time constant.
+// The vector the templates index (y, and the step's normals n) sits in a
+// per-orbit shared-memory column, since template indices are runtime values
+// (y[j] inside sum(j, .)); the per-equation temporaries (f, g, RK4 stages)
+// are indexed by the unrolled equation loop only and live in registers.  Arithmetic is
 // IEEE double with the reference's operation order (explicit _rn intrinsics,
 // --fmad=false), sum(j, .) uses numpy's pairwise order (Appendix B of
 // SURVEY.md), and the noise is the fused Philox / sfc64 / xoshiro256++ +
@@ -33,7 +33,7 @@ namespace sdeb {
 constexpr int kDslNB = (SDB_NN + 3) / 4 > 0 ? (SDB_NN + 3) / 4 : 1;  // 4-normal blocks
 constexpr int kDslNZ = SDB_NN > 0 ? 4 * kDslNB : 0;                   // normals per step
 constexpr double kDslN = double(SDB_N);
-constexpr int kDslUnroll = SDB_UNROLL;  // equation loops: N for small systems (registers), else 1
+constexpr int kDslUnroll = SDB_UNROLL;  // equation loops: unrolled for small systems, else 1
 
 // A per-thread vector with a stride: shared memory columns (stride = the CTA
 // width, conflict-free) or, for very large systems, a global scratch column
@@ -90,15 +90,30 @@ __device__ __noinline__ double2 dsl_sincos_big(double x) {
     return r;
 }
 
-__device__ __forceinline__ double dsl_sin(double x) {
-    if (big_arg(x)) return dsl_sincos_big(x).x;
+// sin / cos in the generated code.  The fast instantiation is branch- and
+// call-free (table sincos, valid for |x| < 2^29) and only flags a huge, inf
+// or NaN argument; a step that flagged anything is recomputed with EXACT =
+// true (libdevice's exact reduction for those arguments).  Keeping the call
+// out of the hot code keeps the coefficients in registers across the sums.
+template <bool EXACT>
+__device__ __forceinline__ double dsl_sin(double x, bool& big) {
+    if constexpr (EXACT) {
+        if (big_arg(x)) return dsl_sincos_big(x).x;
+    } else {
+        big |= big_arg(x);
+    }
     double s, c;
     sincos_small(x, s, c);
     return s;
 }
 
-__device__ __forceinline__ double dsl_cos(double x) {
-    if (big_arg(x)) return dsl_sincos_big(x).y;
+template <bool EXACT>
+__device__ __forceinline__ double dsl_cos(double x, bool& big) {
+    if constexpr (EXACT) {
+        if (big_arg(x)) return dsl_sincos_big(x).y;
+    } else {
+        big |= big_arg(x);
+    }
     double s, c;
     sincos_small(x, s, c);
     return c;
@@ -108,137 +123,284 @@ __device__ __forceinline__ double dsl_sq(double x) { return __dmul_rn(x, x); }
 
 // ---- the model (defined by the generated code after this header) ------------
 
+template <bool EXACT>
 __device__ __forceinline__ double sdb_drift(int i, double t, const DVec& y,
-                                           const double* __restrict__ p);
+                                           const double* __restrict__ p, bool& big);
+template <bool EXACT>
 __device__ __forceinline__ double sdb_diffusion(int i, double t, const DVec& y,
-                                               const double* __restrict__ p, const DVec& n);
+                                               const double* __restrict__ p, const DVec& n,
+                                               bool& big);
 
 __device__ __forceinline__ bool dsl_finite(double x) {
     return (__double2hiint(x) & 0x7ff00000) != 0x7ff00000;
 }
 
-__device__ __forceinline__ void dsl_drift_vec(double t, const DVec& y, const double* __restrict__ p,
-                                              double (&f)[SDB_N]) {
-#pragma unroll kDslUnroll
-    for (int i = 0; i < SDB_N; ++i) f[i] = sdb_drift(i, t, y, p);
+// ---- lane groups -------------------------------------------------------------
+// kL = SDB_LANES consecutive threads of a warp integrate one orbit; lane l owns
+// equations i = l, l + kL, l + 2 kL, ... (kEPL of them).  The vector the
+// templates index (y, the normals) is the orbit's shared column; every step
+// reads it in one phase and writes it in the next, separated by __syncwarp
+// (groups never straddle warps).  Each equation is evaluated exactly as with
+// one lane, so every kL gives bit-identical results.
+constexpr int kL = SDB_LANES;
+constexpr int kEPL = (SDB_N + kL - 1) / kL;   // equations per lane
+constexpr int kBPL = (kDslNB + kL - 1) / kL;  // 4-normal blocks per lane
+
+// Group barrier.  One lane per orbit shares nothing, so the fence (which
+// also makes the compiler re-load the parameters after it) is skipped.
+__device__ __forceinline__ void dsl_sync() {
+    if constexpr (kL > 1) __syncwarp();
 }
 
-// y <- (y + f*dt) + sqrt(dt) * g   (solvers.py:70-71)
-__device__ __forceinline__ void dsl_em(double t, double dt, double sqrt_dt, const DVec& y,
-                                       const double* __restrict__ p, const DVec& nz) {
-    double f[SDB_N], g[SDB_N];
-    dsl_drift_vec(t, y, p, f);
-#pragma unroll kDslUnroll
-    for (int i = 0; i < SDB_N; ++i) g[i] = sdb_diffusion(i, t, y, p, nz);
-#pragma unroll kDslUnroll
-    for (int i = 0; i < SDB_N; ++i)
-        y[i] = __dadd_rn(__dadd_rn(y[i], __dmul_rn(f[i], dt)), __dmul_rn(sqrt_dt, g[i]));
+// "Any lane of the warp flagged a huge argument" (warp-uniform at kL > 1;
+// at kL = 1 each orbit redoes only its own step).
+__device__ __forceinline__ bool dsl_any(bool flag) {
+    if constexpr (kL > 1) {
+        return __any_sync(0xffffffffu, flag);
+    } else {
+        return flag;
+    }
 }
 
-// y <- y + f*dt   (solvers.py:74-77)
-__device__ __forceinline__ void dsl_euler(double t, double dt, const DVec& y,
-                                          const double* __restrict__ p) {
-    double f[SDB_N];
-    dsl_drift_vec(t, y, p, f);
+template <bool EXACT>
+__device__ __forceinline__ void dsl_drift_vec(int lane, double t, const DVec& y,
+                                              const double* __restrict__ p, double (&f)[kEPL],
+                                              bool& big) {
 #pragma unroll kDslUnroll
-    for (int i = 0; i < SDB_N; ++i) y[i] = __dadd_rn(y[i], __dmul_rn(f[i], dt));
+    for (int q = 0; q < kEPL; ++q) {
+        const int i = lane + q * kL;
+        f[q] = (i < SDB_N) ? sdb_drift<EXACT>(i, t, y, p, big) : 0.0;
+    }
 }
 
-// classical RK4 in the reference's order (solvers.py:80-88):
-// y + (dt/6) * (((k1 + 2 k2) + 2 k3) + k4).  `y` is the vector the drift
-// reads (stage states are written into it); the state itself is kept in yk.
-__device__ __forceinline__ void dsl_rk4(double t, double dt, const DVec& y,
-                                        const double* __restrict__ p) {
+// one em step (solvers.py:70-71): ynew = (y + f*dt) + sqrt(dt) * g
+template <bool EXACT>
+__device__ __forceinline__ void dsl_em_pass(int lane, double t, double dt, double sqrt_dt,
+                                            const DVec& y, const double* __restrict__ p,
+                                            const DVec& nz, double (&ynew)[kEPL], bool& big) {
+    double f[kEPL];
+    dsl_drift_vec<EXACT>(lane, t, y, p, f, big);
+#pragma unroll kDslUnroll
+    for (int q = 0; q < kEPL; ++q) {
+        const int i = lane + q * kL;
+        if (i < SDB_N) {
+            const double g = sdb_diffusion<EXACT>(i, t, y, p, nz, big);
+            ynew[q] = __dadd_rn(__dadd_rn(y[i], __dmul_rn(f[q], dt)), __dmul_rn(sqrt_dt, g));
+        } else {
+            ynew[q] = 0.0;
+        }
+    }
+}
+
+__device__ __forceinline__ void dsl_em(int lane, double t, double dt, double sqrt_dt, const DVec& y,
+                                       const double* __restrict__ p, const DVec& nz,
+                                       double (&ynew)[kEPL]) {
+    bool big = false;
+    dsl_em_pass<false>(lane, t, dt, sqrt_dt, y, p, nz, ynew, big);
+    if (dsl_any(big)) dsl_em_pass<true>(lane, t, dt, sqrt_dt, y, p, nz, ynew, big);
+}
+
+// one euler step (solvers.py:74-77): ynew = y + f*dt
+template <bool EXACT>
+__device__ __forceinline__ void dsl_euler_pass(int lane, double t, double dt, const DVec& y,
+                                               const double* __restrict__ p, double (&ynew)[kEPL],
+                                               bool& big) {
+    double f[kEPL];
+    dsl_drift_vec<EXACT>(lane, t, y, p, f, big);
+#pragma unroll kDslUnroll
+    for (int q = 0; q < kEPL; ++q) {
+        const int i = lane + q * kL;
+        ynew[q] = (i < SDB_N) ? __dadd_rn(y[i], __dmul_rn(f[q], dt)) : 0.0;
+    }
+}
+
+__device__ __forceinline__ void dsl_euler(int lane, double t, double dt, const DVec& y,
+                                          const double* __restrict__ p, double (&ynew)[kEPL]) {
+    bool big = false;
+    dsl_euler_pass<false>(lane, t, dt, y, p, ynew, big);
+    if (dsl_any(big)) dsl_euler_pass<true>(lane, t, dt, y, p, ynew, big);
+}
+
+// one classical RK4 step in the reference's order (solvers.py:80-88):
+// y + (dt/6) * (((k1 + 2 k2) + 2 k3) + k4).  The stage states are written
+// into the shared column the drift reads; the step's start state is yk (this
+// lane's equations, registers) and ynew is returned uncommitted.
+template <bool EXACT>
+__device__ __forceinline__ void dsl_rk4_pass(int lane, double t, double dt, const DVec& y,
+                                             const double* __restrict__ p,
+                                             const double (&yk)[kEPL], double (&ynew)[kEPL],
+                                             bool& big) {
     const double half = __dmul_rn(0.5, dt);
     const double th = __dadd_rn(t, half);
-    double k[SDB_N], acc[SDB_N], yk[SDB_N];
+    double k[kEPL], acc[kEPL];
+    dsl_drift_vec<EXACT>(lane, t, y, p, k, big);
+    dsl_sync();
 #pragma unroll kDslUnroll
-    for (int i = 0; i < SDB_N; ++i) yk[i] = y[i];
-    dsl_drift_vec(t, y, p, k);
-#pragma unroll kDslUnroll
-    for (int i = 0; i < SDB_N; ++i) {
-        acc[i] = k[i];
-        y[i] = __dadd_rn(yk[i], __dmul_rn(half, k[i]));
+    for (int q = 0; q < kEPL; ++q) {
+        const int i = lane + q * kL;
+        acc[q] = k[q];
+        if (i < SDB_N) y[i] = __dadd_rn(yk[q], __dmul_rn(half, k[q]));
     }
-    dsl_drift_vec(th, y, p, k);
+    dsl_sync();
+    dsl_drift_vec<EXACT>(lane, th, y, p, k, big);
+    dsl_sync();
 #pragma unroll kDslUnroll
-    for (int i = 0; i < SDB_N; ++i) {
-        acc[i] = __dadd_rn(acc[i], __dmul_rn(2.0, k[i]));
-        y[i] = __dadd_rn(yk[i], __dmul_rn(half, k[i]));
+    for (int q = 0; q < kEPL; ++q) {
+        const int i = lane + q * kL;
+        acc[q] = __dadd_rn(acc[q], __dmul_rn(2.0, k[q]));
+        if (i < SDB_N) y[i] = __dadd_rn(yk[q], __dmul_rn(half, k[q]));
     }
-    dsl_drift_vec(th, y, p, k);
+    dsl_sync();
+    dsl_drift_vec<EXACT>(lane, th, y, p, k, big);
+    dsl_sync();
 #pragma unroll kDslUnroll
-    for (int i = 0; i < SDB_N; ++i) {
-        acc[i] = __dadd_rn(acc[i], __dmul_rn(2.0, k[i]));
-        y[i] = __dadd_rn(yk[i], __dmul_rn(dt, k[i]));
+    for (int q = 0; q < kEPL; ++q) {
+        const int i = lane + q * kL;
+        acc[q] = __dadd_rn(acc[q], __dmul_rn(2.0, k[q]));
+        if (i < SDB_N) y[i] = __dadd_rn(yk[q], __dmul_rn(dt, k[q]));
     }
-    dsl_drift_vec(__dadd_rn(t, dt), y, p, k);
+    dsl_sync();
+    dsl_drift_vec<EXACT>(lane, __dadd_rn(t, dt), y, p, k, big);
     const double dt6 = __ddiv_rn(dt, 6.0);
 #pragma unroll kDslUnroll
-    for (int i = 0; i < SDB_N; ++i) {
-        acc[i] = __dadd_rn(acc[i], k[i]);
-        y[i] = __dadd_rn(yk[i], __dmul_rn(dt6, acc[i]));
+    for (int q = 0; q < kEPL; ++q) {
+        acc[q] = __dadd_rn(acc[q], k[q]);
+        ynew[q] = __dadd_rn(yk[q], __dmul_rn(dt6, acc[q]));
     }
+}
+
+__device__ __forceinline__ void dsl_rk4(int lane, double t, double dt, const DVec& y,
+                                        const double* __restrict__ p, double (&ynew)[kEPL]) {
+    double yk[kEPL];
+#pragma unroll kDslUnroll
+    for (int q = 0; q < kEPL; ++q) {
+        const int i = lane + q * kL;
+        yk[q] = (i < SDB_N) ? y[i] : 0.0;
+    }
+    bool big = false;
+    dsl_rk4_pass<false>(lane, t, dt, y, p, yk, ynew, big);
+    if (dsl_any(big)) {
+        dsl_sync();  // every lane is past its last stage read
+#pragma unroll kDslUnroll
+        for (int q = 0; q < kEPL; ++q) {
+            const int i = lane + q * kL;
+            if (i < SDB_N) y[i] = yk[q];
+        }
+        dsl_sync();
+        dsl_rk4_pass<true>(lane, t, dt, y, p, yk, ynew, big);
+    }
+}
+
+// Write the step's result into the shared column after every lane finished
+// reading it.  check: isfinite(y).all(-1) over the orbit (OR across the
+// group); a failing orbit records its first step and becomes NaN
+// (engine.py:244-261).
+__device__ __forceinline__ void dsl_commit(int lane, const DVec& y, double (&ynew)[kEPL], bool check,
+                                           int64_t& fail, uint64_t step) {
+    dsl_sync();
+    if (check) {
+        bool bad = false;
+#pragma unroll
+        for (int q = 0; q < kEPL; ++q) {
+            const int i = lane + q * kL;
+            bad |= (i < SDB_N) && !dsl_finite(ynew[q]);
+        }
+#pragma unroll
+        for (int o = 1; o < kL; o <<= 1) bad |= __shfl_xor_sync(0xffffffffu, int(bad), o) != 0;
+        if (bad) {
+            if (fail < 0) fail = int64_t(step);
+#pragma unroll
+            for (int q = 0; q < kEPL; ++q) ynew[q] = __longlong_as_double(0x7ff8000000000000ll);
+        }
+    }
+#pragma unroll kDslUnroll
+    for (int q = 0; q < kEPL; ++q) {
+        const int i = lane + q * kL;
+        if (i < SDB_N) y[i] = ynew[q];
+    }
+    dsl_sync();
 }
 
 }  // namespace sdeb
 
 // ---- the kernel ------------------------------------------------------------------
-// Per thread: the state vector y and the step's normals live in a strided
-// column (DVec) -- dynamic shared memory of blockDim.x * (N + NZ) doubles, or
-// (SDB_GLOBAL_STATE) the global scratch [N + NZ][rows].
+// CTA = 128 threads = 128/kL orbit slots.  The per-orbit columns (y, the
+// step's normals) live in dynamic shared memory, [words][slots] per CTA, or
+// (SDB_GLOBAL_STATE) in the global scratch [words][grid * slots].  Tail
+// threads past the last orbit mirror it into their own column and write
+// nothing, so every warp runs the same sequence of __syncwarp.
 
 extern "C" __global__ void __launch_bounds__(128) sdb_dsl_main(const sdeb::DslArgs a) {
     using namespace sdeb;
     extern __shared__ double dsl_smem[];
-    const int64_t row = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (row >= a.rows) return;
+    constexpr int kSlots = 128 / kL;
+    const int lane = int(threadIdx.x) % kL;
+    const int slot = int(threadIdx.x) / kL;
+    const int64_t orbit = int64_t(blockIdx.x) * kSlots + slot;
+    const bool active = orbit < a.rows;
+    const int64_t row = active ? orbit : a.rows - 1;
 #if SDB_GLOBAL_STATE
-    const DVec y{a.scratch + row, a.rows};
-    const DVec nz{a.scratch + int64_t(SDB_N) * a.rows + row, a.rows};
+    const int64_t cols = int64_t(gridDim.x) * kSlots;
+    const DVec y{a.scratch + int64_t(blockIdx.x) * kSlots + slot, cols};
+    const DVec nz{a.scratch + int64_t(SDB_N) * cols + int64_t(blockIdx.x) * kSlots + slot, cols};
 #else
-    const DVec y{dsl_smem + threadIdx.x, int64_t(blockDim.x)};
-    const DVec nz{dsl_smem + int64_t(SDB_N) * blockDim.x + threadIdx.x, int64_t(blockDim.x)};
+    const DVec y{dsl_smem + slot, int64_t(kSlots)};
+    const DVec nz{dsl_smem + int64_t(SDB_N) * kSlots + slot, int64_t(kSlots)};
 #endif
     const double* __restrict__ p = a.params + row * SDB_NP;
 #pragma unroll kDslUnroll
-    for (int i = 0; i < SDB_N; ++i) y[i] = a.state_in[row * SDB_N + i];
+    for (int q = 0; q < kEPL; ++q) {
+        const int i = lane + q * kL;
+        if (i < SDB_N) y[i] = a.state_in[row * SDB_N + i];
+    }
 #if SDB_NN > 0
     if (a.noise != nullptr) {
 #pragma unroll 1
-        for (int k = 0; k < SDB_NN; ++k) nz[k] = a.noise[row * SDB_NN + k];
+        for (int k = lane; k < SDB_NN; k += kL) nz[k] = a.noise[row * SDB_NN + k];
     }
 #endif
+    dsl_sync();
 
 #if SDB_KIND == 8 || SDB_KIND == 9  // drift_eval / diffusion_eval
+    bool big = false;  // evaluation is not a hot loop: always the exact form
 #pragma unroll kDslUnroll
-    for (int i = 0; i < SDB_N; ++i)
-        a.values[row * SDB_N + i] = SDB_KIND == 8 ? sdb_drift(i, a.t, y, p)
-                                                  : sdb_diffusion(i, a.t, y, p, nz);
+    for (int q = 0; q < kEPL; ++q) {
+        const int i = lane + q * kL;
+        if (i < SDB_N && active)
+            a.values[row * SDB_N + i] = SDB_KIND == 8 ? sdb_drift<true>(i, a.t, y, p, big)
+                                                      : sdb_diffusion<true>(i, a.t, y, p, nz, big);
+    }
 #elif SDB_KIND >= 5  // one caller-driven step
+    double ynew[kEPL];
 #if SDB_KIND == 5
-    dsl_em(a.t, a.dt, a.sqrt_dt, y, p, nz);
+    dsl_em(lane, a.t, a.dt, a.sqrt_dt, y, p, nz, ynew);
 #elif SDB_KIND == 6
-    dsl_euler(a.t, a.dt, y, p);
+    dsl_euler(lane, a.t, a.dt, y, p, ynew);
 #else
-    dsl_rk4(a.t, a.dt, y, p);
+    dsl_rk4(lane, a.t, a.dt, y, p, ynew);
 #endif
 #pragma unroll kDslUnroll
-    for (int i = 0; i < SDB_N; ++i) a.state_out[row * SDB_N + i] = y[i];
+    for (int q = 0; q < kEPL; ++q) {
+        const int i = lane + q * kL;
+        if (i < SDB_N && active) a.state_out[row * SDB_N + i] = ynew[q];
+    }
 #else  // run_batch's chunk x step loop (engine.py:231-262)
     constexpr bool kStateful = SDB_KIND == 1 || SDB_KIND == 2;
     const uint32_t orbit_g = uint32_t(a.orbit_offset + row);
     const bool fresh = a.fresh != 0;
     int64_t fail = (fresh || a.fail_step == nullptr) ? -1 : a.fail_step[row];
-    StreamState rs[kDslNB];
+    StreamState rs[kBPL];  // block b = lane + r*kL
     if constexpr (kStateful) {
 #pragma unroll
-        for (int b = 0; b < kDslNB; ++b) {
-            if (fresh) {
-                rs[b] = stream_init<SDB_KIND>(a.seed, uint64_t(orbit_g), uint64_t(b));
+        for (int r = 0; r < kBPL; ++r) {
+            const int b = lane + r * kL;
+            if (b >= kDslNB) {
+                rs[r] = StreamState{0, 0, 0, 0};
+            } else if (fresh) {
+                rs[r] = stream_init<SDB_KIND>(a.seed, uint64_t(orbit_g), uint64_t(b));
             } else {
                 const uint64_t* q = a.rng_state + (row * kDslNB + b) * 4;
-                rs[b] = StreamState{q[0], q[1], q[2], q[3]};
+                rs[r] = StreamState{q[0], q[1], q[2], q[3]};
             }
         }
     }
@@ -247,62 +409,71 @@ extern "C" __global__ void __launch_bounds__(128) sdb_dsl_main(const sdeb::DslAr
     (void)seed_hi;
     const uint64_t ks = uint64_t(a.ksteps);
     uint64_t step = uint64_t(a.chunk_begin) * ks;
+    double ynew[kEPL];
 #pragma unroll 1
     for (int64_t c = a.chunk_begin; c < a.chunk_end; ++c) {
 #pragma unroll 1
         for (uint64_t l = 0; l < ks; ++l, ++step) {
             const double t = __dmul_rn(double(step), a.dt);  // t = step_index * dt
 #if SDB_KIND <= 2
+            // the step's normals: this lane's 4-normal blocks into the column
 #pragma unroll
-            for (int b = 0; b < kDslNB; ++b) {
-                Words4 w;
-                if constexpr (SDB_KIND == 0) {
-                    w = philox4x32_10(seed_hi, uint32_t(step >> 32), uint32_t(step), uint32_t(b),
-                                      seed_lo, orbit_g);
-                } else {
-                    w = stream_block<SDB_KIND>(rs[b]);
+            for (int r = 0; r < kBPL; ++r) {
+                const int b = lane + r * kL;
+                if (b < kDslNB) {
+                    Words4 w;
+                    if constexpr (SDB_KIND == 0) {
+                        w = philox4x32_10(seed_hi, uint32_t(step >> 32), uint32_t(step),
+                                          uint32_t(b), seed_lo, orbit_g);
+                    } else {
+                        w = stream_block<SDB_KIND>(rs[r]);
+                    }
+                    double z0, z1, z2, z3;
+                    box_muller_pair(w.w0, w.w1, z0, z1);
+                    box_muller_pair(w.w2, w.w3, z2, z3);
+                    nz[4 * b] = z0;
+                    nz[4 * b + 1] = z1;
+                    nz[4 * b + 2] = z2;
+                    nz[4 * b + 3] = z3;
                 }
-                double z0, z1, z2, z3;
-                box_muller_pair(w.w0, w.w1, z0, z1);
-                box_muller_pair(w.w2, w.w3, z2, z3);
-                nz[4 * b] = z0;
-                nz[4 * b + 1] = z1;
-                nz[4 * b + 2] = z2;
-                nz[4 * b + 3] = z3;
             }
-            dsl_em(t, a.dt, a.sqrt_dt, y, p, nz);
+            dsl_sync();
+            dsl_em(lane, t, a.dt, a.sqrt_dt, y, p, nz, ynew);
 #elif SDB_KIND == 3
-            dsl_euler(t, a.dt, y, p);
+            dsl_euler(lane, t, a.dt, y, p, ynew);
 #else
-            dsl_rk4(t, a.dt, y, p);
+            dsl_rk4(lane, t, a.dt, y, p, ynew);
 #endif
-            // isfinite(y).all(-1); first failure recorded, row -> NaN (engine.py:244-261)
-            bool bad = false;
+            dsl_commit(lane, y, ynew, true, fail, step);
+        }
+        if (active) {
+            double* out = a.values + (row * a.vstride + (c - a.chunk_begin)) * SDB_N;
 #pragma unroll kDslUnroll
-            for (int i = 0; i < SDB_N; ++i) bad |= !dsl_finite(y[i]);
-            if (bad) {
-                if (fail < 0) fail = int64_t(step);
-#pragma unroll kDslUnroll
-                for (int i = 0; i < SDB_N; ++i) y[i] = __longlong_as_double(0x7ff8000000000000ll);
+            for (int q = 0; q < kEPL; ++q) {
+                const int i = lane + q * kL;
+                if (i < SDB_N) out[i] = y[i];
             }
         }
-        double* out = a.values + (row * a.vstride + (c - a.chunk_begin)) * SDB_N;
-#pragma unroll kDslUnroll
-        for (int i = 0; i < SDB_N; ++i) out[i] = y[i];
     }
-    if (a.state_out != nullptr) {
+    if (active) {
 #pragma unroll kDslUnroll
-        for (int i = 0; i < SDB_N; ++i) a.state_out[row * SDB_N + i] = y[i];
-    }
-    if (a.fail_step != nullptr) a.fail_step[row] = fail;
-    if constexpr (kStateful) {
+        for (int q = 0; q < kEPL; ++q) {
+            const int i = lane + q * kL;
+            if (i < SDB_N && a.state_out != nullptr) a.state_out[row * SDB_N + i] = y[i];
+        }
+        if (a.fail_step != nullptr && lane == 0) a.fail_step[row] = fail;
+        if constexpr (kStateful) {
 #pragma unroll
-        for (int b = 0; b < kDslNB; ++b) {
-            uint64_t* q = a.rng_state + (row * kDslNB + b) * 4;
-            q[0] = rs[b].s0;
-            q[1] = rs[b].s1;
-            q[2] = rs[b].s2;
-            q[3] = rs[b].s3;
+            for (int r = 0; r < kBPL; ++r) {
+                const int b = lane + r * kL;
+                if (b < kDslNB) {
+                    uint64_t* q = a.rng_state + (row * kDslNB + b) * 4;
+                    q[0] = rs[r].s0;
+                    q[1] = rs[r].s1;
+                    q[2] = rs[r].s2;
+                    q[3] = rs[r].s3;
+                }
+            }
         }
     }
 #endif

@@ -163,7 +163,7 @@ def test_generated_code_follows_the_templates():
                           dsl.parse(KURAMOTO_DIFFUSION_TEMPLATE))
     src = cm.source(0)
     assert "#define SDB_N 4" in src and "#define SDB_KIND 0" in src
-    assert "dsl_sum(" in src and "dsl_sin(__dsub_rn(y[s_j], y[i]))" in src
+    assert "dsl_sum(" in src and "dsl_sin<EXACT>(__dsub_rn(y[s_j], y[i]), big)" in src
     assert "__ddiv_rn(p[0], kDslN)" in src
     assert "__dmul_rn(p[((1 + SDB_N) + i)], n[i])" in src
 
@@ -189,9 +189,19 @@ def test_programs_compile_with_nvrtc(kind):
     cm.build(kind)
 
 
-def test_large_system_uses_global_state_columns():
-    cm = program.compiled(400, 1, 400, dsl.parse("p[0] - y[i]"), dsl.parse("n[i]"))
-    cm.build(0)
-    assert "#define SDB_GLOBAL_STATE 1" in cm.source(0)
-    small = program.compiled(40, 1, 40, dsl.parse("p[0] - y[i]"), dsl.parse("n[i]"))
-    assert "#define SDB_GLOBAL_STATE 0" in small.source(0)
+def test_lane_groups_and_state_placement(monkeypatch):
+    small = program.compiled(3, 1, 3, dsl.parse("p[0] - y[i]"), dsl.parse("n[i]"))
+    assert "#define SDB_LANES 1" in small.source(0)
+    mid = program.compiled(16, 1, 16, dsl.parse("p[0] - y[i]"), dsl.parse("n[i]"))
+    assert "#define SDB_LANES 1" in mid.source(0)  # O(1) per equation: one lane
+    mid_sum = program.compiled(16, 1, 16, dsl.parse("p[0] - sum(j, y[j])"), dsl.parse("n[i]"))
+    assert "#define SDB_LANES 4" in mid_sum.source(0)  # O(N) per equation: ~4 per lane
+    big = program.compiled(400, 1, 400, dsl.parse("p[0] - sum(j, y[j] - y[i])"),
+                           dsl.parse("n[i]"))
+    src = big.source(0)
+    assert "#define SDB_LANES 32" in src and "#define SDB_GLOBAL_STATE 0" in src
+    # one lane per orbit: 128 columns of 800 doubles exceed shared memory
+    monkeypatch.setenv("SDEB200_DSL_LANES", "1")
+    src = big.source(0)
+    assert "#define SDB_LANES 1" in src and "#define SDB_GLOBAL_STATE 1" in src
+    big.build(0)

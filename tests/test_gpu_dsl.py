@@ -239,3 +239,42 @@ def test_model_file_runs(tmp_path):
     _, want, _ = O.integrate(batch.init, batch.params, dt=0.01, ksteps=10, chunks=10, seed=4,
                              nnoise=2, drift=drift, diffusion=diffusion)
     assert O.mixed_error(store.values, want) <= PARITY_TOL
+
+
+@pytest.mark.parametrize("name", ["tdep", "nested", "rk4", "fail", "big"])
+def test_lane_groups_bit_identical(golden_dsl, name, monkeypatch):
+    # 1..32 lanes per orbit (and the global-scratch columns at 1 lane for
+    # "big") give the same bits: each equation is evaluated identically
+    arrays, cases = golden_dsl
+    case = cases[name]
+    model = case_model(case, name)
+    hashes = set()
+    for lanes in (1, 2, 4, 8, 16, 32):
+        monkeypatch.setenv("SDEB200_DSL_LANES", str(lanes))
+        store = run_batch(model, case_cfg(case, stream="sfc64" if case["nnoise"] else "philox"),
+                          case_batch(arrays, name))
+        assert last_launch_info()["lanes"] == lanes
+        hashes.add(sdb.store_hash(store))
+    assert len(hashes) == 1
+
+
+def test_global_state_columns_match_shared(monkeypatch):
+    # 120 equations at one lane per orbit: the columns do not fit shared
+    # memory and live in global scratch
+    n = 120
+    model = sdb.model_from_dsl("wide", n, 2, n, "p[0]*sum(j, sin(y[j] - y[i]))/N - p[1]*y[i]",
+                               "0.1*n[i]")
+    g = np.random.default_rng(2)
+    m = 50
+    batch = OrbitBatch(init=g.uniform(-2, 2, (m, n)), params=g.uniform(0.1, 0.9, (m, 2)))
+    cfg = EngineConfig(dt=0.01, tspan=0.2, ksteps=5, orbits=m, seed=3)
+    monkeypatch.setenv("SDEB200_DSL_LANES", "1")
+    a = run_batch(model, cfg, batch)
+    monkeypatch.setenv("SDEB200_DSL_LANES", "32")
+    b = run_batch(model, cfg, batch)
+    assert sdb.store_hash(a) == sdb.store_hash(b)
+    drift, diffusion = O.expression_model("p[0]*sum(j, sin(y[j] - y[i]))/N - p[1]*y[i]",
+                                          "0.1*n[i]")
+    _, want, _ = O.integrate(batch.init, batch.params, dt=0.01, ksteps=5, chunks=4, seed=3,
+                             nnoise=n, drift=drift, diffusion=diffusion)
+    assert O.mixed_error(a.values, want) <= PARITY_TOL
