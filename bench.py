@@ -64,6 +64,12 @@ WORKLOADS = {
     "cfg5": dict(n=32, orbits=131072, dt=1e-3, steps=1000, ksteps=10, stream="philox",
                  solver="em", batch="resample",
                  desc="n=32, 512 parameter sets x 256 realisations, trajectory every 10 steps"),
+    # run_batch fused with coherence_series: only (r, Phi) per sample leaves
+    # the GPU; the e2e line includes the D2H of that instead of the 3.2 GiB store
+    "cfg5_coherence": dict(n=32, orbits=131072, dt=1e-3, steps=1000, ksteps=10, stream="philox",
+                           solver="em", batch="resample", coherence=True,
+                           desc="cfg5 through analysis.run_coherence: order parameter of every "
+                                "10th step fused into the stepper"),
     # expression-template models through the NVRTC-generated program
     "cfg2_codegen": dict(n=16, orbits=65536, dt=1e-3, steps=10000, ksteps=10000, stream="sfc64",
                          solver="em", batch="kgrid", model="kuramoto_template",
@@ -375,7 +381,9 @@ def run_ours(args, w, world, rank, local, dist):
 
     d_init = torch.from_numpy(np.ascontiguousarray(batch.init)).cuda()
     d_params = torch.from_numpy(np.ascontiguousarray(batch.params)).cuda()
-    d_values = torch.empty((m, chunks, n), dtype=torch.float64, device="cuda")
+    coherence = bool(w.get("coherence"))
+    d_values = (torch.empty((m, 2, chunks + 1), dtype=torch.float64, device="cuda") if coherence
+                else torch.empty((m, chunks, n), dtype=torch.float64, device="cuda"))
     d_fail = torch.empty(m, dtype=torch.int64, device="cuda")
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
     stream = torch.cuda.current_stream()
@@ -386,6 +394,12 @@ def run_ours(args, w, world, rank, local, dist):
         program_handle = program.model_program(model).handle
 
     def launch():
+        if coherence:
+            nat.check(lib.sdb_run_coherence_device(ctx, desc, d_init.data_ptr(),
+                                                   d_params.data_ptr(), d_values.data_ptr(),
+                                                   d_fail.data_ptr(), stream.cuda_stream),
+                      ctx, "sdb_run_coherence_device")
+            return
         if program_handle is not None:
             nat.check(lib.sdb_run_model_device(ctx, program_handle, desc, d_init.data_ptr(),
                                                d_params.data_ptr(), d_values.data_ptr(),
@@ -431,18 +445,20 @@ def run_ours(args, w, world, rank, local, dist):
 
     # --- e2e through the public API (host numpy buffers) ---
     host_batch = sdb.OrbitBatch(init=batch.init.copy(), params=batch.params.copy())
-    sdb.run_batch(model, cfg, host_batch, orbit_offset=offset)  # warm (autotune cache, pageable staging)
+    api = sdb.run_coherence if coherence else sdb.run_batch
+    api(model, cfg, host_batch, orbit_offset=offset)  # warm (autotune cache, pinned staging)
     barrier(dist)
     t0 = time.perf_counter()
     e2e_steps = max(1, min(args.steps, 5))
     for _ in range(e2e_steps):
-        store = sdb.run_batch(model, cfg, host_batch, orbit_offset=offset)
+        store = api(model, cfg, host_batch, orbit_offset=offset)
     e2e_s = reduce_max(dist, time.perf_counter() - t0) / e2e_steps
     h2d = batch.init.nbytes + batch.params.nbytes
-    d2h = m * chunks * n * 8 + m * 8
+    d2h = (m * (chunks + 1) * 2 * 8 if coherence else m * chunks * n * 8) + m * 8
     e2e = {"value": world * orbit_steps / e2e_s, "unit": "orbit-steps/s",
            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-           "ms_per_step": e2e_s * 1e3, "host_buffers": "pageable numpy (run_batch)"}
+           "ms_per_step": e2e_s * 1e3,
+           "host_buffers": "pageable numpy (%s)" % api.__name__}
     del store
 
     # --- roofline (FP64 pipe) ---

@@ -166,6 +166,27 @@ sdb_status sdb_fp64_peak(sdb_ctx* ctx, double* ops_per_s, double* ms);
 sdb_status sdb_math_probe(sdb_ctx* ctx, int32_t func, const double* x, int64_t count,
                           double* out);
 
+/* ---- analysis (analysis.py:72-186) -------------------------------------------- */
+
+/* run_batch fused with coherence_series (analysis.py:98-101): the Kuramoto
+ * integration of sdb_run, but each sample is the orbit's order parameter
+ * r e^{i Phi} = mean_j e^{i theta_j} computed in the kernel (r = min(|z|, 1),
+ * Phi = wrap_phase(arg z), Phi = 0 at r = 0; analysis.py:77-82) -- the phases
+ * never leave the GPU.  r_phi: [orbits][2][chunks+1] (per orbit the r series then
+ * the Phi series), sample 0 = the initial state's.  fail_step as sdb_run;
+ * failed orbits give NaN. */
+sdb_status sdb_run_coherence(sdb_ctx* ctx, const sdb_desc* desc, const double* init,
+                             const double* params, double* r_phi, int64_t* fail_step);
+/* The same on device buffers (first device, asynchronous on `stream`). */
+sdb_status sdb_run_coherence_device(sdb_ctx* ctx, const sdb_desc* desc, const double* d_init,
+                                    const double* d_params, double* d_r_phi, int64_t* d_fail_step,
+                                    void* stream);
+/* Order parameter of `rows` populations of n phases each (phases [rows][n]),
+ * e.g. a stored trajectory viewed as [orbits * samples][n]
+ * (_order_parameter_arrays, analysis.py:77-82). */
+sdb_status sdb_order_parameter(sdb_ctx* ctx, int32_t n, int64_t rows, const double* phases,
+                               double* r, double* phi);
+
 /* ---- expression-template models (dsl.py / model.py:291-323) -----------------
  *
  * The reference evaluates a model's drift and diffusion templates with a numpy

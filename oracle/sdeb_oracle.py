@@ -506,6 +506,28 @@ def expression_model(drift_text, diffusion_text=None):
     return drift, diffusion
 
 
+# ---------------------------------------------------------------------------
+# Analysis (analysis.py:72-186)
+
+def wrap_phase(x):
+    """analysis.py:72-74: onto [-pi, pi)."""
+    return np.mod(np.asarray(x, dtype=np.float64) + math.pi, 2.0 * math.pi) - math.pi
+
+
+def order_parameter_arrays(phases):
+    """analysis.py:77-82: r = min(|mean(e^{i theta})|, 1), Phi wrapped, Phi = 0 at r = 0."""
+    z = np.exp(1j * np.asarray(phases, dtype=np.float64)).mean(axis=-1)
+    r = np.minimum(np.abs(z), 1.0)
+    phi = wrap_phase(np.arctan2(z.imag, z.real))
+    return r, np.where(r == 0.0, 0.0, phi)
+
+
+def ensemble_mean_std(r):
+    """analysis.py:126-130: per-time mean and population std over realizations."""
+    r = np.asarray(r, dtype=np.float64)
+    return r.mean(axis=0), r.std(axis=0)
+
+
 def mixed_error(got, ref):
     """max |got - ref| / max(1, |ref|) -- the parity metric (north_star 1e-10).
     NaNs must coincide; returns inf otherwise."""

@@ -17,7 +17,10 @@ from .engine import (EngineConfig, TrajectoryStore, OrbitFailure, ConfigError, r
 from .solvers import (euler_maruyama_step, euler_step, rk4_step, implicit_euler_step,
                       implicit_midpoint_step, get_solver, SOLVERS)
 from .storage import store_hash
-from . import dsl, rng
+from .analysis import (CoherencePoint, CoherenceSeries, EnsembleStats, order_parameter,
+                       coherence_series, ensemble_stats, dt_sweep, kymograph_export, wrap_phase,
+                       run_coherence)
+from . import analysis, dsl, rng
 
 __all__ = [
     "__version__",
@@ -28,5 +31,7 @@ __all__ = [
     "iteration_count", "partition_orbits",
     "euler_maruyama_step", "euler_step", "rk4_step",
     "implicit_euler_step", "implicit_midpoint_step", "get_solver", "SOLVERS",
-    "store_hash", "dsl", "rng",
+    "store_hash", "dsl", "rng", "analysis",
+    "CoherencePoint", "CoherenceSeries", "EnsembleStats", "order_parameter", "coherence_series",
+    "ensemble_stats", "dt_sweep", "kymograph_export", "wrap_phase", "run_coherence",
 ]

@@ -556,10 +556,18 @@ sdb_status launch_model(sdb_ctx* ctx, Slot& s, const sdb_desc& d, sdb_model* m,
     return SDB_OK;
 }
 
+// out_mode 0: samples of the state, d_values [orbits][chunks][n]; 1 (Kuramoto
+// only): the order parameter, d_values [orbits][2][chunks + 1] (r, Phi planes)
+// with sample 0.
 sdb_status launch_device(sdb_ctx* ctx, Slot& s, const sdb_desc& d, sdb_model* m,
                          const double* d_init, const double* d_params, double* d_values,
-                         int64_t* d_fail, cudaStream_t st) {
-    if (m) return launch_model(ctx, s, d, m, d_init, d_params, d_values, d_fail, st);
+                         int64_t* d_fail, cudaStream_t st, int out_mode = 0) {
+    if (m) {
+        if (out_mode != 0)
+            return fail_with(ctx, SDB_ERR_UNSUPPORTED,
+                             "fused order parameter is implemented for the Kuramoto stepper");
+        return launch_model(ctx, s, d, m, d_init, d_params, d_values, d_fail, st);
+    }
     Layout lay;
     sdb_status rc = choose_layout(ctx, s, d, d_init, d_params, st, &lay);
     if (rc != SDB_OK) return rc;
@@ -578,8 +586,12 @@ sdb_status launch_device(sdb_ctx* ctx, Slot& s, const sdb_desc& d, sdb_model* m,
     rc = configure_layout(ctx, s, s.work, d, lay, d.chunks * d.ksteps, st, &a);
     if (rc != SDB_OK) return rc;
     const int P = next_pow2(d.nequat);
-    cudaError_t e = launch_run(a, P / lay.lanes, kind_solver, kind_stream, d.coupling,
-                               kernel_variant(d, lay.tight), st);
+    int variant = kernel_variant(d, out_mode ? 0 : lay.tight);
+    if (out_mode) {
+        variant += sdeb::kVarCoherence;  // same layout, order-parameter samples
+        a.vstride = d.chunks + 1;
+    }
+    cudaError_t e = launch_run(a, P / lay.lanes, kind_solver, kind_stream, d.coupling, variant, st);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "kuramoto_run_kernel launch");
     s.launches += 1;
     s.lanes = lay.lanes;
@@ -664,7 +676,7 @@ int64_t shard_tiles(const sdb_desc& d, int64_t rows, int device) {
 // noise is keyed by global orbit id and orbits are independent.
 sdb_status run_shard(sdb_ctx* ctx, Slot& s, sdb_desc d, sdb_model* m, int64_t r0, int64_t rows,
                      const double* init, const double* params, double* values, int64_t* fail,
-                     int shards) {
+                     int shards, int out_mode) {
     SDB_CUDA(ctx, cudaSetDevice(s.device));
     const bool tr = trace_enabled();
     const double t0 = tr ? now_ms() : 0.0;
@@ -676,14 +688,16 @@ sdb_status run_shard(sdb_ctx* ctx, Slot& s, sdb_desc d, sdb_model* m, int64_t r0
     d.orbits = rows;
     SDB_CUDA(ctx, s.init.ensure(size_t(rows) * n * sizeof(double)));
     SDB_CUDA(ctx, s.params.ensure(size_t(rows) * np_ * sizeof(double)));
-    SDB_CUDA(ctx, s.values.ensure(size_t(rows) * k * n * sizeof(double)));
+    // device words per row: samples 1..k of the state, or (r, Phi) of samples 0..k
+    const int64_t width = out_mode ? (k + 1) * 2 : k * n;
+    SDB_CUDA(ctx, s.values.ensure(size_t(rows) * width * sizeof(double)));
     SDB_CUDA(ctx, s.fail.ensure(size_t(rows) * sizeof(int64_t)));
     if (!s.ev_in) SDB_CUDA(ctx, cudaEventCreateWithFlags(&s.ev_in, cudaEventDisableTiming));
 
     const int64_t tiles = shard_tiles(d, rows, s.device);
     const size_t piece_cap = size_t(std::max(1, env_int("SDEB200_PIECE_KB", 65536))) << 10;
     const size_t in_row = size_t(n + np_) * sizeof(double);
-    const size_t out_row = size_t(k * n + 1) * sizeof(double);  // samples + fail word
+    const size_t out_row = size_t(width + 1) * sizeof(double);  // samples + fail word
     const int64_t in_piece = std::max<int64_t>(1, int64_t(piece_cap / in_row));
     const int64_t out_piece = std::max<int64_t>(1, int64_t(piece_cap / out_row));
     double* d_init = s.init.as<double>();
@@ -707,10 +721,14 @@ sdb_status run_shard(sdb_ctx* ctx, Slot& s, sdb_desc d, sdb_model* m, int64_t r0
         SDB_CUDA(ctx, cudaEventSynchronize(pb.ev));
         const double w1 = now_ms();
         const double* src = pb.as<double>();
-        const int64_t* fsrc = reinterpret_cast<const int64_t*>(src + p.rows * k * n);
+        const int64_t* fsrc = reinterpret_cast<const int64_t*>(src + p.rows * width);
         parallel_rows(p.rows, size_t(p.rows) * out_row, threads, [&](int64_t a, int64_t b) {
             for (int64_t r = a; r < b; ++r) {
                 const int64_t g = r0 + p.a + r;
+                if (out_mode) {
+                    std::memcpy(values + g * width, src + r * width, size_t(width) * sizeof(double));
+                    continue;
+                }
                 double* dst = values + g * (k + 1) * n;
                 std::memcpy(dst, init + g * n, size_t(n) * sizeof(double));
                 std::memcpy(dst + n, src + r * k * n, size_t(k) * n * sizeof(double));
@@ -764,7 +782,7 @@ sdb_status run_shard(sdb_ctx* ctx, Slot& s, sdb_desc d, sdb_model* m, int64_t r0
         td.orbit_offset = d.orbit_offset + a;
         td.orbits = b - a;
         sdb_status rc = launch_device(ctx, s, td, m, d_init + a * n, d_params + a * np_,
-                                      d_values + a * k * n, d_fail + a, s.stream);
+                                      d_values + a * width, d_fail + a, s.stream, out_mode);
         if (rc != SDB_OK) return rc;
         SDB_CUDA(ctx, cudaEventRecord(s.ev_tile[t], s.stream));
         return SDB_OK;
@@ -784,10 +802,10 @@ sdb_status run_shard(sdb_ctx* ctx, Slot& s, sdb_desc d, sdb_model* m, int64_t r0
             PinBuf& pb = s.pin_out[slot];
             SDB_CUDA(ctx, pb.ensure(size_t(pr) * out_row));
             double* dst = pb.as<double>();
-            SDB_CUDA(ctx, cudaMemcpyAsync(dst, d_values + p0 * k * n,
-                                          size_t(pr) * k * n * sizeof(double),
+            SDB_CUDA(ctx, cudaMemcpyAsync(dst, d_values + p0 * width,
+                                          size_t(pr) * width * sizeof(double),
                                           cudaMemcpyDeviceToHost, s.d2h));
-            SDB_CUDA(ctx, cudaMemcpyAsync(dst + pr * k * n, d_fail + p0,
+            SDB_CUDA(ctx, cudaMemcpyAsync(dst + pr * width, d_fail + p0,
                                           size_t(pr) * sizeof(int64_t), cudaMemcpyDeviceToHost,
                                           s.d2h));
             SDB_CUDA(ctx, cudaEventRecord(pb.ev, s.d2h));
@@ -869,7 +887,7 @@ sdb_status validate_model(sdb_ctx* ctx, const sdb_desc* d, const sdb_model* m) {
 
 // Host-buffer run over all of the context's devices (validated descriptor).
 sdb_status run_host(sdb_ctx* ctx, const sdb_desc& d, sdb_model* m, const double* init,
-                    const double* params, double* values, int64_t* fail_step) {
+                    const double* params, double* values, int64_t* fail_step, int out_mode = 0) {
     if (!init || !params || !values || !fail_step)
         return fail_with(ctx, SDB_ERR_ARGUMENT, "null host buffer");
     const int64_t nslots = int64_t(ctx->slots.size());
@@ -884,7 +902,7 @@ sdb_status run_host(sdb_ctx* ctx, const sdb_desc& d, sdb_model* m, const double*
     auto shard = [&](int64_t g) {
         const int64_t r0 = g * d.orbits / used, r1 = (g + 1) * d.orbits / used;
         status[g] = run_shard(ctx, ctx->slots[g], d, m, r0, r1 - r0, init, params, values,
-                              fail_step, int(used));
+                              fail_step, int(used), out_mode);
     };
     if (used == 1) {
         shard(0);
@@ -906,14 +924,15 @@ sdb_status run_host(sdb_ctx* ctx, const sdb_desc& d, sdb_model* m, const double*
 
 // Device-buffer run on the first device (validated descriptor).
 sdb_status run_dev(sdb_ctx* ctx, const sdb_desc& d, sdb_model* m, const double* d_init,
-                   const double* d_params, double* d_values, int64_t* d_fail_step, void* stream) {
+                   const double* d_params, double* d_values, int64_t* d_fail_step, void* stream,
+                   int out_mode = 0) {
     if (!d_init || !d_params || !d_values || !d_fail_step)
         return fail_with(ctx, SDB_ERR_ARGUMENT, "null device buffer");
     Slot& s = ctx->slots[0];
     SDB_CUDA(ctx, cudaSetDevice(s.device));
     s.launches = 0;
     sdb_status rc = launch_device(ctx, s, d, m, d_init, d_params, d_values, d_fail_step,
-                                  static_cast<cudaStream_t>(stream));
+                                  static_cast<cudaStream_t>(stream), out_mode);
     ctx->launches = s.launches;
     ctx->last_lanes = s.lanes;
     ctx->last_persistent = s.persistent;
@@ -1064,6 +1083,49 @@ sdb_status sdb_run_device(sdb_ctx* ctx, const sdb_desc* desc, const double* d_in
     sdb_status rc = validate(ctx, desc);
     if (rc != SDB_OK) return rc;
     return run_dev(ctx, *desc, nullptr, d_init, d_params, d_values, d_fail_step, stream);
+}
+
+/* ---- analysis (analysis.py) ---------------------------------------------- */
+
+sdb_status sdb_run_coherence(sdb_ctx* ctx, const sdb_desc* desc, const double* init,
+                             const double* params, double* r_phi, int64_t* fail_step) {
+    if (!ctx) return fail_with(nullptr, SDB_ERR_ARGUMENT, "null context");
+    ctx->error.clear();
+    sdb_status rc = validate(ctx, desc);
+    if (rc != SDB_OK) return rc;
+    return run_host(ctx, *desc, nullptr, init, params, r_phi, fail_step, 1);
+}
+
+sdb_status sdb_run_coherence_device(sdb_ctx* ctx, const sdb_desc* desc, const double* d_init,
+                                    const double* d_params, double* d_r_phi, int64_t* d_fail_step,
+                                    void* stream) {
+    if (!ctx) return fail_with(nullptr, SDB_ERR_ARGUMENT, "null context");
+    ctx->error.clear();
+    sdb_status rc = validate(ctx, desc);
+    if (rc != SDB_OK) return rc;
+    return run_dev(ctx, *desc, nullptr, d_init, d_params, d_r_phi, d_fail_step, stream, 1);
+}
+
+sdb_status sdb_order_parameter(sdb_ctx* ctx, int32_t n, int64_t rows, const double* phases,
+                               double* r, double* phi) {
+    sdb_status rc = utility_prologue(ctx);
+    if (rc != SDB_OK) return rc;
+    if (n < 1 || rows < 0 || !phases || !r || !phi)
+        return fail_with(ctx, SDB_ERR_ARGUMENT, "bad order-parameter arguments");
+    if (rows == 0) return SDB_OK;
+    TmpBuf dth, dr, dphi;
+    SDB_CUDA(ctx, cudaMalloc(&dth.p, size_t(rows) * n * sizeof(double)));
+    SDB_CUDA(ctx, cudaMalloc(&dr.p, size_t(rows) * sizeof(double)));
+    SDB_CUDA(ctx, cudaMalloc(&dphi.p, size_t(rows) * sizeof(double)));
+    SDB_CUDA(ctx, cudaMemcpy(dth.p, phases, size_t(rows) * n * sizeof(double),
+                             cudaMemcpyHostToDevice));
+    SDB_CUDA(ctx, sdeb::launch_order_parameter(static_cast<const double*>(dth.p), n, rows,
+                                               static_cast<double*>(dr.p),
+                                               static_cast<double*>(dphi.p), nullptr));
+    SDB_CUDA(ctx, cudaMemcpy(r, dr.p, size_t(rows) * sizeof(double), cudaMemcpyDeviceToHost));
+    SDB_CUDA(ctx, cudaMemcpy(phi, dphi.p, size_t(rows) * sizeof(double), cudaMemcpyDeviceToHost));
+    ctx->launches = 1;
+    return SDB_OK;
 }
 
 /* ---- expression-template models ------------------------------------------ */

@@ -20,6 +20,7 @@
 #include <cstdint>
 #include <math_constants.h>
 
+#include "sdeb_analysis.cuh"
 #include "sdeb_rng.cuh"
 
 namespace sdeb {
@@ -182,6 +183,26 @@ __device__ __forceinline__ void drift(const double (&y)[J], const double (&om)[J
     }
 }
 
+// Order parameter of the orbit (analysis.py:77-82) from its lanes' phases:
+// the canonical-tree sums of cos / sin (as drift_meanfield), every lane gets
+// (r, Phi).  Used at sample time when the run stores coherence instead of y.
+template <int J, bool PADDED>
+__device__ __forceinline__ void group_order_param(const double (&y)[J], int base, int n, int lanes,
+                                                  double& r, double& phi) {
+    double sn[J], cs[J];
+    sincos_vec<J>(y, sn, cs);
+#pragma unroll
+    for (int q = 0; q < J; ++q) {
+        if (PADDED && base + q >= n) {
+            sn[q] = 0.0;
+            cs[q] = 0.0;
+        }
+    }
+    const double ss = group_sum(lane_tree_sum<J>(sn), lanes);
+    const double sc = group_sum(lane_tree_sum<J>(cs), lanes);
+    order_param_from_sums(sc, ss, n, r, phi);
+}
+
 // ---- noise for one step (rng.py:150-188 / DESIGN.md streams) ---------------
 
 template <int J>
@@ -261,7 +282,11 @@ __device__ __forceinline__ void step_noise_apply(const RunArgs& a, int64_t row, 
 // rng seeded / loaded per a.fresh); otherwise the state saved by the previous
 // slab is resumed from state_out / rng_state / fail_step.  Saving and resuming
 // are exact, so any slab split gives bit-identical results.
-template <int J, int SOLVER, int STREAM, int COUPLING, bool PADDED>
+// COH: samples are the orbit's order parameter instead of its phases
+// (analysis.py coherence_series fused into the run): per orbit row a plane of
+// r then a plane of Phi, values[row*2*vstride + {0, vstride} + 1 + c-chunk_begin],
+// sample 0 (the initial state) at offset 0.
+template <int J, int SOLVER, int STREAM, int COUPLING, bool PADDED, bool COH = false>
 __device__ __forceinline__ void run_item(const RunArgs& a, int64_t cg, uint64_t s0, uint64_t s1,
                                          bool first, double* sh, double* shs) {
     constexpr bool kStochastic = (SOLVER == KS_EM) && (STREAM != KS_NONE);
@@ -323,6 +348,15 @@ __device__ __forceinline__ void run_item(const RunArgs& a, int64_t cg, uint64_t 
             }
         }
 
+        if (COH && fresh && s0 == 0) {  // coherence of the initial state
+            double r, phi;
+            group_order_param<J, PADDED>(y, base, n, lanes, r, phi);
+            if (active && lane == 0) {
+                double* o = a.values + row * a.vstride * 2;
+                o[0] = r;
+                o[a.vstride] = phi;
+            }
+        }
         const double dt = a.dt;
         const uint64_t ks = uint64_t(a.ksteps);
         // Segments between chunk ends: the sample write sits outside the hot
@@ -396,8 +430,16 @@ __device__ __forceinline__ void run_item(const RunArgs& a, int64_t cg, uint64_t 
 #pragma unroll
                     for (int q = 0; q < J; ++q) y[q] = CUDART_NAN;
                 }
-                if (active) {
-                    const int64_t c = int64_t(step / ks) - 1;
+                const int64_t c = int64_t(step / ks) - 1;
+                if constexpr (COH) {
+                    double r, phi;
+                    group_order_param<J, PADDED>(y, base, n, lanes, r, phi);
+                    if (active && lane == 0) {
+                        double* o = a.values + row * a.vstride * 2 + 1 + (c - a.chunk_begin);
+                        o[0] = r;
+                        o[a.vstride] = phi;
+                    }
+                } else if (active) {
                     double* out = a.values + (row * a.vstride + (c - a.chunk_begin)) * n + base;
 #pragma unroll
                     for (int q = 0; q < J; ++q)
@@ -453,6 +495,8 @@ __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
 // VAR: 0 = unpadded (n == lanes * J, no per-oscillator predicates),
 // 1 = padded, 2 = unpadded with registers capped (tight_minb<J>() CTAs/SM):
 // more resident warps against fewer registers; the autotuner decides.
+// VAR + kVarCoherence (4, 5): the same with order-parameter samples.
+constexpr int kVarCoherence = 4;
 template <int J>
 __host__ __device__ constexpr int tight_minb() {
     return J == 4 ? 6 : (J == 8 ? 4 : 1);
@@ -461,7 +505,8 @@ __host__ __device__ constexpr int tight_minb() {
 template <int J, int SOLVER, int STREAM, int COUPLING, int VAR>
 __global__ void __launch_bounds__(kBlock, (VAR == 2 ? tight_minb<J>() : 0))
     kuramoto_run_kernel(const RunArgs a) {
-    constexpr bool PADDED = VAR == 1;
+    constexpr bool PADDED = (VAR & 1) != 0;
+    constexpr bool COH = VAR >= kVarCoherence;
     extern __shared__ double smem[];
     double* sh = smem;                  // pairwise: [J][kBlock]
     double* shs = smem + J * kBlock;    // pairwise L==1: [J][kBlock]
@@ -492,7 +537,7 @@ __global__ void __launch_bounds__(kBlock, (VAR == 2 ? tight_minb<J>() : 0))
         if (persistent) __syncthreads();
         const uint64_t s0 = begin + uint64_t(k) * slab;
         const uint64_t s1 = s0 + slab < end ? s0 + slab : end;
-        run_item<J, SOLVER, STREAM, COUPLING, PADDED>(a, cg, s0, s1, k == 0, sh, shs);
+        run_item<J, SOLVER, STREAM, COUPLING, PADDED, COH>(a, cg, s0, s1, k == 0, sh, shs);
         if (!persistent) break;
         __threadfence();
         __syncthreads();

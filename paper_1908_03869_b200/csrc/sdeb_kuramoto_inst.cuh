@@ -38,8 +38,9 @@ static cudaError_t occupancy_one(size_t smem, int* blocks) {
 
 // Visits the kernel instantiation for (solver, stream, coupling, variant)
 // with op.template run<J, S, R, C, V>() (V: 0 unpadded, 1 padded, 2 unpadded
-// register-capped).  Pairwise and the explicit-noise / drift entry points
-// always use the padded form; capped variants exist where tight_minb<J>() > 1.
+// register-capped; +4: samples are the order parameter, kVarCoherence).
+// Pairwise and the explicit-noise / drift entry points always use the padded
+// form; capped variants exist where tight_minb<J>() > 1.
 template <int J, class Op>
 static cudaError_t dispatch(int solver, int stream, int coupling, int variant, Op&& op) {
     if (variant == 2 && tight_minb<J>() == 1) variant = 0;
@@ -47,16 +48,21 @@ static cudaError_t dispatch(int solver, int stream, int coupling, int variant, O
     switch (variant) {                                                           \
         case 0: return op.template run<J, S, R, KC_MEANFIELD, 0>();              \
         case 1: return op.template run<J, S, R, KC_MEANFIELD, 1>();              \
+        case 4: return op.template run<J, S, R, KC_MEANFIELD, 4>();              \
+        case 5: return op.template run<J, S, R, KC_MEANFIELD, 5>();              \
         default: return op.template run<J, S, R, KC_MEANFIELD, (tight_minb<J>() > 1 ? 2 : 0)>(); \
     }
+#define SDEB_PAIR(S, R)                                                          \
+    return variant >= kVarCoherence ? op.template run<J, S, R, KC_PAIRWISE, 5>() \
+                                    : op.template run<J, S, R, KC_PAIRWISE, 1>();
     if (coupling == KC_PAIRWISE) {
-        if (solver == KS_RK4) return op.template run<J, KS_RK4, KS_NONE, KC_PAIRWISE, 1>();
+        if (solver == KS_RK4) SDEB_PAIR(KS_RK4, KS_NONE);
         if (solver == KS_DRIFT) return op.template run<J, KS_DRIFT, KS_NONE, KC_PAIRWISE, 1>();
         switch (stream) {
-            case KS_PHILOX: return op.template run<J, KS_EM, KS_PHILOX, KC_PAIRWISE, 1>();
-            case KS_SFC64: return op.template run<J, KS_EM, KS_SFC64, KC_PAIRWISE, 1>();
-            case KS_XOSHIRO: return op.template run<J, KS_EM, KS_XOSHIRO, KC_PAIRWISE, 1>();
-            case KS_NONE: return op.template run<J, KS_EM, KS_NONE, KC_PAIRWISE, 1>();
+            case KS_PHILOX: SDEB_PAIR(KS_EM, KS_PHILOX);
+            case KS_SFC64: SDEB_PAIR(KS_EM, KS_SFC64);
+            case KS_XOSHIRO: SDEB_PAIR(KS_EM, KS_XOSHIRO);
+            case KS_NONE: SDEB_PAIR(KS_EM, KS_NONE);
             case KS_EXPLICIT: return op.template run<J, KS_EM, KS_EXPLICIT, KC_PAIRWISE, 1>();
             default: return cudaErrorInvalidValue;
         }
@@ -72,6 +78,7 @@ static cudaError_t dispatch(int solver, int stream, int coupling, int variant, O
         default: return cudaErrorInvalidValue;
     }
 #undef SDEB_PICK
+#undef SDEB_PAIR
 }
 
 struct LaunchOp {

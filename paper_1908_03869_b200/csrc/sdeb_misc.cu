@@ -9,6 +9,7 @@
 #include <cstdint>
 
 #include "sdeb_misc.h"
+#include "sdeb_analysis.cuh"
 #include "sdeb_rng.cuh"
 
 namespace sdeb {
@@ -204,6 +205,24 @@ cudaError_t launch_sample_kuramoto(int n, uint64_t seed, const uint32_t* orbits,
                                    cudaStream_t st) {
     sample_kuramoto_kernel<<<grid_for(count * ((3 * n + 3) / 4), 128), 128, 0, st>>>(
         n, seed, orbits, count, omega_lo, omega_w, noise_lo, noise_w, coupling, init, params);
+    return cudaGetLastError();
+}
+
+// analysis.py:77-82 over a stored trajectory: one thread per population.
+__global__ void order_parameter_kernel(const double* __restrict__ th, int n, int64_t rows,
+                                       double* __restrict__ r, double* __restrict__ phi) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= rows) return;
+    double rr, pp;
+    order_param_row(th + i * n, n, rr, pp);
+    r[i] = rr;
+    phi[i] = pp;
+}
+
+cudaError_t launch_order_parameter(const double* th, int n, int64_t rows, double* r, double* phi,
+                                   cudaStream_t st) {
+    if (rows <= 0) return cudaSuccess;
+    order_parameter_kernel<<<unsigned((rows + 127) / 128), 128, 0, st>>>(th, n, rows, r, phi);
     return cudaGetLastError();
 }
 

@@ -18,6 +18,10 @@ cudaError_t launch_sample_kuramoto(int n, uint64_t seed, const uint32_t* orbits,
                                    double noise_w, double coupling, double* init, double* params,
                                    cudaStream_t st);
 
+// Order parameter (r, Phi) of `rows` populations of n phases (analysis.py:77-82).
+cudaError_t launch_order_parameter(const double* th, int n, int64_t rows, double* r, double* phi,
+                                   cudaStream_t st);
+
 // FP64 DFMA-throughput probe: blocks x 256 threads x iters x 128 DFMA.
 cudaError_t launch_fp64_peak(int blocks, int iters, double* out, cudaStream_t st);
 cudaError_t launch_math_probe(int func, const double* x, int64_t count, double* out,

@@ -222,16 +222,11 @@ def shard_bounds(orbits: int, world: int, rank: int) -> tuple[int, int]:
     return rank * orbits // world, (rank + 1) * orbits // world
 
 
-def run_batch(model: ModelSpec, config: EngineConfig, batch: OrbitBatch, *,
-              orbit_offset: int = 0) -> TrajectoryStore:
-    """Integrate every orbit of the batch on the GPU and sample once per chunk
-    (engine.py:221-314).  Validation happens before any device allocation,
-    in the reference's order.
-
-    ``orbit_offset`` (keyword, default 0 = the reference's numbering) is the
-    global id of row 0: noise is keyed by global id and failures report it, so
-    a shard of a larger batch integrates exactly as those rows of the whole.
-    """
+def validate_run(model: ModelSpec, config: EngineConfig, batch: OrbitBatch, orbit_offset: int = 0,
+                 store_cap: bool = True) -> int:
+    """run_batch's checks in the reference's order (engine.py:229-247); returns
+    the chunk count.  ``store_cap=False`` skips the trajectory-store size cap
+    (runs that never materialise the store, e.g. analysis.run_coherence)."""
     batch.check_against(model)
     if batch.orbits != config.orbits:
         raise ConfigError("config says %d orbits but batch has %d"
@@ -246,12 +241,27 @@ def run_batch(model: ModelSpec, config: EngineConfig, batch: OrbitBatch, *,
 
     samples = chunks + 1
     store_bytes = batch.orbits * samples * model.nequat * 8
-    if store_bytes > config.max_store_bytes:
+    if store_cap and store_bytes > config.max_store_bytes:
         raise ConfigError(
             "trajectory store would need %d bytes (orbits=%d, samples=%d, nequat=%d), "
             "above the configured cap of %d"
             % (store_bytes, batch.orbits, samples, model.nequat, config.max_store_bytes))
     _check_stepper(model, config)
+    return chunks
+
+
+def run_batch(model: ModelSpec, config: EngineConfig, batch: OrbitBatch, *,
+              orbit_offset: int = 0) -> TrajectoryStore:
+    """Integrate every orbit of the batch on the GPU and sample once per chunk
+    (engine.py:221-314).  Validation happens before any device allocation,
+    in the reference's order.
+
+    ``orbit_offset`` (keyword, default 0 = the reference's numbering) is the
+    global id of row 0: noise is keyed by global id and failures report it, so
+    a shard of a larger batch integrates exactly as those rows of the whole.
+    """
+    chunks = validate_run(model, config, batch, orbit_offset)
+    samples = chunks + 1
     desc = make_desc(model, config, chunks, batch.orbits, orbit_offset)
     if desc.model == nat.SDB_MODEL_EXPRESSION:
         # indices are checked up front: the reference raises DomainError at step 0

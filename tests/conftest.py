@@ -62,3 +62,12 @@ def golden_dsl():
     with open(os.path.join(GOLDEN_DIR, "cases_dsl.json")) as fh:
         cases = json.load(fh)
     return {k: data[k] for k in data.files}, cases
+
+
+@pytest.fixture(scope="session")
+def golden_analysis():
+    """Reference analysis outputs (tests/golden/make_golden_analysis.py)."""
+    data = np.load(os.path.join(GOLDEN_DIR, "golden_analysis_v1.npz"))
+    with open(os.path.join(GOLDEN_DIR, "cases_analysis.json")) as fh:
+        cases = json.load(fh)
+    return {k: data[k] for k in data.files}, cases
