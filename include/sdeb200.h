@@ -166,6 +166,20 @@ sdb_status sdb_fp64_peak(sdb_ctx* ctx, double* ops_per_s, double* ms);
 sdb_status sdb_math_probe(sdb_ctx* ctx, int32_t func, const double* x, int64_t count,
                           double* out);
 
+/* ---- streaming store writer (storage.py:108-131) -------------------------------- */
+
+/* run_batch straight into an SDB1 binary store file (storage.py write_store_bin):
+ * the caller has written the header and the sample times; the value section,
+ * [orbits][chunks+1][nequat] little-endian float64 rows of [initial state |
+ * samples 1..k], starts at byte `offset` of the existing file `path`.  Each
+ * output piece is written with pwrite as it drains from the GPU, so the store
+ * is never held in host memory.  model: NULL for the Kuramoto stepper, else an
+ * expression-template model (desc->model = SDB_MODEL_EXPRESSION).  fail_step
+ * as sdb_run. */
+sdb_status sdb_run_to_file(sdb_ctx* ctx, sdb_model* model, const sdb_desc* desc,
+                           const double* init, const double* params, const char* path,
+                           int64_t offset, int64_t* fail_step);
+
 /* ---- analysis (analysis.py:72-186) -------------------------------------------- */
 
 /* run_batch fused with coherence_series (analysis.py:98-101): the Kuramoto

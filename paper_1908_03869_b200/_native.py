@@ -59,6 +59,9 @@ SIGNATURES = {
     "sdb_last_lanes": (ctypes.c_int32, [ctypes.c_void_p]),
     "sdb_last_layout": (None, [ctypes.c_void_p] + [ctypes.POINTER(ctypes.c_int32)] * 5),
     "sdb_philox_words": (ctypes.c_int, [ctypes.c_void_p, _c_u32_p, ctypes.c_int64, _c_u32_p]),
+    "sdb_run_to_file": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(SdbDesc),
+                                       _c_double_p, _c_double_p, ctypes.c_char_p, ctypes.c_int64,
+                                       _c_i64_p]),
     "sdb_run_coherence": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(SdbDesc), _c_double_p,
                                          _c_double_p, _c_double_p, _c_i64_p]),
     "sdb_run_coherence_device": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(SdbDesc)]

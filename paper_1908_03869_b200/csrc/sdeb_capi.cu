@@ -5,8 +5,12 @@
 // driven by one host thread each, and the per-group Python step loop is the
 // fused kernel of sdeb_kuramoto.cuh.
 #include <cuda_runtime.h>
+#include <fcntl.h>
+#include <unistd.h>
 
 #include <algorithm>
+#include <atomic>
+#include <cerrno>
 #include <chrono>
 #include <cmath>
 #include <cstdarg>
@@ -674,9 +678,35 @@ int64_t shard_tiles(const sdb_desc& d, int64_t rows, int device) {
 // before the outputs of tile t are drained, so host copies, both DMA
 // directions and the kernels overlap.  Results are identical for any tiling:
 // noise is keyed by global orbit id and orbits are independent.
+// pwrite the whole buffer (retrying short writes); false on error.
+bool pwrite_all(int fd, const void* buf, size_t bytes, int64_t offset) {
+    const char* p = static_cast<const char*>(buf);
+    while (bytes > 0) {
+        const ssize_t w = ::pwrite(fd, p, bytes, off_t(offset));
+        if (w < 0) {
+            if (errno == EINTR) continue;
+            return false;
+        }
+        p += w;
+        bytes -= size_t(w);
+        offset += w;
+    }
+    return true;
+}
+
+// Where a host-buffer run's store goes: the caller's (M, k+1, n) array, or
+// (fd >= 0) an SDB1 file whose value section starts at byte `offset`.
+struct OutSink {
+    double* values = nullptr;
+    int fd = -1;
+    int64_t offset = 0;
+};
+
 sdb_status run_shard(sdb_ctx* ctx, Slot& s, sdb_desc d, sdb_model* m, int64_t r0, int64_t rows,
-                     const double* init, const double* params, double* values, int64_t* fail,
+                     const double* init, const double* params, const OutSink& sink, int64_t* fail,
                      int shards, int out_mode) {
+    double* values = sink.values;
+    std::atomic<int> write_errno{0};
     SDB_CUDA(ctx, cudaSetDevice(s.device));
     const bool tr = trace_enabled();
     const double t0 = tr ? now_ms() : 0.0;
@@ -723,6 +753,19 @@ sdb_status run_shard(sdb_ctx* ctx, Slot& s, sdb_desc d, sdb_model* m, int64_t r0
         const double* src = pb.as<double>();
         const int64_t* fsrc = reinterpret_cast<const int64_t*>(src + p.rows * width);
         parallel_rows(p.rows, size_t(p.rows) * out_row, threads, [&](int64_t a, int64_t b) {
+            if (sink.fd >= 0) {  // rows [a, b) of the piece are contiguous in the file
+                const size_t row_words = size_t(k + 1) * n;
+                std::vector<double> buf(size_t(b - a) * row_words);
+                for (int64_t r = a; r < b; ++r) {
+                    double* dst = buf.data() + size_t(r - a) * row_words;
+                    std::memcpy(dst, init + (r0 + p.a + r) * n, size_t(n) * sizeof(double));
+                    std::memcpy(dst + n, src + r * k * n, size_t(k) * n * sizeof(double));
+                }
+                const int64_t at = sink.offset + (r0 + p.a + a) * int64_t(row_words * sizeof(double));
+                if (!pwrite_all(sink.fd, buf.data(), buf.size() * sizeof(double), at))
+                    write_errno.store(errno ? errno : EIO);
+                return;
+            }
             for (int64_t r = a; r < b; ++r) {
                 const int64_t g = r0 + p.a + r;
                 if (out_mode) {
@@ -825,6 +868,9 @@ sdb_status run_shard(sdb_ctx* ctx, Slot& s, sdb_desc d, sdb_model* m, int64_t r0
         if (rc == SDB_OK) rc = issue_outputs(t, lo(t), lo(t + 1));
     }
     while (rc == SDB_OK && head < pending.size()) rc = drain_one();
+    if (rc == SDB_OK && write_errno.load() != 0)
+        rc = fail_with(ctx, SDB_ERR_CUDA, "writing the store file failed: %s",
+                       std::strerror(write_errno.load()));
     if (rc != SDB_OK) {
         cudaStreamSynchronize(s.h2d);  // leave no DMA in flight into pinned slots
         cudaStreamSynchronize(s.stream);
@@ -887,9 +933,14 @@ sdb_status validate_model(sdb_ctx* ctx, const sdb_desc* d, const sdb_model* m) {
 
 // Host-buffer run over all of the context's devices (validated descriptor).
 sdb_status run_host(sdb_ctx* ctx, const sdb_desc& d, sdb_model* m, const double* init,
-                    const double* params, double* values, int64_t* fail_step, int out_mode = 0) {
-    if (!init || !params || !values || !fail_step)
+                    const double* params, double* values, int64_t* fail_step, int out_mode = 0,
+                    int fd = -1, int64_t file_offset = 0) {
+    if (!init || !params || (!values && fd < 0) || !fail_step)
         return fail_with(ctx, SDB_ERR_ARGUMENT, "null host buffer");
+    OutSink sink;
+    sink.values = values;
+    sink.fd = fd;
+    sink.offset = file_offset;
     const int64_t nslots = int64_t(ctx->slots.size());
     const int64_t used = std::min<int64_t>(nslots, d.orbits);
     std::vector<sdb_status> status(used, SDB_OK);
@@ -901,7 +952,7 @@ sdb_status run_host(sdb_ctx* ctx, const sdb_desc& d, sdb_model* m, const double*
     // contiguous shards [g*M/G, (g+1)*M/G)
     auto shard = [&](int64_t g) {
         const int64_t r0 = g * d.orbits / used, r1 = (g + 1) * d.orbits / used;
-        status[g] = run_shard(ctx, ctx->slots[g], d, m, r0, r1 - r0, init, params, values,
+        status[g] = run_shard(ctx, ctx->slots[g], d, m, r0, r1 - r0, init, params, sink,
                               fail_step, int(used), out_mode);
     };
     if (used == 1) {
@@ -1083,6 +1134,24 @@ sdb_status sdb_run_device(sdb_ctx* ctx, const sdb_desc* desc, const double* d_in
     sdb_status rc = validate(ctx, desc);
     if (rc != SDB_OK) return rc;
     return run_dev(ctx, *desc, nullptr, d_init, d_params, d_values, d_fail_step, stream);
+}
+
+/* ---- streaming store writer (storage.py:108-131) ------------------------- */
+
+sdb_status sdb_run_to_file(sdb_ctx* ctx, sdb_model* model, const sdb_desc* desc,
+                           const double* init, const double* params, const char* path,
+                           int64_t offset, int64_t* fail_step) {
+    if (!ctx) return fail_with(nullptr, SDB_ERR_ARGUMENT, "null context");
+    ctx->error.clear();
+    sdb_status rc = model ? validate_model(ctx, desc, model) : validate(ctx, desc);
+    if (rc != SDB_OK) return rc;
+    if (!path || offset < 0) return fail_with(ctx, SDB_ERR_ARGUMENT, "bad store file arguments");
+    const int fd = ::open(path, O_WRONLY | O_CLOEXEC);
+    if (fd < 0) return fail_with(ctx, SDB_ERR_CUDA, "opening %s: %s", path, std::strerror(errno));
+    rc = run_host(ctx, *desc, model, init, params, nullptr, fail_step, 0, fd, offset);
+    if (::close(fd) != 0 && rc == SDB_OK)
+        rc = fail_with(ctx, SDB_ERR_CUDA, "closing %s: %s", path, std::strerror(errno));
+    return rc;
 }
 
 /* ---- analysis (analysis.py) ---------------------------------------------- */
