@@ -16,11 +16,11 @@ from .engine import (EngineConfig, TrajectoryStore, OrbitFailure, ConfigError, r
                      iteration_count, partition_orbits)
 from .solvers import (euler_maruyama_step, euler_step, rk4_step, implicit_euler_step,
                       implicit_midpoint_step, get_solver, SOLVERS)
-from .storage import store_hash
+from .storage import store_hash, write_store, read_store, run_batch_to_file
 from .analysis import (CoherencePoint, CoherenceSeries, EnsembleStats, order_parameter,
                        coherence_series, ensemble_stats, dt_sweep, kymograph_export, wrap_phase,
                        run_coherence)
-from . import analysis, dsl, rng
+from . import analysis, dsl, rng, storage
 
 __all__ = [
     "__version__",
@@ -31,7 +31,8 @@ __all__ = [
     "iteration_count", "partition_orbits",
     "euler_maruyama_step", "euler_step", "rk4_step",
     "implicit_euler_step", "implicit_midpoint_step", "get_solver", "SOLVERS",
-    "store_hash", "dsl", "rng", "analysis",
+    "store_hash", "write_store", "read_store", "run_batch_to_file", "storage",
+    "dsl", "rng", "analysis",
     "CoherencePoint", "CoherenceSeries", "EnsembleStats", "order_parameter", "coherence_series",
     "ensemble_stats", "dt_sweep", "kymograph_export", "wrap_phase", "run_coherence",
 ]

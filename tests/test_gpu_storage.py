@@ -29,7 +29,7 @@ def test_stream_to_file_kuramoto(tmp_path, stream, monkeypatch):
     n, m = 16, 777
     batch = sdb.sample_kuramoto_batch(n, m, (0.2, 0.4), (0.01, 0.1), 0.3, seed=2)
     params = batch.params.copy()
-    params[500, 3] = 1e308  # a failing orbit
+    params[500, 3] = np.inf  # a failing orbit (inf frequency: non-finite at step 0)
     batch = OrbitBatch(init=batch.init, params=params)
     cfg = EngineConfig(dt=1e-2, tspan=1.0, ksteps=10, orbits=m, seed=6, stream=stream)
     ref = _same_file(tmp_path, sdb.kuramoto_model(n), cfg, batch, {"run": "k"})
