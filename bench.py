@@ -89,35 +89,40 @@ TEMPLATES = {
 }
 
 
-SINCOS_OPS = 17      # csrc/sdeb_math.cuh sincos_tab: 5 reduction + 8 poly + 4 rotation
-BOX_MULLER_PAIR = 44  # 2 uniforms, log 13, -2*log 1, sqrt 8, angle 1, sincos 17, 2 products
+SINCOS_OPS = 15      # csrc/sdeb_math.cuh sincos_tab: 5 reduction + 6 poly + 4 rotation
+SIN_OPS = 13         # the same when only sin is used (the cos rotation is dead code)
+BOX_MULLER_PAIR = 42  # 2 uniforms, log 13, -2*log 1, sqrt 8, angle 1, sincos 15, 2 products
 
 
 def template_fp64_ops(n: int, model: str) -> float:
     """FP64 lane-ops per orbit-step of the generated program (counted from the
-    generated code): Kuramoto template n^2 terms x (difference 1, sin 15 --
-    the table sincos minus its cos-only ops --, sum 1) + per equation
-    (K/N 2, omega + 1) + noise 22 + update 5; OU 2 drift + 1 diffusion + noise
-    22 + update 5 per equation."""
+    generated code): Kuramoto template n^2 terms x (difference 1, sin 13, sum
+    1) + per equation (p[0]/N, *, + 3; diffusion product 1; noise 21; update
+    4); OU per equation drift 2 + diffusion 1 + noise 21 + update 4."""
     if model == "kuramoto_template":
-        return n * n * 17 + n * (3 + 22 + 5 + 1)
-    return n * (2 + 1 + 22 + 5)
+        return n * n * (1 + SIN_OPS + 1) + n * (3 + 1 + BOX_MULLER_PAIR / 2 + 4)
+    return n * (2 + 1 + BOX_MULLER_PAIR / 2 + 4)
 
 
 def algorithmic_fp64_ops(n: int, solver: str, coupling: str) -> float:
-    """FP64 lane-ops (DFMA/DMUL/DADD/DSETP) per orbit-step of the algorithm the
+    """FP64 lane-ops (DFMA/DMUL/DADD) per orbit-step of the algorithm the
     kernel runs, counted from the device code:
-    meanfield drift 24/oscillator (sincos 17, sums 2, S_i 3, f_i 2); pairwise
-    drift 20 per unordered pair (difference, sincos, 2 accumulates) + 2/osc;
-    Box-Muller 44 per pair of normals; EM update 5/osc; RK4 4 drifts + 13/osc."""
+    meanfield sums 20/oscillator (sincos 15, tree sums 2, S_i 3) and, for em,
+    the folded update 4 (fma(K/n*dt, S, omega*dt), 2 adds, (sqrt(dt)*s)*N) +
+    Box-Muller 42 per pair of normals; other solvers f_i = omega + K/n*S 2 more;
+    pairwise 16 per unordered pair (difference, sin 13, 2 accumulates) + 2/osc
+    and the unfolded em update 5; RK4 4 drifts + 13/osc."""
     if coupling == "meanfield":
-        drift = n * (SINCOS_OPS + 2 + 3 + 2)
+        sums = n * (SINCOS_OPS + 2 + 3)
+        if solver == "em":
+            return sums + n * (4 + BOX_MULLER_PAIR / 2)
+        drift = sums + 2 * n
     else:
-        drift = n * (n - 1) / 2 * (SINCOS_OPS + 3) + n * 2
+        drift = n * (n - 1) / 2 * (1 + SIN_OPS + 2) + n * 2
+        if solver == "em":
+            return drift + n * (5 + BOX_MULLER_PAIR / 2)
     if solver == "rk4":
         return 4 * drift + n * 13
-    if solver == "em":
-        return drift + n * (BOX_MULLER_PAIR / 2 + 5)
     return drift + n * 2
 
 

@@ -94,9 +94,8 @@ __device__ __forceinline__ int64_t group_fail(int64_t f, int lanes) {
 // the sums; the unpadded instantiation (n a power of two: every BASELINE
 // config) carries no per-oscillator predicates at all.
 template <int J, bool PADDED>
-__device__ __forceinline__ void drift_meanfield(const double (&y)[J], const double (&om)[J],
-                                                double kn, int base, int n, int lanes,
-                                                double (&f)[J]) {
+__device__ __forceinline__ void meanfield_sums(const double (&y)[J], int base, int n, int lanes,
+                                               double (&S)[J]) {
     double sn[J], cs[J], ts[J], tc[J];
     sincos_vec<J>(y, sn, cs);
 #pragma unroll
@@ -115,10 +114,19 @@ __device__ __forceinline__ void drift_meanfield(const double (&y)[J], const doub
 #pragma unroll
     for (int q = 0; q < J; ++q) {
         // two rounded products, not an FMA: the self term cos*sin - sin*cos
-        // then cancels exactly (n=1 gives f == omega, like sin(0) == 0)
-        const double s = __dsub_rn(__dmul_rn(cs[q], a), __dmul_rn(sn[q], b));
-        f[q] = __dadd_rn(om[q], __dmul_rn(kn, s));
+        // then cancels exactly (n=1 gives S == 0, like sin(0) == 0)
+        S[q] = __dsub_rn(__dmul_rn(cs[q], a), __dmul_rn(sn[q], b));
     }
+}
+
+template <int J, bool PADDED>
+__device__ __forceinline__ void drift_meanfield(const double (&y)[J], const double (&om)[J],
+                                                double kn, int base, int n, int lanes,
+                                                double (&f)[J]) {
+    double S[J];
+    meanfield_sums<J, PADDED>(y, base, n, lanes, S);
+#pragma unroll
+    for (int q = 0; q < J; ++q) f[q] = __dadd_rn(om[q], __dmul_rn(kn, S[q]));
 }
 
 // PAIRWISE: S_i = sum_{j=0}^{n-1} sin(fl(y_j - y_i)), accumulated in j order.
@@ -316,6 +324,15 @@ __device__ __forceinline__ void run_item(const RunArgs& a, int64_t cg, uint64_t 
         sg[q] = (kStochastic && valid) ? __ldg(prow + 1 + n + i) : 0.0;
     }
 
+    // folded step constants of the meanfield EM form (see the step below)
+    double omdt[J], sgs[J];
+    const double kndt = __dmul_rn(kn, a.dt);
+#pragma unroll
+    for (int q = 0; q < J; ++q) {
+        omdt[q] = __dmul_rn(om[q], a.dt);
+        sgs[q] = __dmul_rn(a.sqrt_dt, sg[q]);
+    }
+
     if constexpr (SOLVER == KS_DRIFT) {
         double f[J];
         drift<J, COUPLING, PADDED>(y, om, kn, base, n, lanes, sh, shs, f);
@@ -368,7 +385,19 @@ __device__ __forceinline__ void run_item(const RunArgs& a, int64_t cg, uint64_t 
           for (; step < seg_end; ++step) {
             if constexpr (SOLVER == KS_EM) {
                 double f[J];
-                if constexpr (kStochastic) {
+                if constexpr (kStochastic && COUPLING == KC_MEANFIELD) {
+                    // the meanfield form, with the step constants folded:
+                    // (y + (omega*dt + (K/n*dt)*S)) + (sqrt(dt)*s_i)*N_i -- the
+                    // reference's (y + f*dt) + sqrt(dt)*(s_i*N_i) reassociated
+                    // (a few ulp per step), 4 FP64 ops instead of 7
+                    double S[J];
+                    meanfield_sums<J, PADDED>(y, base, n, lanes, S);
+                    step_noise_apply<J, STREAM, PADDED>(
+                        a, row, orbit_g, step, base, rs, [&](int q, double z) {
+                            y[q] = __dadd_rn(__dadd_rn(y[q], __fma_rn(kndt, S[q], omdt[q])),
+                                             __dmul_rn(sgs[q], z));
+                        });
+                } else if constexpr (kStochastic) {
                     drift<J, COUPLING, PADDED>(y, om, kn, base, n, lanes, sh, shs, f);
                     // (y + f*dt) + sqrt(dt) * (s_i * N_i)   (solvers.py:70-71, model.py:201)
                     step_noise_apply<J, STREAM, PADDED>(

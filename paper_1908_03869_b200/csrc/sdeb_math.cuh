@@ -37,8 +37,8 @@ enum MathConst : int {
     MC_C1, MC_C2, MC_C3, MC_C4, MC_C5, MC_C6,  // fdlibm k_cos.c
     MC_TWO_OVER_PI, MC_PIO2_1, MC_PIO2_2, MC_PIO2_3,
     MC_LN2_HI, MC_LN2_LO, MC_U32_BIAS, MC_INV7, MC_NEG_INV6, MC_INV5, MC_INV3,
-    MC_128_OVER_PI, MC_PI128_1, MC_PI128_2, MC_PI128_3,  // table sincos reduction
-    MC_T_S3, MC_T_S5, MC_T_S7, MC_T_C4, MC_T_C6,         // Taylor terms on |r| <= pi/256
+    MC_TAB_OVER_PI, MC_PITAB_1, MC_PITAB_2, MC_PITAB_3,  // table sincos reduction (pi/512)
+    MC_T_S3, MC_T_S5, MC_T_C4,                           // Taylor terms on |r| <= pi/1024
     MC_COUNT
 };
 
@@ -55,12 +55,12 @@ __constant__ static double kMC[MC_COUNT] = {  // non-const: keeps ptxas from fol
     2.31904681384629955842e-17,  // fl(ln 2 - fl(ln 2))
     1048576.0 - 2.3283064365386963e-10,  // 2^20 - 2^-32 (exact)
     0.14285714285714285, -0.16666666666666666, 0.2, 0.3333333333333333,
-    40.74366543152521,           // 128/pi
-    0.02454369260617026,         // fl(pi/128) = fl(pi) * 2^-7
-    9.567553118338697e-19,       // (pi - fl(pi))_hi * 2^-7
-    -2.3396639138424529e-35,     // next 53 bits * 2^-7
-    -0.16666666666666666, 0.008333333333333333, -0.0001984126984126984,  // -1/6, 1/120, -1/5040
-    0.041666666666666664, -0.001388888888888889,                         // 1/24, -1/720
+    162.97466172610083,          // 512/pi = 4 * fl(128/pi) (exact scaling)
+    0.006135923151542565,        // fl(pi/512) = fl(pi) * 2^-9
+    2.391888279584674e-19,       // (pi - fl(pi))_hi * 2^-9
+    -5.849159784606132e-36,      // next 53 bits * 2^-9
+    -0.16666666666666666, 0.008333333333333333,  // -1/6, 1/120
+    0.041666666666666664,                        // 1/24
 };
 
 constexpr double kRoundMagic = 6755399441055744.0;  // 1.5 * 2^52
@@ -112,26 +112,25 @@ __device__ __forceinline__ void sincos_quadrant(double x, double& s, double& c) 
     sincos_reduced(r, q, s, c);
 }
 
-// Table-driven sincos, |x| < 2^29: x = k*pi/128 + r, |r| <= pi/256 (3-part
-// Cody-Waite, first step exact), (sin, cos)(k*pi/128) from a 256-entry
-// correctly-rounded table indexed by k & 255 (no quadrant logic), short
-// Taylor series for r, and the angle-addition rotation.  17 FP64 ops + one
-// 16-byte load, vs 22 FP64 + ~8 select/sign ops for the minimax/quadrant
-// form.  Exactly odd in x (the table is antisymmetric in sin).
+// Table-driven sincos, |x| < 2^29: x = k*pi/512 + r, |r| <= pi/1024 (3-part
+// Cody-Waite, first step exact), (sin, cos)(k*pi/512) from a 1024-entry
+// correctly-rounded table indexed by k & 1023 (no quadrant logic), Taylor
+// terms to r^5 / r^4 (the next ones are < 2^-60 relative), and the
+// angle-addition rotation: 15 FP64 ops + one 16-byte load (the v10 256-entry
+// table needed 17, the minimax/quadrant form 22 + ~8 select/sign ops).
+// Exactly odd in x (the table is antisymmetric in sin).
 __device__ __forceinline__ void sincos_tab(double x, double& s, double& c) {
-    const double t = __fma_rn(x, kMC[MC_128_OVER_PI], kRoundMagic);
+    const double t = __fma_rn(x, kMC[MC_TAB_OVER_PI], kRoundMagic);
     const int k = __double2loint(t);
     const double kd = __dsub_rn(t, kRoundMagic);
-    double r = __fma_rn(-kd, kMC[MC_PI128_1], x);
-    r = __fma_rn(-kd, kMC[MC_PI128_2], r);
-    r = __fma_rn(-kd, kMC[MC_PI128_3], r);
-    const double2 e = __ldg(reinterpret_cast<const double2*>(kSinCosTable[k & 255]));
+    double r = __fma_rn(-kd, kMC[MC_PITAB_1], x);
+    r = __fma_rn(-kd, kMC[MC_PITAB_2], r);
+    r = __fma_rn(-kd, kMC[MC_PITAB_3], r);
+    const double2 e = __ldg(reinterpret_cast<const double2*>(kSinCosTable[k & (kSinCosN - 1)]));
     const double r2 = __dmul_rn(r, r);
-    double ps = __fma_rn(r2, kMC[MC_T_S7], kMC[MC_T_S5]);
-    ps = __fma_rn(r2, ps, kMC[MC_T_S3]);
+    const double ps = __fma_rn(r2, kMC[MC_T_S5], kMC[MC_T_S3]);
     const double sr = __fma_rn(__dmul_rn(r2, r), ps, r);             // sin r
-    double pc = __fma_rn(r2, kMC[MC_T_C6], kMC[MC_T_C4]);
-    pc = __fma_rn(r2, pc, -0.5);
+    const double pc = __fma_rn(r2, kMC[MC_T_C4], -0.5);
     const double cr = __fma_rn(r2, pc, 1.0);                         // cos r
     s = __fma_rn(e.x, cr, __dmul_rn(e.y, sr));                       // sin(a + r)
     c = __fma_rn(e.y, cr, -__dmul_rn(e.x, sr));                      // cos(a + r)

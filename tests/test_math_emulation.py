@@ -147,19 +147,17 @@ SCT = _sincos_table()
 
 
 def emu_sincos_tab(x):
-    t = fma(x, C["MC_128_OVER_PI"], MAGIC)
+    t = fma(x, C["MC_TAB_OVER_PI"], MAGIC)
     k = _bits(t) & 0xFFFFFFFF
     kd = t - MAGIC
-    r = fma(-kd, C["MC_PI128_1"], x)
-    r = fma(-kd, C["MC_PI128_2"], r)
-    r = fma(-kd, C["MC_PI128_3"], r)
-    sa, ca = SCT[k & 255]
+    r = fma(-kd, C["MC_PITAB_1"], x)
+    r = fma(-kd, C["MC_PITAB_2"], r)
+    r = fma(-kd, C["MC_PITAB_3"], r)
+    sa, ca = SCT[k & (len(SCT) - 1)]
     r2 = r * r
-    ps = fma(r2, C["MC_T_S7"], C["MC_T_S5"])
-    ps = fma(r2, ps, C["MC_T_S3"])
+    ps = fma(r2, C["MC_T_S5"], C["MC_T_S3"])
     sr = fma(r2 * r, ps, r)
-    pc = fma(r2, C["MC_T_C6"], C["MC_T_C4"])
-    pc = fma(r2, pc, -0.5)
+    pc = fma(r2, C["MC_T_C4"], -0.5)
     cr = fma(r2, pc, 1.0)
     return fma(sa, cr, ca * sr), fma(ca, cr, -(sa * sr))
 
@@ -168,18 +166,19 @@ def test_table_sincos_constants():
     from decimal import Decimal, getcontext
     getcontext().prec = 50
     pi = Decimal("3.14159265358979323846264338327950288419716939937510582097494")
-    split = Decimal(C["MC_PI128_1"]) + Decimal(C["MC_PI128_2"]) + Decimal(C["MC_PI128_3"])
-    assert abs(split - pi / 128) < Decimal(10) ** -45
-    assert C["MC_PI128_1"] == math.pi / 128
-    assert len(SCT) == 256 and SCT[0] == (0.0, 1.0) and SCT[64] == (1.0, 0.0)
-    for k in range(1, 256):
-        assert SCT[256 - k][0] == -SCT[k][0] and SCT[256 - k][1] == SCT[k][1]
+    split = Decimal(C["MC_PITAB_1"]) + Decimal(C["MC_PITAB_2"]) + Decimal(C["MC_PITAB_3"])
+    assert abs(split - pi / 512) < Decimal(10) ** -47
+    assert C["MC_PITAB_1"] == math.pi / 512 and C["MC_TAB_OVER_PI"] == 512 / math.pi
+    assert len(SCT) == 1024 and SCT[0] == (0.0, 1.0) and SCT[256] == (1.0, 0.0)
+    for k in range(1, 1024):
+        assert SCT[1024 - k][0] == -SCT[k][0] and SCT[1024 - k][1] == SCT[k][1]
 
 
 def test_emulated_table_sincos_within_2ulp_and_odd():
     g = np.random.default_rng(7)
     xs = list(g.uniform(-np.pi, np.pi, 1500)) + list(g.uniform(-2e3, 2e3, 1500)) + \
-        list(g.uniform(0, 2 * np.pi, 500)) + [k * math.pi / 128 for k in range(-300, 301, 7)] + \
+        list(g.uniform(0, 2 * np.pi, 500)) + [k * math.pi / 512 for k in range(-1200, 1201, 7)] + \
+        [(k + 0.5) * math.pi / 512 for k in range(-40, 40)] + \
         [0.0, 1e-300, 3.0e8, 2 * math.pi]
     for x in xs:
         s, c = emu_sincos_tab(float(x))
