@@ -329,7 +329,7 @@ int64_t slab_steps_for(int64_t total_steps, int64_t groups, int64_t grid) {
 
 // Candidate layouts per lanes-per-orbit: natural occupancy; CTA-per-SM caps
 // below it that turn a ragged last wave into full ones; and the persistent
-// work-pulling grid (when there are enough CTA-groups to feed it).
+// work-pulling grid (whenever the CTA-groups exceed one wave).
 sdb_status candidate_layouts(sdb_ctx* ctx, const Slot& s, const sdb_desc& d, int kind_solver,
                              int kind_stream, std::vector<Layout>* out) {
     const int P = next_pow2(d.nequat);
@@ -352,7 +352,7 @@ sdb_status candidate_layouts(sdb_ctx* ctx, const Slot& s, const sdb_desc& d, int
         if (occ < 1) continue;
         const int64_t ctas = cta_groups(d, L);
         out->push_back(Layout{L, 0, 0, occ, tight});
-        if (ctas >= 2 * int64_t(sms) * occ) out->push_back(Layout{L, 1, 0, occ, tight});
+        if (ctas > int64_t(sms) * occ) out->push_back(Layout{L, 1, 0, occ, tight});
         if (tight) continue;
         for (int cap = occ - 1; cap >= 1 && cap >= occ - 4; --cap) {
             const double waves_cap = double(ctas) / (double(sms) * cap);
@@ -398,6 +398,17 @@ sdb_status configure_layout(sdb_ctx* ctx, const Slot& s, DevBuf& work, const sdb
         a->slab_done = reinterpret_cast<unsigned*>(work.as<char>() + sizeof(uint64_t));
     }
     return SDB_OK;
+}
+
+// One device's contiguous shard [r0, r0+rows) of a host-buffer run.
+// SDEB200_TRACE=1: per-phase wall-clock of host-buffer runs on stderr (adds
+// stream synchronisations between phases; for diagnosis only).
+bool trace_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("SDEB200_TRACE");
+        return e && *e && *e != '0';
+    }();
+    return on;
 }
 
 // Pick the launch layout: cached, pinned (SDEB200_LAYOUT), single candidate,
@@ -459,7 +470,10 @@ sdb_status choose_layout(sdb_ctx* ctx, Slot& s, const sdb_desc& d, const double*
     float best = 1e30f;
     Layout best_l = cands[0];
     const int P = next_pow2(d.nequat);
-    auto timed = [&](const Layout& lay, int64_t steps, float* ms_out) -> sdb_status {
+    // reps launches of `steps` steps, best time; real_slabs: persistent slabs
+    // sized as a real run of that length would size them
+    auto timed = [&](const Layout& lay, int64_t steps, float* ms_out, int reps = 2,
+                     bool real_slabs = false) -> sdb_status {
         sdeb::RunArgs a = make_args(d, lay.lanes);
         a.state_in = d_init;
         a.params = d_params;
@@ -471,10 +485,10 @@ sdb_status choose_layout(sdb_ctx* ctx, Slot& s, const sdb_desc& d, const double*
         a.ksteps = steps;
         a.chunk_end = 1;
         float ms_best = 1e30f;
-        for (int rep = 0; rep < 2; ++rep) {
+        for (int rep = 0; rep < reps; ++rep) {
             sdb_status r2 = configure_layout(ctx, s, s.t_work, d, lay, steps, st, &a);
             if (r2 != SDB_OK) return r2;
-            if (a.persistent) a.slab_steps = std::max<int64_t>(16, p1 / 2);
+            if (a.persistent && !real_slabs) a.slab_steps = std::max<int64_t>(16, p1 / 2);
             cudaEventRecord(e0, st);
             cudaError_t e = launch_run(a, P / lay.lanes, kind_solver, kind_stream, d.coupling,
                                        kernel_variant(d, lay.tight), st);
@@ -489,7 +503,10 @@ sdb_status choose_layout(sdb_ctx* ctx, Slot& s, const sdb_desc& d, const double*
         *ms_out = ms_best;
         return SDB_OK;
     };
-    for (const Layout& lay : cands) {
+    // stage 1: every candidate on the short differential probe
+    std::vector<std::pair<float, size_t>> scores;
+    for (size_t ci = 0; ci < cands.size(); ++ci) {
+        const Layout& lay = cands[ci];
         float t1 = 0.f, t2 = 0.f;
         rc = timed(lay, p1, &t1);
         if (rc != SDB_OK) break;
@@ -499,9 +516,36 @@ sdb_status choose_layout(sdb_ctx* ctx, Slot& s, const sdb_desc& d, const double*
             if (rc != SDB_OK) break;
             score = t2 - t1;
         }
+        scores.emplace_back(score, ci);
+        if (trace_enabled())
+            std::fprintf(stderr, "[sdeb200] tune n=%d L=%d pers=%d ctas=%d tight=%d: %.4f ms/%lld steps\n",
+                         d.nequat, lay.lanes, lay.persistent, lay.ctas_per_sm, lay.tight, score,
+                         (long long)(p2 - p1 > 0 ? p2 - p1 : p1));
         if (score < best) {
             best = score;
             best_l = lay;
+        }
+    }
+    // stage 2: the four best re-timed on a long probe (1/8 of the run, up to
+    // 4096 steps, persistent slabs as the real run sizes them, best of 3):
+    // the short probe cannot resolve layouts a few percent apart
+    const int64_t p3 = std::min<int64_t>(total, std::min<int64_t>(4096, std::max<int64_t>(p2, total / 8)));
+    if (rc == SDB_OK && p3 > p2 && scores.size() > 1) {
+        std::sort(scores.begin(), scores.end());
+        float best3 = 1e30f;
+        for (size_t r = 0; r < scores.size() && r < 4; ++r) {
+            float t3 = 0.f;
+            rc = timed(cands[scores[r].second], p3, &t3, 3, true);
+            if (rc != SDB_OK) break;
+            if (trace_enabled()) {
+                const Layout& l = cands[scores[r].second];
+                std::fprintf(stderr, "[sdeb200] tune stage 2 L=%d pers=%d ctas=%d tight=%d: %.4f ms/%lld steps\n",
+                             l.lanes, l.persistent, l.ctas_per_sm, l.tight, t3, (long long)p3);
+            }
+            if (t3 < best3) {
+                best3 = t3;
+                best_l = cands[scores[r].second];
+            }
         }
     }
     cudaEventDestroy(e0);
@@ -603,17 +647,6 @@ sdb_status launch_device(sdb_ctx* ctx, Slot& s, const sdb_desc& d, sdb_model* m,
     s.ctas_per_sm = lay.ctas_per_sm;
     s.tight = lay.tight;
     return SDB_OK;
-}
-
-// One device's contiguous shard [r0, r0+rows) of a host-buffer run.
-// SDEB200_TRACE=1: per-phase wall-clock of host-buffer runs on stderr (adds
-// stream synchronisations between phases; for diagnosis only).
-bool trace_enabled() {
-    static const bool on = [] {
-        const char* e = std::getenv("SDEB200_TRACE");
-        return e && *e && *e != '0';
-    }();
-    return on;
 }
 
 double now_ms() {
