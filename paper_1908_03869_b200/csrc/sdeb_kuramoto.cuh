@@ -79,6 +79,25 @@ __device__ __forceinline__ double group_sum(double x, int lanes) {
     return x;
 }
 
+// Both coupling sums over the orbit's lanes, upper levels of the canonical
+// tree, as one unrolled butterfly with warp-uniform exits: a runtime-bounded
+// loop per sum cost ~9 issue slots per level (divergence checks, moves, loop
+// control) around its 2 SHFLs.
+__device__ __forceinline__ void xor_level(double& a, double& b, int o) {
+    const double pa = __shfl_xor_sync(0xffffffffu, a, o);
+    const double pb = __shfl_xor_sync(0xffffffffu, b, o);
+    a = __dadd_rn(a, pa);
+    b = __dadd_rn(b, pb);
+}
+
+__device__ __forceinline__ void group_sum2(double& a, double& b, int lanes) {
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        if (o >= lanes) break;  // warp-uniform exit
+        xor_level(a, b, o);
+    }
+}
+
 __device__ __forceinline__ int64_t group_fail(int64_t f, int lanes) {
     for (int o = 1; o < lanes; o <<= 1) {
         const long long other = __shfl_xor_sync(0xffffffffu, (long long)f, o);
@@ -109,8 +128,7 @@ __device__ __forceinline__ void meanfield_sums(const double (&y)[J], int base, i
     }
     double a = lane_tree_sum<J>(ts);
     double b = lane_tree_sum<J>(tc);
-    a = group_sum(a, lanes);
-    b = group_sum(b, lanes);
+    group_sum2(a, b, lanes);
 #pragma unroll
     for (int q = 0; q < J; ++q) {
         // two rounded products, not an FMA: the self term cos*sin - sin*cos
@@ -206,8 +224,8 @@ __device__ __forceinline__ void group_order_param(const double (&y)[J], int base
             cs[q] = 0.0;
         }
     }
-    const double ss = group_sum(lane_tree_sum<J>(sn), lanes);
-    const double sc = group_sum(lane_tree_sum<J>(cs), lanes);
+    double ss = lane_tree_sum<J>(sn), sc = lane_tree_sum<J>(cs);
+    group_sum2(ss, sc, lanes);
     order_param_from_sums(sc, ss, n, r, phi);
 }
 
