@@ -305,7 +305,8 @@ int smem_for_cap(int device, int cap) {
     int per_sm = 0;
     cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device);
     const int reserved = 1024;  // per-CTA reservation on sm_100
-    return std::max(0, per_sm / cap - reserved) & ~255;
+    // the stepper's static shared memory (staged math tables) is part of the budget
+    return std::max(0, per_sm / cap - reserved - int(sdeb::kTableSmemBytes)) & ~255;
 }
 
 // Kernel instantiation variant: 1 padded (n < next_pow2(n)), else 0, or 2

@@ -431,7 +431,8 @@ std::string program_source(const sdb_model* m, int kind, int lanes) {
     char head[360];
     std::snprintf(head, sizeof(head),
                   "#define SDB_N %d\n#define SDB_NP %d\n#define SDB_NN %d\n#define SDB_KIND %d\n"
-                  "#define SDB_LANES %d\n#define SDB_UNROLL %d\n#define SDB_GLOBAL_STATE %d\n",
+                  "#define SDB_LANES %d\n#define SDB_UNROLL %d\n#define SDB_GLOBAL_STATE %d\n"
+                  "#define SDEB_SMEM_TABLES 1\n",
                   m->nequat, m->nparams, m->nnoise, kind, lanes, unroll,
                   global_state(m, lanes) ? 1 : 0);
     return std::string("// generated by sdeb200 from expression templates\n") + head +
@@ -528,13 +529,14 @@ cudaError_t launch(sdb_model* m, int kind, const sdeb::DslArgs& a, cudaStream_t 
         }
     } else {
         smem = size_t(slots) * state_words(m) * sizeof(double);
-        if (smem > 48 * 1024) {
-            e = cudaFuncSetAttribute(reinterpret_cast<const void*>(k),
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-            if (e != cudaSuccess) {
-                *err = std::string("shared-memory opt-in: ") + cudaGetErrorString(e);
-                return e;
-            }
+    }
+    // the staged math tables are static shared memory on top of the columns
+    if (smem + kTableSmem > 48 * 1024) {
+        e = cudaFuncSetAttribute(reinterpret_cast<const void*>(k),
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        if (e != cudaSuccess) {
+            *err = std::string("shared-memory opt-in: ") + cudaGetErrorString(e);
+            return e;
         }
     }
     const dim3 grid(unsigned((a.rows + slots - 1) / slots)), block(kBlock);

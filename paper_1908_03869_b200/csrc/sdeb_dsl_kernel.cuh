@@ -334,6 +334,7 @@ extern "C" __global__ void __launch_bounds__(128) sdb_dsl_main(const sdeb::DslAr
     using namespace sdeb;
     extern __shared__ double dsl_smem[];
     constexpr int kSlots = 128 / kL;
+    stage_tables();  // sincos / log tables into shared memory (SDEB_SMEM_TABLES)
     const int lane = int(threadIdx.x) % kL;
     const int slot = int(threadIdx.x) / kL;
     const int64_t orbit = int64_t(blockIdx.x) * kSlots + slot;

@@ -463,10 +463,14 @@ __device__ __forceinline__ void run_item(const RunArgs& a, int64_t cg, uint64_t 
             bool bad = false;
 #pragma unroll
             for (int q = 0; q < J; ++q) bad |= !finite_bits(y[q]);
-            if (bad && a.check_finite) {
-                if (fail < 0) fail = int64_t(step);
+            // a warp vote keeps the (rare) NaN fill out of the issue stream:
+            // as predicated code it cost ~11 slots every step
+            if (__any_sync(0xffffffffu, bad)) {
+                if (bad && a.check_finite) {
+                    if (fail < 0) fail = int64_t(step);
 #pragma unroll
-                for (int q = 0; q < J; ++q) y[q] = CUDART_NAN;
+                    for (int q = 0; q < J; ++q) y[q] = CUDART_NAN;
+                }
             }
             }
             if (step == next_sample) {
@@ -554,6 +558,7 @@ __global__ void __launch_bounds__(kBlock, (VAR == 2 ? tight_minb<J>() : 0))
     kuramoto_run_kernel(const RunArgs a) {
     constexpr bool PADDED = (VAR & 1) != 0;
     constexpr bool COH = VAR >= kVarCoherence;
+    stage_tables();
     extern __shared__ double smem[];
     double* sh = smem;                  // pairwise: [J][kBlock]
     double* shs = smem + J * kBlock;    // pairwise L==1: [J][kBlock]

@@ -12,7 +12,9 @@ static cudaError_t launch_one(const RunArgs& a, cudaStream_t st) {
                                            : unsigned((threads + kBlock - 1) / kBlock);
     const size_t need = pairwise_smem_bytes(J, C);
     const size_t smem = need > size_t(a.smem_pad) ? need : size_t(a.smem_pad);
-    if (smem > 48 * 1024) {
+    // static shared memory (the staged math tables) counts against the 48 KB
+    // default too: opt in whenever the sum exceeds it
+    if (smem + kStaticSmemBytes > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(kuramoto_run_kernel<J, S, R, C, P>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              int(smem));
@@ -26,7 +28,7 @@ template <int J, int S, int R, int C, int P>
 static cudaError_t occupancy_one(size_t smem, int* blocks) {
     const size_t need = pairwise_smem_bytes(J, C);
     if (smem < need) smem = need;
-    if (smem > 48 * 1024) {
+    if (smem + kStaticSmemBytes > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(kuramoto_run_kernel<J, S, R, C, P>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              int(smem));

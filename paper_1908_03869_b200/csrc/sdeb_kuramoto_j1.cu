@@ -1,4 +1,6 @@
 // Instantiates the fused stepper for J = 1 oscillators per lane.
+// the stepper reads the sincos / log tables from shared memory (sdeb_math.cuh)
+#define SDEB_SMEM_TABLES 1
 #include "sdeb_kuramoto_inst.cuh"
 
 namespace sdeb {

@@ -63,6 +63,40 @@ __constant__ static double kMC[MC_COUNT] = {  // non-const: keeps ptxas from fol
     0.041666666666666664,                        // 1/24
 };
 
+// Table reads.  Translation units that define SDEB_SMEM_TABLES (the fused
+// stepper's) stage both tables in static shared memory at kernel start
+// (stage_tables()) and read them with LDS: a 32-bit address from the index in
+// two integer ops instead of four for the 64-bit global address, and no L1 tag
+// traffic.  Everything else reads the global copies through the read-only path.
+constexpr size_t kTableSmemBytes = 16 * (kSinCosN + (1 << kLogTableBits));  // both, staged
+#ifdef SDEB_SMEM_TABLES
+__shared__ double2 s_sincos_tab[kSinCosN];
+__shared__ double2 s_log_tab[1 << kLogTableBits];
+
+// Cooperative copy of both tables into shared memory; every thread of the CTA
+// must call it (it ends with a barrier).
+__device__ __forceinline__ void stage_tables() {
+    const double2* gs = reinterpret_cast<const double2*>(kSinCosTable);
+    const double2* gl = reinterpret_cast<const double2*>(kLogTable);
+    for (int i = threadIdx.x; i < kSinCosN; i += blockDim.x) s_sincos_tab[i] = __ldg(gs + i);
+    for (int i = threadIdx.x; i < (1 << kLogTableBits); i += blockDim.x) s_log_tab[i] = __ldg(gl + i);
+    __syncthreads();
+}
+
+__device__ __forceinline__ double2 sincos_entry(int k) { return s_sincos_tab[k & (kSinCosN - 1)]; }
+constexpr size_t kStaticSmemBytes = kTableSmemBytes;
+__device__ __forceinline__ double2 log_entry(int i) { return s_log_tab[i]; }
+#else
+constexpr size_t kStaticSmemBytes = 0;
+__device__ __forceinline__ void stage_tables() {}
+__device__ __forceinline__ double2 sincos_entry(int k) {
+    return __ldg(reinterpret_cast<const double2*>(kSinCosTable[k & (kSinCosN - 1)]));
+}
+__device__ __forceinline__ double2 log_entry(int i) {
+    return __ldg(reinterpret_cast<const double2*>(kLogTable[i]));
+}
+#endif
+
 constexpr double kRoundMagic = 6755399441055744.0;  // 1.5 * 2^52
 constexpr double kSmallArg = 536870912.0;           // 2^29: fast reduction bound
 
@@ -126,7 +160,7 @@ __device__ __forceinline__ void sincos_tab(double x, double& s, double& c) {
     double r = __fma_rn(-kd, kMC[MC_PITAB_1], x);
     r = __fma_rn(-kd, kMC[MC_PITAB_2], r);
     r = __fma_rn(-kd, kMC[MC_PITAB_3], r);
-    const double2 e = __ldg(reinterpret_cast<const double2*>(kSinCosTable[k & (kSinCosN - 1)]));
+    const double2 e = sincos_entry(k);
     const double r2 = __dmul_rn(r, r);
     const double ps = __fma_rn(r2, kMC[MC_T_S5], kMC[MC_T_S3]);
     const double sr = __fma_rn(__dmul_rn(r2, r), ps, r);             // sin r
@@ -182,7 +216,7 @@ __device__ __forceinline__ double log_pos(double x) {
     const int i = int((tmp >> (52 - kLogTableBits)) & ((1u << kLogTableBits) - 1));
     const int64_t k = int64_t(tmp) >> 52;
     const double z = __longlong_as_double((long long)(ix - (tmp & (0xFFFull << 52))));
-    const double2 e = __ldg(reinterpret_cast<const double2*>(kLogTable[i]));  // (invc, logc)
+    const double2 e = log_entry(i);  // (invc, logc)
     const double r = __fma_rn(z, e.x, -1.0);
     const double kd = __dsub_rn(__longlong_as_double((long long)(0x4338000000000000ll + k)),
                                 kRoundMagic);
