@@ -390,6 +390,12 @@ int state_words(const sdb_model* m) {
     return m->nequat + (m->nnoise > 0 ? 4 * nb : 0);
 }
 
+// Stage the sincos / log tables in shared memory unless the templates carry
+// sums: there the O(N^2) table reads per step compete with the state-column
+// reads for the shared-memory pipe (measured: Kuramoto templates 2.44e9 ->
+// 1.53e9 orbit-steps/s staged; the OU template 1.94e10 -> 2.26e10).
+bool stage_tables(const sdb_model* m) { return !m->uses_sum; }
+
 int lanes_for(const sdb_model* m) {
     if (const char* e = std::getenv("SDEB200_DSL_LANES")) {
         const int v = std::atoi(e);
@@ -431,10 +437,10 @@ std::string program_source(const sdb_model* m, int kind, int lanes) {
     char head[360];
     std::snprintf(head, sizeof(head),
                   "#define SDB_N %d\n#define SDB_NP %d\n#define SDB_NN %d\n#define SDB_KIND %d\n"
-                  "#define SDB_LANES %d\n#define SDB_UNROLL %d\n#define SDB_GLOBAL_STATE %d\n"
-                  "#define SDEB_SMEM_TABLES 1\n",
+                  "#define SDB_LANES %d\n#define SDB_UNROLL %d\n#define SDB_GLOBAL_STATE %d\n%s",
                   m->nequat, m->nparams, m->nnoise, kind, lanes, unroll,
-                  global_state(m, lanes) ? 1 : 0);
+                  global_state(m, lanes) ? 1 : 0,
+                  stage_tables(m) ? "#define SDEB_SMEM_TABLES 1\n" : "");
     return std::string("// generated by sdeb200 from expression templates\n") + head +
            "#include \"sdeb_dsl_kernel.cuh\"\n\n// drift: " + m->drift_text + "\n" + m->drift_cu +
            "\n// diffusion: " + m->diffusion_text + "\n" + m->diffusion_cu;
@@ -531,7 +537,7 @@ cudaError_t launch(sdb_model* m, int kind, const sdeb::DslArgs& a, cudaStream_t 
         smem = size_t(slots) * state_words(m) * sizeof(double);
     }
     // the staged math tables are static shared memory on top of the columns
-    if (smem + kTableSmem > 48 * 1024) {
+    if (smem + (stage_tables(m) ? kTableSmem : 0) > 48 * 1024) {
         e = cudaFuncSetAttribute(reinterpret_cast<const void*>(k),
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
         if (e != cudaSuccess) {

@@ -64,6 +64,8 @@ int state_words(const sdb_model* m);
 // with sums (O(N) work per equation), ~16 without, or SDEB200_DSL_LANES.
 // Results do not depend on it.
 int lanes_for(const sdb_model* m);
+// True when the program stages the math tables in shared memory.
+bool stage_tables(const sdb_model* m);
 // True when the columns go to global scratch instead of shared memory.
 bool global_state(const sdb_model* m, int lanes);
 // Doubles of global scratch a launch over `rows` orbits needs (0 = none).
