@@ -91,7 +91,7 @@ TEMPLATES = {
 
 SINCOS_OPS = 15      # csrc/sdeb_math.cuh sincos_tab: 5 reduction + 6 poly + 4 rotation
 SIN_OPS = 13         # the same when only sin is used (the cos rotation is dead code)
-BOX_MULLER_PAIR = 42  # 2 uniforms, log 13, -2*log 1, sqrt 8, angle 1, sincos 15, 2 products
+BOX_MULLER_PAIR = 37  # uniform 1, log 13, -2*log 1, sqrt 8, angle from the word 2, sincos poly+rotation 10, 2 products
 
 
 def template_fp64_ops(n: int, model: str) -> float:

@@ -162,7 +162,8 @@ sdb_status sdb_fp64_peak(sdb_ctx* ctx, double* ops_per_s, double* ms);
 
 /* Evaluate one of the stepper's device math routines element-wise (accuracy
  * tests): func 0 = sin, 1 = cos (the stepper's sincos), 2 = log (Box-Muller
- * radius), 3 = sqrt, 4 = sin / 5 = cos / 6 = log of libdevice for comparison. */
+ * radius), 3 = sqrt, 4 = sin / 5 = cos / 6 = log of libdevice for comparison,
+ * 7 = sin / 8 = cos of the Box-Muller angle 2*pi*(w+1)*2^-32 with x = the word w. */
 sdb_status sdb_math_probe(sdb_ctx* ctx, int32_t func, const double* x, int64_t count,
                           double* out);
 

@@ -487,7 +487,9 @@ sdb_status choose_layout(sdb_ctx* ctx, Slot& s, const sdb_desc& d, const double*
         a.chunk_end = 1;
         float ms_best = 1e30f;
         for (int rep = 0; rep < reps; ++rep) {
-            sdb_status r2 = configure_layout(ctx, s, s.t_work, d, lay, steps, st, &a);
+            // real_slabs: persistent slabs sized for the whole run, as it will run
+            sdb_status r2 = configure_layout(ctx, s, s.t_work, d, lay, real_slabs ? total : steps,
+                                             st, &a);
             if (r2 != SDB_OK) return r2;
             if (a.persistent && !real_slabs) a.slab_steps = std::max<int64_t>(16, p1 / 2);
             cudaEventRecord(e0, st);
@@ -527,12 +529,23 @@ sdb_status choose_layout(sdb_ctx* ctx, Slot& s, const sdb_desc& d, const double*
             best_l = lay;
         }
     }
-    // stage 2: the four best re-timed on a long probe (1/8 of the run, up to
-    // 4096 steps, persistent slabs as the real run sizes them, best of 3):
-    // the short probe cannot resolve layouts a few percent apart
-    const int64_t p3 = std::min<int64_t>(total, std::min<int64_t>(4096, std::max<int64_t>(p2, total / 8)));
+    // stage 2: the four best re-timed on a long probe (>= 1/8 of the run and
+    // >= 4 of the run's persistent slabs, persistent slabs sized as in the real
+    // run, best of 3): the short probe cannot resolve layouts a few percent
+    // apart, and with short slabs it over-charges the persistent hand-offs
+    std::sort(scores.begin(), scores.end());
+    int64_t longest_slab = 0;  // the probe must span several real slabs
+    for (size_t r = 0; r < scores.size() && r < 4; ++r) {
+        const Layout& l = cands[scores[r].second];
+        if (!l.persistent) continue;
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s.device);
+        longest_slab = std::max(longest_slab, slab_steps_for(total, cta_groups(d, l.lanes),
+                                                             int64_t(sms) * l.ctas_per_sm));
+    }
+    const int64_t p3 = std::min<int64_t>(
+        total, std::max<int64_t>({p2, total / 8, std::min<int64_t>(4 * longest_slab, 8192)}));
     if (rc == SDB_OK && p3 > p2 && scores.size() > 1) {
-        std::sort(scores.begin(), scores.end());
         float best3 = 1e30f;
         for (size_t r = 0; r < scores.size() && r < 4; ++r) {
             float t3 = 0.f;
@@ -1519,7 +1532,7 @@ sdb_status sdb_math_probe(sdb_ctx* ctx, int32_t func, const double* x, int64_t c
                           double* out) {
     sdb_status rc = utility_prologue(ctx);
     if (rc != SDB_OK) return rc;
-    if (func < 0 || func > 6) return fail_with(ctx, SDB_ERR_ARGUMENT, "unknown math probe %d", func);
+    if (func < 0 || func > 8) return fail_with(ctx, SDB_ERR_ARGUMENT, "unknown math probe %d", func);
     if (count <= 0) return SDB_OK;
     TmpBuf dx, dout;
     SDB_CUDA(ctx, cudaMalloc(&dx.p, size_t(count) * sizeof(double)));

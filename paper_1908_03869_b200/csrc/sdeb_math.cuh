@@ -39,6 +39,7 @@ enum MathConst : int {
     MC_LN2_HI, MC_LN2_LO, MC_U32_BIAS, MC_INV7, MC_NEG_INV6, MC_INV5, MC_INV3,
     MC_TAB_OVER_PI, MC_PITAB_1, MC_PITAB_2, MC_PITAB_3,  // table sincos reduction (pi/512)
     MC_T_S3, MC_T_S5, MC_T_C4,                           // Taylor terms on |r| <= pi/1024
+    MC_TURN_BIAS, MC_TWO_PI_2M32,                        // Box-Muller angle (sincos_turn)
     MC_COUNT
 };
 
@@ -61,6 +62,8 @@ __constant__ static double kMC[MC_COUNT] = {  // non-const: keeps ptxas from fol
     -5.849159784606132e-36,      // next 53 bits * 2^-9
     -0.16666666666666666, 0.008333333333333333,  // -1/6, 1/120
     0.041666666666666664,                        // 1/24
+    4503601774854144.0,                          // 2^52 + 2^31 (biased int -> double)
+    1.4629180792671596e-09,                      // fl(2 pi) * 2^-32 (exact scaling)
 };
 
 // Table reads.  Translation units that define SDEB_SMEM_TABLES (the fused
@@ -168,6 +171,30 @@ __device__ __forceinline__ void sincos_tab(double x, double& s, double& c) {
     const double cr = __fma_rn(r2, pc, 1.0);                         // cos r
     s = __fma_rn(e.x, cr, __dmul_rn(e.y, sr));                       // sin(a + r)
     c = __fma_rn(e.y, cr, -__dmul_rn(e.x, sr));                      // cos(a + r)
+}
+
+// sin / cos of the Box-Muller angle 2*pi*u, u = (w + 1) * 2^-32 (rng.py:183-187),
+// reduced in integer arithmetic: v = w + 1 = k*2^22 + m with |m| <= 2^21, so
+// 2*pi*u = k*pi/512 + m*(2*pi*2^-32): the table entry k & 1023 and a residual
+// r = m * fl(2 pi) * 2^-32 with one rounding (|r| <= pi/1024).  2 FP64 ops
+// replace the uniform conversion, the angle product and the 5-op reduction.
+// Differs from sin/cos(fl(2*pi*u)) by <= ~1 ulp of the angle (the reference
+// rounds the angle first; this evaluates the exact one).
+__device__ __forceinline__ void sincos_turn(uint32_t w, double& s, double& c) {
+    const uint64_t v = uint64_t(w) + 1u;
+    const uint32_t k = uint32_t((v + (1u << 21)) >> 22);            // 0 .. 1024
+    const int m = int(int64_t(v) - (int64_t(k) << 22));             // -2^21 .. 2^21
+    const double md = __dsub_rn(__hiloint2double(0x43300000, int(uint32_t(m) ^ 0x80000000u)),
+                                kMC[MC_TURN_BIAS]);                 // exact
+    const double r = __dmul_rn(md, kMC[MC_TWO_PI_2M32]);
+    const double2 e = sincos_entry(int(k));
+    const double r2 = __dmul_rn(r, r);
+    const double ps = __fma_rn(r2, kMC[MC_T_S5], kMC[MC_T_S3]);
+    const double sr = __fma_rn(__dmul_rn(r2, r), ps, r);
+    const double pc = __fma_rn(r2, kMC[MC_T_C4], -0.5);
+    const double cr = __fma_rn(r2, pc, 1.0);
+    s = __fma_rn(e.x, cr, __dmul_rn(e.y, sr));
+    c = __fma_rn(e.y, cr, -__dmul_rn(e.x, sr));
 }
 
 // The stepper's sincos for |x| < 2^29 (NaN/inf propagate to NaN).

@@ -150,6 +150,9 @@ __global__ void math_probe_kernel(int func, const double* __restrict__ x, int64_
         case 4: r = sin(v); break;
         case 5: r = cos(v); break;
         case 6: r = log(v); break;
+        // Box-Muller angle: x carries the 32-bit word w (exactly, as a double)
+        case 7: sincos_turn(uint32_t(v), s, c); r = s; break;
+        case 8: sincos_turn(uint32_t(v), s, c); r = c; break;
         default: r = CUDART_NAN;
     }
     out[i] = r;

@@ -48,15 +48,14 @@ __host__ __device__ __forceinline__ Words4 philox4x32_10(uint32_t c0, uint32_t c
 // to_uniform (rng.py:121-129): (w + 1.0) * 2^-32, exact in double.
 __device__ __forceinline__ double to_uniform(uint32_t w) { return u32_to_uniform(w); }
 
-// One Box-Muller pair with the reference's operation order (rng.py:179-187):
-// r = sqrt(-2 ln u_a); ang = TWO_PI * u_b; (r cos ang, r sin ang).
-// ang is in (0, 2pi], so the small-argument sincos needs no fallback.
+// One Box-Muller pair in the reference's form (rng.py:179-187):
+// r = sqrt(-2 ln u_a); (r cos(2 pi u_b), r sin(2 pi u_b)).  The angle's sincos
+// is reduced in integer arithmetic from the word itself (sincos_turn).
 __device__ __forceinline__ void box_muller_pair(uint32_t wa, uint32_t wb, double& z0, double& z1) {
-    const double ua = u32_to_uniform(wa), ub = u32_to_uniform(wb);
+    const double ua = u32_to_uniform(wa);
     const double r = sqrt_nonneg(__dmul_rn(-2.0, log_pos(ua)));
-    const double ang = __dmul_rn(kTwoPi, ub);
     double s, c;
-    sincos_small(ang, s, c);
+    sincos_turn(wb, s, c);
     z0 = __dmul_rn(r, c);
     z1 = __dmul_rn(r, s);
 }

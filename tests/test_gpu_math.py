@@ -79,3 +79,18 @@ def test_libdevice_probe_matches_numpy_closely():
     g = np.random.default_rng(4)
     x = g.uniform(-100, 100, 10000)
     assert ulp_err(probe(4, x), np.sin(x)).max() <= 2
+
+
+def test_box_muller_angle_sincos():
+    # sin / cos(2 pi u), u = (w + 1) 2^-32, reduced from the word (sincos_turn)
+    g = np.random.default_rng(5)
+    w = np.concatenate([g.integers(0, 2 ** 32, 20000), np.arange(0, 3000),
+                        2 ** 32 - 1 - np.arange(0, 3000), (np.arange(-3, 4) + 2 ** 31),
+                        np.arange(1025) * 2 ** 22 - 1]).astype(np.uint64)
+    w = w[w < 2 ** 32].astype(np.float64)
+    ang = 2.0 * np.pi * ((w + 1.0) * 2.0 ** -32)
+    s, c = probe(7, w), probe(8, w)
+    # vs the reference's sin(fl(2 pi u)): the exact angle differs from the rounded
+    # one by <= 0.5 ulp(angle) <= 4.5e-16
+    assert np.abs(s - np.sin(ang)).max() <= 8e-16
+    assert np.abs(c - np.cos(ang)).max() <= 8e-16

@@ -186,3 +186,33 @@ def test_emulated_table_sincos_within_2ulp_and_odd():
         assert ulps(c, math.cos(x)) <= 2 or abs(c - math.cos(x)) <= 2.3e-16, x
         ns, nc = emu_sincos_tab(-float(x))
         assert ns == -s and nc == c, x
+
+
+def emu_sincos_turn(w):
+    v = w + 1
+    k = (v + 2 ** 21) >> 22
+    m = v - (k << 22)
+    md = float(m)
+    r = md * C["MC_TWO_PI_2M32"]
+    sa, ca = SCT[k & (len(SCT) - 1)]
+    r2 = r * r
+    ps = fma(r2, C["MC_T_S5"], C["MC_T_S3"])
+    sr = fma(r2 * r, ps, r)
+    pc = fma(r2, C["MC_T_C4"], -0.5)
+    cr = fma(r2, pc, 1.0)
+    return fma(sa, cr, ca * sr), fma(ca, cr, -(sa * sr))
+
+
+def test_box_muller_angle_reduction():
+    assert C["MC_TWO_PI_2M32"] == 2.0 * math.pi * 2.0 ** -32
+    assert C["MC_TURN_BIAS"] == 2.0 ** 52 + 2.0 ** 31
+    g = np.random.default_rng(11)
+    ws = [int(x) for x in g.integers(0, 2 ** 32, 3000)] + list(range(300)) + \
+        [2 ** 32 - 1 - j for j in range(300)] + [k * 2 ** 22 + d for k in range(0, 1024, 37)
+                                                for d in (-1, 0, 1, 2 ** 21 - 1, 2 ** 21)]
+    for w in ws:
+        if not 0 <= w < 2 ** 32:
+            continue
+        ang = 2.0 * math.pi * ((w + 1.0) * 2.0 ** -32)
+        s, c = emu_sincos_turn(w)
+        assert abs(s - math.sin(ang)) <= 8e-16 and abs(c - math.cos(ang)) <= 8e-16, w
