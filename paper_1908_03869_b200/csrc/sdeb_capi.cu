@@ -18,6 +18,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <mutex>
 #include <string>
 #include <thread>
 #include <tuple>
@@ -141,6 +142,7 @@ struct sdb_ctx {
     int32_t last_tight = 0;
     int32_t last_tiles = 0;
     std::map<TuneKey, Layout> tune;
+    std::mutex mu;  // guards tune and error: shard threads of one run share the context
 };
 
 namespace {
@@ -151,7 +153,10 @@ sdb_status fail_with(sdb_ctx* ctx, sdb_status st, const char* fmt, ...) {
     va_start(ap, fmt);
     vsnprintf(buf, sizeof(buf), fmt, ap);
     va_end(ap);
-    if (ctx) ctx->error = buf;
+    if (ctx) {
+        std::lock_guard<std::mutex> lock(ctx->mu);
+        ctx->error = buf;
+    }
     g_thread_error = buf;
     return st;
 }
@@ -423,10 +428,13 @@ sdb_status choose_layout(sdb_ctx* ctx, Slot& s, const sdb_desc& d, const double*
     const int64_t total = d.chunks * d.ksteps;
     const TuneKey key{s.device, d.nequat, kind_solver, kind_stream, d.coupling, d.orbits,
                       int(std::min<int64_t>(total, 1 << 20)), d.lanes};
-    auto it = ctx->tune.find(key);
-    if (it != ctx->tune.end()) {
-        *out = it->second;
-        return SDB_OK;
+    {
+        std::lock_guard<std::mutex> lock(ctx->mu);
+        auto it = ctx->tune.find(key);
+        if (it != ctx->tune.end()) {
+            *out = it->second;
+            return SDB_OK;
+        }
     }
     // SDEB200_LAYOUT="lanes,persistent,ctas_per_sm[,tight]" pins the layout
     // (profiling runs must not capture autotune probes); ctas_per_sm 0 =
@@ -440,7 +448,10 @@ sdb_status choose_layout(sdb_ctx* ctx, Slot& s, const sdb_desc& d, const double*
                                         kernel_variant(d, tight), 0, &occ));
             Layout lay{L, pers, (cap > 0 && !pers) ? smem_for_cap(s.device, cap) : 0,
                        cap > 0 ? cap : occ, tight};
-            ctx->tune[key] = lay;
+            {
+                std::lock_guard<std::mutex> lock(ctx->mu);
+                ctx->tune[key] = lay;
+            }
             *out = lay;
             return SDB_OK;
         }
@@ -451,7 +462,10 @@ sdb_status choose_layout(sdb_ctx* ctx, Slot& s, const sdb_desc& d, const double*
     if (cands.empty()) return fail_with(ctx, SDB_ERR_CUDA, "no launchable layout for n=%d", d.nequat);
     if (cands.size() == 1) {
         *out = cands[0];
-        ctx->tune[key] = cands[0];
+        {
+            std::lock_guard<std::mutex> lock(ctx->mu);
+            ctx->tune[key] = cands[0];
+        }
         return SDB_OK;
     }
     // Differential probe: time P1 and P2 = 2*P1 steps and rank layouts by
@@ -565,7 +579,10 @@ sdb_status choose_layout(sdb_ctx* ctx, Slot& s, const sdb_desc& d, const double*
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     if (rc != SDB_OK) return rc;
-    ctx->tune[key] = best_l;
+    {
+        std::lock_guard<std::mutex> lock(ctx->mu);
+        ctx->tune[key] = best_l;
+    }
     *out = best_l;
     return SDB_OK;
 }
