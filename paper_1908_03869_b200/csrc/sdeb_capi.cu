@@ -18,6 +18,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <condition_variable>
+#include <functional>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -691,7 +693,70 @@ int env_int(const char* name, int dflt) {
     return (e && *e) ? std::atoi(e) : dflt;
 }
 
-// Host copy of rows [0, rows) split over `threads` std::threads (the calling
+// Persistent host workers for the pipeline's copies (spawning a std::thread
+// per piece cost ~50 us each, ~0.8 ms per 16-way copy).  Jobs are ranges of
+// one parallel_rows call; the caller runs a share itself and waits.
+class CopyPool {
+  public:
+    static CopyPool& get() {
+        static CopyPool pool;
+        return pool;
+    }
+    // run fn(t) for t in [1, n) on the workers and fn(0) here; returns when all done
+    template <class F>
+    void run(int n, F& fn) {
+        // one job at a time: shard threads of a multi-device run take turns
+        std::lock_guard<std::mutex> serial(run_mu_);
+        std::unique_lock<std::mutex> lock(mu_);
+        while (workers_.size() < size_t(n - 1)) workers_.emplace_back([this] { loop(); });
+        job_ = [&fn](int t) { fn(t); };
+        pending_ = n - 1;
+        next_ = 1;
+        total_ = n;
+        ++generation_;
+        lock.unlock();
+        cv_.notify_all();
+        fn(0);
+        lock.lock();
+        done_cv_.wait(lock, [this] { return pending_ == 0; });
+        job_ = nullptr;
+    }
+
+  private:
+    CopyPool() = default;
+    ~CopyPool() {
+        {
+            std::lock_guard<std::mutex> lock(mu_);
+            stop_ = true;
+        }
+        cv_.notify_all();
+        for (auto& w : workers_) w.join();
+    }
+    void loop() {
+        uint64_t seen = 0;
+        for (;;) {
+            std::unique_lock<std::mutex> lock(mu_);
+            cv_.wait(lock, [&] { return stop_ || (generation_ != seen && next_ < total_); });
+            if (stop_) return;
+            const int t = next_++;
+            if (next_ >= total_) seen = generation_;
+            auto job = job_;
+            lock.unlock();
+            job(t);
+            lock.lock();
+            if (--pending_ == 0) done_cv_.notify_one();
+        }
+    }
+    std::mutex run_mu_, mu_;
+    std::condition_variable cv_, done_cv_;
+    std::vector<std::thread> workers_;
+    std::function<void(int)> job_;
+    int pending_ = 0, next_ = 0, total_ = 0;
+    uint64_t generation_ = 0;
+    bool stop_ = false;
+};
+
+// Host copy of rows [0, rows) split over up to `threads` workers (the calling
 // thread takes the first range).  Pageable numpy destinations fault their
 // pages in on first touch; spreading the copy spreads the faults too.
 template <class F>
@@ -702,12 +767,8 @@ void parallel_rows(int64_t rows, size_t bytes, int threads, F&& fn) {
         fn(int64_t(0), rows);
         return;
     }
-    std::vector<std::thread> pool;
-    pool.reserve(nt - 1);
-    for (int t = 1; t < nt; ++t)
-        pool.emplace_back([&, t] { fn(rows * t / nt, rows * (t + 1) / nt); });
-    fn(int64_t(0), rows / nt);
-    for (auto& th : pool) th.join();
+    auto part = [&](int t) { fn(rows * t / nt, rows * (t + 1) / nt); };
+    CopyPool::get().run(nt, part);
 }
 
 int host_copy_threads(int shards) {
