@@ -64,6 +64,18 @@ WORKLOADS = {
     "cfg5": dict(n=32, orbits=131072, dt=1e-3, steps=1000, ksteps=10, stream="philox",
                  solver="em", batch="resample",
                  desc="n=32, 512 parameter sets x 256 realisations, trajectory every 10 steps"),
+    # the paper's own speed protocol: K = 1, omega ~ U[0.01, 0.03],
+    # p ~ U[0.001, 0.003], dt = 0.05, 400 s = 8000 steps, FP64, largest M = 163,840 orbits;
+    # BASELINE.md section 2 lists SODECL's published times (P100, 2x Xeon Gold 6142, ...)
+    "paper_n5": dict(n=5, orbits=163840, dt=0.05, steps=8000, ksteps=8000, stream="philox",
+                     solver="em", batch="speed", published=163840 * 8000 / 4.719,
+                     desc="paper protocol N=5, M=163,840, dt=0.05, 8000 steps (P100: 4.719 s)"),
+    "paper_n10": dict(n=10, orbits=163840, dt=0.05, steps=8000, ksteps=8000, stream="philox",
+                      solver="em", batch="speed", published=163840 * 8000 / 9.315,
+                      desc="paper protocol N=10, M=163,840, dt=0.05, 8000 steps (P100: 9.315 s)"),
+    "paper_n15": dict(n=15, orbits=163840, dt=0.05, steps=8000, ksteps=8000, stream="philox",
+                      solver="em", batch="speed", published=163840 * 8000 / 17.656,
+                      desc="paper protocol N=15, M=163,840, dt=0.05, 8000 steps (P100: 17.656 s)"),
     # run_batch fused with coherence_series: only (r, Phi) per sample leaves
     # the GPU; the e2e line includes the D2H of that instead of the 3.2 GiB store
     "cfg5_coherence": dict(n=32, orbits=131072, dt=1e-3, steps=1000, ksteps=10, stream="philox",
@@ -490,7 +502,11 @@ def run_ours(args, w, world, rank, local, dist):
         line = {
             "metric": "orbit-steps/s", "value": value, "unit": "orbit-steps/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "weak",
+            # only the paper-protocol workloads have a published number (SODECL on a
+            # P100); cfg2 has none
+            "vs_baseline": (value / w["published"]) if w.get("published") else None,
+            "dtype": "f64",
             "data": "synthetic (device-sampled Kuramoto batch, reference sampler bit-exact)",
             "config": {"workload": args.workload, "desc": w["desc"], "n": n,
                        "orbits_per_gpu": m, "sde_steps": steps, "ksteps": w["ksteps"],
