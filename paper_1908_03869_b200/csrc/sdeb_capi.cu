@@ -771,11 +771,12 @@ void parallel_rows(int64_t rows, size_t bytes, int threads, F&& fn) {
     CopyPool::get().run(nt, part);
 }
 
-int host_copy_threads(int shards) {
+int host_copy_threads(int /*shards*/) {
     const int hw = int(std::max(1u, std::thread::hardware_concurrency()));
-    // every hardware thread: the copies are bound by page faults / memory traffic
-    // (cfg3 n=256 e2e 393 -> 303 ms going from 8 to 16 threads on a 16-thread host)
-    return std::max(1, env_int("SDEB200_HOST_THREADS", std::min(32, hw / std::max(1, shards))));
+    // every hardware thread, whatever the shard count: the copies are bound by
+    // page faults / memory traffic (cfg3 n=256 e2e 393 -> 303 ms going from 8 to
+    // 16 threads on a 16-thread host), and the pool runs one piece at a time
+    return std::max(1, env_int("SDEB200_HOST_THREADS", std::min(32, hw)));
 }
 
 // Orbit tiles of a host-buffer shard: copies of tile t+1 / t-1 overlap the
