@@ -106,14 +106,20 @@ SIN_OPS = 13         # the same when only sin is used (the cos rotation is dead 
 BOX_MULLER_PAIR = 37  # uniform 1, log 13, -2*log 1, sqrt 8, angle from the word 2, sincos poly+rotation 10, 2 products
 
 
-def template_fp64_ops(n: int, model: str) -> float:
+def template_fp64_ops(n: int, model: str, coupling: str = "meanfield") -> float:
     """FP64 lane-ops per orbit-step of the generated program (counted from the
-    generated code): Kuramoto template n^2 terms x (difference 1, sin 13, sum
-    1) + per equation (p[0]/N, *, + 3; diffusion product 1; noise 21; update
-    4); OU per equation drift 2 + diffusion 1 + noise 21 + update 4."""
+    generated code).  Kuramoto templates, literal form (coupling="pairwise"):
+    n^2 terms x (difference 1, sin 13, sum 1); factored form (meanfield): one
+    sincos 15 + 2 sum adds per oscillator in the prologue (its (sin, cos)
+    kept for the equations), then per equation the addition formula 3.  Both: per equation p[0]/N, *, + 3,
+    diffusion product 1, noise 18.5, update 4.  OU per equation drift 2 +
+    diffusion 1 + noise 18.5 + update 4."""
+    tail = 1 + BOX_MULLER_PAIR / 2 + 4
     if model == "kuramoto_template":
-        return n * n * (1 + SIN_OPS + 1) + n * (3 + 1 + BOX_MULLER_PAIR / 2 + 4)
-    return n * (2 + 1 + BOX_MULLER_PAIR / 2 + 4)
+        if coupling == "meanfield":
+            return n * (SINCOS_OPS + 2) + n * (3 + 3 + tail)
+        return n * n * (1 + SIN_OPS + 1) + n * (3 + tail)
+    return n * (2 + tail)
 
 
 def algorithmic_fp64_ops(n: int, solver: str, coupling: str) -> float:
@@ -480,7 +486,7 @@ def run_ours(args, w, world, rank, local, dist):
 
     # --- roofline (FP64 pipe) ---
     peak_ops = ctypes_peak(lib, ctx)
-    ops = (template_fp64_ops(n, w["model"]) if "model" in w
+    ops = (template_fp64_ops(n, w["model"], args.coupling) if "model" in w
            else algorithmic_fp64_ops(n, w["solver"], args.coupling))
     achieved = ops * orbit_steps / (np.mean(kernel_ms) * 1e-3)
     roofline = {

@@ -221,7 +221,11 @@ sdb_status sdb_order_parameter(sdb_ctx* ctx, int32_t n, int64_t rows, const doub
 sdb_status sdb_model_create(int32_t nequat, int32_t nparams, int32_t nnoise, const char* drift,
                             const char* diffusion, sdb_model** out);
 void sdb_model_free(sdb_model* model);
-/* Generated CUDA source of program `kind` (0..9, see sdeb_dsl_args.h DslKind):
+/* Generated CUDA source of program `kind` (0..9, see sdeb_dsl_args.h DslKind;
+ * + 256: the meanfield form sdb_run_model uses when desc->coupling is
+ * SDB_COUPLING_MEANFIELD -- sum(j, sin|cos(A_j - B)) factored by the addition
+ * formulas into two equation-independent sums; sums that do not depend on the
+ * equation are always computed once per evaluation):
  * copies at most cap-1 bytes + NUL into buf (may be NULL) and returns the full
  * length, or -1. */
 int64_t sdb_model_source(const sdb_model* model, int32_t kind, char* buf, int64_t cap);

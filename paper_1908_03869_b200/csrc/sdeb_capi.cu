@@ -622,15 +622,19 @@ sdb_status launch_model(sdb_ctx* ctx, Slot& s, const sdb_desc& d, sdb_model* m,
     a.dt = d.dt;
     a.sqrt_dt = std::sqrt(d.dt);
     a.fresh = 1;
-    if (const size_t words = sdeb_dsl::scratch_doubles(m, sdeb_dsl::lanes_for(m), d.orbits)) {
+    const bool factor = d.coupling == SDB_COUPLING_MEANFIELD;
+    if (const size_t words =
+            sdeb_dsl::scratch_doubles(m, sdeb_dsl::lanes_for(m, factor), d.orbits)) {
         SDB_CUDA(ctx, s.scratch.ensure(words * sizeof(double)));
         a.scratch = s.scratch.as<double>();
     }
     std::string err;
-    cudaError_t e = sdeb_dsl::launch(m, kind, a, st, &err);
+    // the meanfield setting lets the generated program factor
+    // sum(j, sin|cos(A_j - B)); pairwise keeps the literal form
+    cudaError_t e = sdeb_dsl::launch(m, kind, a, st, &err, factor);
     if (e != cudaSuccess) return fail_with(ctx, SDB_ERR_CUDA, "%s", err.c_str());
     s.launches += 1;
-    s.lanes = sdeb_dsl::lanes_for(m);
+    s.lanes = sdeb_dsl::lanes_for(m, factor);
     s.persistent = 0;
     s.ctas_per_sm = 0;
     s.tight = 0;
@@ -1151,7 +1155,7 @@ sdb_status model_rows(sdb_ctx* ctx, sdb_model* m, int kind, double t, double dt,
     a.dt = dt;
     a.sqrt_dt = dt > 0.0 ? std::sqrt(dt) : 0.0;
     TmpBuf scratch;
-    if (const size_t words = sdeb_dsl::scratch_doubles(m, sdeb_dsl::lanes_for(m), count)) {
+    if (const size_t words = sdeb_dsl::scratch_doubles(m, sdeb_dsl::lanes_for(m, false), count)) {
         SDB_CUDA(ctx, cudaMalloc(&scratch.p, words * sizeof(double)));
         a.scratch = static_cast<double*>(scratch.p);
     }
@@ -1353,8 +1357,10 @@ sdb_status sdb_model_create(int32_t nequat, int32_t nparams, int32_t nnoise, con
 void sdb_model_free(sdb_model* m) { delete m; }
 
 int64_t sdb_model_source(const sdb_model* m, int32_t kind, char* buf, int64_t cap) {
-    if (!m || kind < 0 || kind >= sdeb::DK_COUNT) return -1;
-    const std::string src = sdeb_dsl::program_source(m, kind, sdeb_dsl::lanes_for(m));
+    if (!m || kind < 0 || (kind & 255) >= sdeb::DK_COUNT || kind > 511) return -1;
+    const bool factor = (kind & 256) != 0;
+    const std::string src = sdeb_dsl::program_source(m, kind & 255, sdeb_dsl::lanes_for(m, factor),
+                                                     factor);
     if (buf && cap > 0) {
         const size_t n = std::min<size_t>(src.size(), size_t(cap - 1));
         std::memcpy(buf, src.data(), n);
@@ -1364,10 +1370,12 @@ int64_t sdb_model_source(const sdb_model* m, int32_t kind, char* buf, int64_t ca
 }
 
 sdb_status sdb_model_build(sdb_model* m, int32_t kind) {
-    if (!m || kind < 0 || kind >= sdeb::DK_COUNT)
+    if (!m || kind < 0 || (kind & 255) >= sdeb::DK_COUNT || kind > 511)
         return fail_with(nullptr, SDB_ERR_ARGUMENT, "bad model or program kind");
     std::string err;
-    cudaError_t e = sdeb_dsl::compile_only(m, kind, sdeb_dsl::lanes_for(m), &err);
+    const bool factor = (kind & 256) != 0;
+    cudaError_t e = sdeb_dsl::compile_only(m, kind & 255, sdeb_dsl::lanes_for(m, factor), factor,
+                                           &err);
     if (e != cudaSuccess) return fail_with(nullptr, SDB_ERR_CUDA, "%s", err.c_str());
     return SDB_OK;
 }

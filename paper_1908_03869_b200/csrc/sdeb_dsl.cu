@@ -245,10 +245,53 @@ std::string literal(double v) {
     return "(" + s + ")";
 }
 
+// Does `n` read variable `v` (sum indices shadow)?
+bool uses(const Node& n, const std::string& v) {
+    switch (n.kind) {
+        case Node::NUM: return false;
+        case Node::VAR: return n.name == v;
+        case Node::SUM: return n.name != v && uses(*n.a, v);
+        case Node::BIN: return uses(*n.a, v) || uses(*n.b, v);
+        default: return uses(*n.a, v);  // INDEX, NEG, CALL
+    }
+}
+
+P clone(const Node& n) {
+    P c(new Node);
+    c->kind = n.kind;
+    c->num = n.num;
+    c->name = n.name;
+    c->op = n.op;
+    c->line = n.line;
+    c->col = n.col;
+    if (n.a) c->a = clone(*n.a);
+    if (n.b) c->b = clone(*n.b);
+    return c;
+}
+
+// `other` is `jside` with sum index j replaced by the equation index i
+// (e.g. y[i] against y[j]): the equation's angle is one of the j-terms.
+bool same_at_i(const Node& other, const Node& jside, const std::string& j) {
+    if (jside.kind == Node::VAR && jside.name == j) return other.kind == Node::VAR && other.name == "i";
+    if (other.kind != jside.kind || other.name != jside.name || other.op != jside.op) return false;
+    if (jside.kind == Node::NUM) return other.num == jside.num;
+    if (jside.kind == Node::SUM && jside.name == j) return false;  // shadowed: keep it simple
+    if (bool(other.a) != bool(jside.a) || bool(other.b) != bool(jside.b)) return false;
+    if (jside.a && !same_at_i(*other.a, *jside.a, j)) return false;
+    if (jside.b && !same_at_i(*other.b, *jside.b, j)) return false;
+    return true;
+}
+
 class Gen {
   public:
-    explicit Gen(bool has_noise) : has_noise_(has_noise) {}
+    // factor: rewrite sum(j, sin|cos(A_j - B)) with the addition formulas so
+    // the j-sums no longer depend on the equation (meanfield form, changes
+    // rounding by a few ulp); hoisting of equation-independent sums is always
+    // on (bit-identical: the same value for every equation).
+    Gen(bool has_noise, bool factor, int n) : has_noise_(has_noise), factor_(factor), n_(n) {}
     bool used_sum = false;
+    bool eq_sum = false;               // a sum is still evaluated per equation
+    std::vector<std::string> hoisted;  // prologue statements H[k] = ...
 
     // Double-valued expression (dsl.py _Evaluator.eval).
     std::string num(const Node& n) {
@@ -292,11 +335,25 @@ class Gen {
             case Node::SUM: {
                 if (scope_.count(n.name) || n.name == "t" || n.name == "N" || n.name == "i")
                     throw GenError{"sum index '" + n.name + "' shadows a name in scope", n.line, n.col};
-                scope_.insert(n.name);
                 used_sum = true;
+                if (factor_) {
+                    std::string f;
+                    if (factored(n, &f)) return f;
+                }
+                const bool hoist = hoistable(n);
+                std::set<std::string> saved;
+                if (hoist) saved.swap(scope_);  // the prologue sees no enclosing sums
+                scope_.insert(n.name);
                 const std::string body = num(*n.a);
                 scope_.erase(n.name);
-                return "dsl_sum([&](int s_" + n.name + ") -> double { return " + body + "; })";
+                const std::string code =
+                    "dsl_sum([&](int s_" + n.name + ") -> double { return " + body + "; })";
+                if (!hoist) {
+                    eq_sum = true;
+                    return code;
+                }
+                scope_.swap(saved);
+                return hoist_value(code);
             }
         }
         throw GenError{"bad node", n.line, n.col};
@@ -331,30 +388,112 @@ class Gen {
     }
 
   private:
-    bool has_noise_;
+    bool has_noise_, factor_;
+    int n_;  // equation count (kept-term slots)
     std::set<std::string> scope_;
+
+    // Same value for every equation: reads neither i nor an enclosing sum index.
+    bool hoistable(const Node& sum) const {
+        if (uses(sum, "i")) return false;
+        for (const std::string& v : scope_)
+            if (uses(sum, v)) return false;
+        return true;
+    }
+
+    std::string hoist_value(const std::string& code) {
+        const std::string ref = "H[" + std::to_string(hoisted.size()) + "]";
+        hoisted.push_back(ref + " = " + code + ";");
+        return ref;
+    }
+
+    // sum(j, sin(A - B)) / sum(j, cos(A - B)) with exactly one side reading j
+    // (and that side free of i and enclosing sums): the addition formulas turn
+    // it into two equation-independent sums of sin / cos of the j-side, done
+    // in one pass (one sincos per term) and hoisted.
+    bool factored(const Node& sum, std::string* out) {
+        const Node& body = *sum.a;
+        if (body.kind != Node::CALL || (body.name != "sin" && body.name != "cos")) return false;
+        const Node& arg = *body.a;
+        if (arg.kind != Node::BIN || arg.op != '-') return false;
+        const std::string& j = sum.name;
+        const bool ja = uses(*arg.a, j), jb = uses(*arg.b, j);
+        if (ja == jb) return false;
+        const Node& jside = ja ? *arg.a : *arg.b;
+        const Node& other = ja ? *arg.b : *arg.a;
+        if (uses(jside, "i")) return false;
+        for (const std::string& v : scope_)
+            if (uses(jside, v)) return false;
+        // the j-side's sums of sin and cos, one pass
+        std::set<std::string> saved;
+        saved.swap(scope_);
+        scope_.insert(j);
+        const std::string term = num(jside);
+        scope_.erase(j);
+        scope_.swap(saved);
+        const size_t k = hoisted.size();
+        const std::string hs = "H[" + std::to_string(k) + "]", hc = "H[" + std::to_string(k + 1) + "]";
+        std::string so, co;
+        if (same_at_i(other, jside, j)) {
+            // the equation's angle is the j-term at j = i: keep every term's
+            // (sin, cos) from the pass (H[k+2 ..], H[k+2+N ..]) instead of a
+            // second sincos per equation
+            const std::string ks = std::to_string(k + 2), kc = std::to_string(k + 2) + " + SDB_N";
+            hoisted.push_back("dsl_sum_sincos_keep<EXACT>([&](int s_" + j + ") -> double { return " +
+                              term + "; }, big, " + hs + ", " + hc + ", &H[" + ks + "], &H[" + kc +
+                              "]);");
+            for (int q = 0; q < 1 + 2 * n_; ++q) hoisted.push_back("");  // H[k+1], kept terms
+            so = "H[" + ks + " + i]";
+            co = "H[" + kc + " + i]";
+        } else {
+            hoisted.push_back("dsl_sum_sincos<EXACT>([&](int s_" + j + ") -> double { return " +
+                              term + "; }, big, " + hs + ", " + hc + ");");
+            hoisted.push_back("");  // the slot H[k+1] is written by the same statement
+            const std::string o = num(other);  // the equation-side angle
+            so = "dsl_sin<EXACT>(" + o + ", big)";
+            co = "dsl_cos<EXACT>(" + o + ", big)";
+        }
+        // A = j-side, B = other.  sin(A-B) = sinA cosB - cosA sinB; sin(B-A) = -(...)
+        // cos(A-B) = cos(B-A) = cosA cosB + sinA sinB
+        if (body.name == "cos") {
+            *out = "__dadd_rn(__dmul_rn(" + hc + ", " + co + "), __dmul_rn(" + hs + ", " + so + "))";
+        } else if (ja) {
+            *out = "__dsub_rn(__dmul_rn(" + hs + ", " + co + "), __dmul_rn(" + hc + ", " + so + "))";
+        } else {
+            *out = "__dsub_rn(__dmul_rn(" + so + ", " + hc + "), __dmul_rn(" + co + ", " + hs + "))";
+        }
+        return true;
+    }
 };
 
-bool gen_function(const std::string& text, bool diffusion, std::string* out, std::string* err,
-                  bool* used_sum) {
+// Device functions of one template: a prologue computing the equation-
+// independent (hoisted) values H[] once per evaluation, and the per-equation
+// function reading them.
+bool gen_function(const std::string& text, bool diffusion, bool factor, int n, std::string* out,
+                  int* nhoist, std::string* err, bool* eq_sum) {
     try {
         Parser ps(text);
         P root = ps.parse();
-        Gen g(diffusion);
+        Gen g(diffusion, factor, n);
         const std::string body = g.num(*root);
-        *used_sum = *used_sum || g.used_sum;
-        if (diffusion) {
-            *out = "template <bool EXACT>\n"
-                   "__device__ __forceinline__ double sdeb::sdb_diffusion(int i, double t, "
-                   "const DVec& y, const double* __restrict__ p, const DVec& n, bool& big) {\n"
-                   "    (void)i; (void)t; (void)y; (void)p; (void)n; (void)big;\n"
-                   "    return " + body + ";\n}\n";
-        } else {
-            *out = "template <bool EXACT>\n"
-                   "__device__ __forceinline__ double sdeb::sdb_drift(int i, double t, "
-                   "const DVec& y, const double* __restrict__ p, bool& big) {\n"
-                   "    (void)i; (void)t; (void)y; (void)p; (void)big;\n    return " + body + ";\n}\n";
-        }
+        *eq_sum = *eq_sum || g.eq_sum;
+        const std::string name = diffusion ? "diffusion" : "drift";
+        const std::string hn = diffusion ? "SDB_DIFF_H" : "SDB_DRIFT_H";
+        const std::string params = diffusion
+            ? "const DVec& y, const double* __restrict__ p, const DVec& n, bool& big"
+            : "const DVec& y, const double* __restrict__ p, bool& big";
+        const std::string unused = diffusion ? "(void)t; (void)y; (void)p; (void)n; (void)big;"
+                                             : "(void)t; (void)y; (void)p; (void)big;";
+        std::string pro;
+        for (const std::string& st : g.hoisted)
+            if (!st.empty()) pro += "    " + st + "\n";
+        *nhoist = int(std::max<size_t>(1, g.hoisted.size()));
+        *out = "template <bool EXACT>\n"
+               "__device__ __forceinline__ void sdeb::sdb_" + name + "_pre(double t, " + params +
+               ", double (&H)[" + hn + "]) {\n    " + unused + " (void)H;\n" + pro + "}\n"
+               "template <bool EXACT>\n"
+               "__device__ __forceinline__ double sdeb::sdb_" + name + "(int i, double t, " + params +
+               ", const double (&H)[" + hn + "]) {\n    (void)i; " + unused + " (void)H;\n"
+               "    return " + body + ";\n}\n";
         return true;
     } catch (const SyntaxError& e) {
         char buf[64];
@@ -394,14 +533,17 @@ int state_words(const sdb_model* m) {
 // sums: there the O(N^2) table reads per step compete with the state-column
 // reads for the shared-memory pipe (measured: Kuramoto templates 2.44e9 ->
 // 1.53e9 orbit-steps/s staged; the OU template 1.94e10 -> 2.26e10).
-bool stage_tables(const sdb_model* m) { return !m->uses_sum; }
+bool stage_tables(const sdb_model* m, bool factor) { return !m->eq_sum[factor ? 1 : 0]; }
 
-int lanes_for(const sdb_model* m) {
+int lanes_for(const sdb_model* m, bool factor) {
     if (const char* e = std::getenv("SDEB200_DSL_LANES")) {
         const int v = std::atoi(e);
         if (v >= 1 && v <= 32 && (v & (v - 1)) == 0) return v;
     }
-    const int per_lane = m->uses_sum ? 4 : 16;
+    // O(N) work per equation (sums left in the equation): ~4 equations per lane;
+    // O(1) (no sums, or all hoisted into the per-evaluation prologue, which
+    // every lane of a group would repeat): ~16
+    const int per_lane = m->eq_sum[factor ? 1 : 0] ? 4 : 16;
     const int want = (m->nequat + per_lane - 1) / per_lane;
     int l = 1;
     while (l < want && l < 32) l <<= 1;
@@ -420,12 +562,18 @@ size_t scratch_doubles(const sdb_model* m, int lanes, int64_t rows) {
 }
 
 bool generate(sdb_model* m, std::string* err) {
-    m->uses_sum = false;
-    return gen_function(m->drift_text, false, &m->drift_cu, err, &m->uses_sum) &&
-           gen_function(m->diffusion_text, true, &m->diffusion_cu, err, &m->uses_sum);
+    for (int f = 0; f < 2; ++f) {
+        m->eq_sum[f] = false;
+        if (!gen_function(m->drift_text, false, f == 1, m->nequat, &m->drift_cu[f], &m->drift_h[f],
+                          err, &m->eq_sum[f]) ||
+            !gen_function(m->diffusion_text, true, f == 1, m->nequat, &m->diffusion_cu[f],
+                          &m->diffusion_h[f], err, &m->eq_sum[f]))
+            return false;
+    }
+    return true;
 }
 
-std::string program_source(const sdb_model* m, int kind, int lanes) {
+std::string program_source(const sdb_model* m, int kind, int lanes, bool factor) {
     // unrolled equation loops keep f / g / RK4 stages in registers; the
     // unrolled model code grows as (N / lanes) x (drift evaluations per
     // step), and ptxas time with it, so larger systems run the loops rolled
@@ -434,24 +582,27 @@ std::string program_source(const sdb_model* m, int kind, int lanes) {
     const int evals = (kind == sdeb::DK_RUN_RK4 || kind == sdeb::DK_STEP_RK4) ? 4
                       : (kind <= sdeb::DK_RUN_XOSHIRO || kind == sdeb::DK_STEP_EM) ? 2 : 1;
     const int unroll = epl * evals <= kUnrollWork ? epl : 1;
-    char head[360];
+    char head[420];
     std::snprintf(head, sizeof(head),
                   "#define SDB_N %d\n#define SDB_NP %d\n#define SDB_NN %d\n#define SDB_KIND %d\n"
-                  "#define SDB_LANES %d\n#define SDB_UNROLL %d\n#define SDB_GLOBAL_STATE %d\n%s",
+                  "#define SDB_LANES %d\n#define SDB_UNROLL %d\n#define SDB_GLOBAL_STATE %d\n"
+                  "#define SDB_DRIFT_H %d\n#define SDB_DIFF_H %d\n%s",
                   m->nequat, m->nparams, m->nnoise, kind, lanes, unroll,
-                  global_state(m, lanes) ? 1 : 0,
-                  stage_tables(m) ? "#define SDEB_SMEM_TABLES 1\n" : "");
+                  global_state(m, lanes) ? 1 : 0, m->drift_h[factor ? 1 : 0],
+                  m->diffusion_h[factor ? 1 : 0],
+                  stage_tables(m, factor) ? "#define SDEB_SMEM_TABLES 1\n" : "");
     return std::string("// generated by sdeb200 from expression templates\n") + head +
-           "#include \"sdeb_dsl_kernel.cuh\"\n\n// drift: " + m->drift_text + "\n" + m->drift_cu +
-           "\n// diffusion: " + m->diffusion_text + "\n" + m->diffusion_cu;
+           "#include \"sdeb_dsl_kernel.cuh\"\n\n// drift: " + m->drift_text +
+           (factor ? "  (sums factored)" : "") + "\n" + m->drift_cu[factor ? 1 : 0] +
+           "\n// diffusion: " + m->diffusion_text + "\n" + m->diffusion_cu[factor ? 1 : 0];
 }
 
 namespace {
 
 // NVRTC: generated source -> sm_100a cubin.
-cudaError_t nvrtc_cubin(const sdb_model* m, int kind, int lanes, std::vector<char>* cubin,
-                        std::string* log, std::string* err) {
-    const std::string src = program_source(m, kind, lanes);
+cudaError_t nvrtc_cubin(const sdb_model* m, int kind, int lanes, bool factor,
+                        std::vector<char>* cubin, std::string* log, std::string* err) {
+    const std::string src = program_source(m, kind, lanes, factor);
     nvrtcProgram prog;
     std::vector<const char*> names, texts;
     for (const RtcHeader& h : kRtcHeaders) {
@@ -484,9 +635,10 @@ cudaError_t nvrtc_cubin(const sdb_model* m, int kind, int lanes, std::vector<cha
     return cudaSuccess;
 }
 
-cudaError_t compile(sdb_model* m, int kind, int lanes, sdb_model::Program* out, std::string* err) {
+cudaError_t compile(sdb_model* m, int kind, int lanes, bool factor, sdb_model::Program* out,
+                    std::string* err) {
     std::vector<char> cubin;
-    cudaError_t e = nvrtc_cubin(m, kind, lanes, &cubin, &out->log, err);
+    cudaError_t e = nvrtc_cubin(m, kind, lanes, factor, &cubin, &out->log, err);
     if (e != cudaSuccess) return e;
     e = cudaLibraryLoadData(&out->lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
     if (e == cudaSuccess) e = cudaLibraryGetKernel(&out->kernel, out->lib, "sdb_dsl_main");
@@ -496,22 +648,23 @@ cudaError_t compile(sdb_model* m, int kind, int lanes, sdb_model::Program* out, 
 
 }  // namespace
 
-cudaError_t compile_only(sdb_model* m, int kind, int lanes, std::string* err) {
+cudaError_t compile_only(sdb_model* m, int kind, int lanes, bool factor, std::string* err) {
     std::vector<char> cubin;
     std::string log;
-    cudaError_t e = nvrtc_cubin(m, kind, lanes, &cubin, &log, err);
+    cudaError_t e = nvrtc_cubin(m, kind, lanes, factor, &cubin, &log, err);
     std::lock_guard<std::mutex> lock(m->mu);
     m->error = e == cudaSuccess ? log : *err;
     return e;
 }
 
-cudaError_t kernel_for(sdb_model* m, int kind, int lanes, cudaKernel_t* out, std::string* err) {
+cudaError_t kernel_for(sdb_model* m, int kind, int lanes, bool factor, cudaKernel_t* out,
+                       std::string* err) {
     std::lock_guard<std::mutex> lock(m->mu);
-    const int key = kind + 64 * lanes;
+    const int key = kind + 64 * lanes + (factor ? 4096 : 0);
     auto it = m->programs.find(key);
     if (it == m->programs.end()) {
         sdb_model::Program prog;
-        cudaError_t e = compile(m, kind, lanes, &prog, err);
+        cudaError_t e = compile(m, kind, lanes, factor, &prog, err);
         if (e != cudaSuccess) return e;
         it = m->programs.emplace(key, prog).first;
     }
@@ -520,10 +673,10 @@ cudaError_t kernel_for(sdb_model* m, int kind, int lanes, cudaKernel_t* out, std
 }
 
 cudaError_t launch(sdb_model* m, int kind, const sdeb::DslArgs& a, cudaStream_t st,
-                   std::string* err) {
-    const int lanes = lanes_for(m);
+                   std::string* err, bool factor) {
+    const int lanes = lanes_for(m, factor);
     cudaKernel_t k = nullptr;
-    cudaError_t e = kernel_for(m, kind, lanes, &k, err);
+    cudaError_t e = kernel_for(m, kind, lanes, factor, &k, err);
     if (e != cudaSuccess) return e;
     if (a.rows <= 0) return cudaSuccess;
     const int64_t slots = kBlock / lanes;
@@ -537,7 +690,7 @@ cudaError_t launch(sdb_model* m, int kind, const sdeb::DslArgs& a, cudaStream_t 
         smem = size_t(slots) * state_words(m) * sizeof(double);
     }
     // the staged math tables are static shared memory on top of the columns
-    if (smem + (stage_tables(m) ? kTableSmem : 0) > 48 * 1024) {
+    if (smem + (stage_tables(m, factor) ? kTableSmem : 0) > 48 * 1024) {
         e = cudaFuncSetAttribute(reinterpret_cast<const void*>(k),
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
         if (e != cudaSuccess) {

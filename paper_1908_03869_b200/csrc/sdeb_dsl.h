@@ -20,16 +20,17 @@
 struct sdb_model {
     int32_t nequat = 0, nparams = 0, nnoise = 0;
     std::string drift_text, diffusion_text;  // as given
-    std::string drift_cu, diffusion_cu;      // generated device functions
+    std::string drift_cu[2], diffusion_cu[2];  // generated device functions: [literal, factored]
+    int drift_h[2] = {1, 1}, diffusion_h[2] = {1, 1};  // hoisted values per evaluation
     std::string error;                       // last compile / launch error
-    bool uses_sum = false;                   // O(N) work per equation (sets lanes_for)
+    bool eq_sum[2] = {false, false};         // [literal, factored]: a sum stays per equation
     std::mutex mu;
     struct Program {
         cudaLibrary_t lib = nullptr;
         cudaKernel_t kernel = nullptr;
         std::string log;
     };
-    std::map<int, Program> programs;  // by kind + 64 * lanes
+    std::map<int, Program> programs;  // by kind + 64 * lanes + 4096 * factor
     ~sdb_model();
 };
 
@@ -39,19 +40,21 @@ namespace sdeb_dsl {
 // false with `err` = "drift: line L, column C: message" style text.
 bool generate(sdb_model* m, std::string* err);
 
-// Full CUDA source of one program kind (for inspection / tests).
-std::string program_source(const sdb_model* m, int kind, int lanes);
+// Full CUDA source of one program kind (for inspection / tests).  factor:
+// the meanfield form (sum(j, sin|cos(A_j - B)) via the addition formulas).
+std::string program_source(const sdb_model* m, int kind, int lanes, bool factor);
 
 // NVRTC compile only (no device needed); the log lands in m->error.
-cudaError_t compile_only(sdb_model* m, int kind, int lanes, std::string* err);
+cudaError_t compile_only(sdb_model* m, int kind, int lanes, bool factor, std::string* err);
 
 // The compiled kernel of one (kind, lanes) (compiled on first use, thread-safe).
-cudaError_t kernel_for(sdb_model* m, int kind, int lanes, cudaKernel_t* out, std::string* err);
+cudaError_t kernel_for(sdb_model* m, int kind, int lanes, bool factor, cudaKernel_t* out,
+                       std::string* err);
 
 // Launch one program over `a.rows` orbits (lanes_for(m) threads each); the
 // caller provides a.scratch of scratch_doubles() when global_state().
 cudaError_t launch(sdb_model* m, int kind, const sdeb::DslArgs& a, cudaStream_t st,
-                   std::string* err);
+                   std::string* err, bool factor = false);
 
 constexpr int kBlock = 128;      // threads per CTA = 128 / lanes orbit slots
 constexpr int kSmemMax = 96 * 1024;
@@ -63,9 +66,9 @@ int state_words(const sdb_model* m);
 // Lanes per orbit (power of two <= 32): ~4 equations per lane for templates
 // with sums (O(N) work per equation), ~16 without, or SDEB200_DSL_LANES.
 // Results do not depend on it.
-int lanes_for(const sdb_model* m);
+int lanes_for(const sdb_model* m, bool factor);
 // True when the program stages the math tables in shared memory.
-bool stage_tables(const sdb_model* m);
+bool stage_tables(const sdb_model* m, bool factor);
 // True when the columns go to global scratch instead of shared memory.
 bool global_state(const sdb_model* m, int lanes);
 // Doubles of global scratch a launch over `rows` orbits needs (0 = none).

@@ -82,6 +82,86 @@ __device__ __forceinline__ double dsl_sum(F&& f) {
     return pw_sum<0, SDB_N>(f);
 }
 
+// sum(j, sin(a_j)) and sum(j, cos(a_j)) in one pass (one sincos per term),
+// each in numpy's pairwise order: the factored meanfield form of the
+// generated code (sdeb_dsl.cu Gen::factored).
+template <int LO, int CNT, bool EXACT, class F>
+__device__ __forceinline__ void pw_sum_sincos(F&& f, bool& big, double& ss, double& sc,
+                                              double* keep_s = nullptr, double* keep_c = nullptr) {
+    auto sc_of = [&](int j, double& s, double& c) {
+        const double x = f(j);
+        if constexpr (EXACT) {
+            if (big_arg(x)) {
+                sincos(x, &s, &c);
+            } else {
+                sincos_small(x, s, c);
+            }
+        } else {
+            big |= big_arg(x);
+            sincos_small(x, s, c);
+        }
+        if (keep_s) {  // the equation-side values (sum(j, sin(y[j] - y[i])) form)
+            keep_s[j] = s;
+            keep_c[j] = c;
+        }
+    };
+    if constexpr (CNT < 8) {
+        ss = 0.0;
+        sc = 0.0;
+#pragma unroll
+        for (int k = 0; k < CNT; ++k) {
+            double s, c;
+            sc_of(LO + k, s, c);
+            ss = __dadd_rn(ss, s);
+            sc = __dadd_rn(sc, c);
+        }
+    } else if constexpr (CNT <= 128) {
+        double rs[8], rc[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) sc_of(LO + k, rs[k], rc[k]);
+        constexpr int body = CNT - CNT % 8;
+#pragma unroll 1
+        for (int i = 8; i < body; i += 8) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                double s, c;
+                sc_of(LO + i + k, s, c);
+                rs[k] = __dadd_rn(rs[k], s);
+                rc[k] = __dadd_rn(rc[k], c);
+            }
+        }
+        ss = __dadd_rn(__dadd_rn(__dadd_rn(rs[0], rs[1]), __dadd_rn(rs[2], rs[3])),
+                       __dadd_rn(__dadd_rn(rs[4], rs[5]), __dadd_rn(rs[6], rs[7])));
+        sc = __dadd_rn(__dadd_rn(__dadd_rn(rc[0], rc[1]), __dadd_rn(rc[2], rc[3])),
+                       __dadd_rn(__dadd_rn(rc[4], rc[5]), __dadd_rn(rc[6], rc[7])));
+#pragma unroll
+        for (int i = body; i < CNT; ++i) {
+            double s, c;
+            sc_of(LO + i, s, c);
+            ss = __dadd_rn(ss, s);
+            sc = __dadd_rn(sc, c);
+        }
+    } else {
+        constexpr int half = CNT / 2 - (CNT / 2) % 8;
+        double s1, c1, s2, c2;
+        pw_sum_sincos<LO, half, EXACT>(f, big, s1, c1, keep_s, keep_c);
+        pw_sum_sincos<LO + half, CNT - half, EXACT>(f, big, s2, c2, keep_s, keep_c);
+        ss = __dadd_rn(s1, s2);
+        sc = __dadd_rn(c1, c2);
+    }
+}
+
+template <bool EXACT, class F>
+__device__ __forceinline__ void dsl_sum_sincos(F&& f, bool& big, double& ss, double& sc) {
+    pw_sum_sincos<0, SDB_N, EXACT>(f, big, ss, sc);
+}
+
+template <bool EXACT, class F>
+__device__ __forceinline__ void dsl_sum_sincos_keep(F&& f, bool& big, double& ss, double& sc,
+                                                    double* keep_s, double* keep_c) {
+    pw_sum_sincos<0, SDB_N, EXACT>(f, big, ss, sc, keep_s, keep_c);
+}
+
 // |x| >= 2^29 (or inf/NaN): libdevice's exact reduction, out of line so the
 // unrolled model code stays small.
 __device__ __noinline__ double2 dsl_sincos_big(double x) {
@@ -123,13 +203,24 @@ __device__ __forceinline__ double dsl_sq(double x) { return __dmul_rn(x, x); }
 
 // ---- the model (defined by the generated code after this header) ------------
 
+// Each template comes as a prologue computing the values that do not depend
+// on the equation (hoisted sums, H) once per evaluation, and the per-equation
+// function reading them.
+template <bool EXACT>
+__device__ __forceinline__ void sdb_drift_pre(double t, const DVec& y, const double* __restrict__ p,
+                                              bool& big, double (&H)[SDB_DRIFT_H]);
 template <bool EXACT>
 __device__ __forceinline__ double sdb_drift(int i, double t, const DVec& y,
-                                           const double* __restrict__ p, bool& big);
+                                           const double* __restrict__ p, bool& big,
+                                           const double (&H)[SDB_DRIFT_H]);
+template <bool EXACT>
+__device__ __forceinline__ void sdb_diffusion_pre(double t, const DVec& y,
+                                                  const double* __restrict__ p, const DVec& n,
+                                                  bool& big, double (&H)[SDB_DIFF_H]);
 template <bool EXACT>
 __device__ __forceinline__ double sdb_diffusion(int i, double t, const DVec& y,
                                                const double* __restrict__ p, const DVec& n,
-                                               bool& big);
+                                               bool& big, const double (&H)[SDB_DIFF_H]);
 
 __device__ __forceinline__ bool dsl_finite(double x) {
     return (__double2hiint(x) & 0x7ff00000) != 0x7ff00000;
@@ -166,10 +257,12 @@ template <bool EXACT>
 __device__ __forceinline__ void dsl_drift_vec(int lane, double t, const DVec& y,
                                               const double* __restrict__ p, double (&f)[kEPL],
                                               bool& big) {
+    double H[SDB_DRIFT_H];
+    sdb_drift_pre<EXACT>(t, y, p, big, H);
 #pragma unroll kDslUnroll
     for (int q = 0; q < kEPL; ++q) {
         const int i = lane + q * kL;
-        f[q] = (i < SDB_N) ? sdb_drift<EXACT>(i, t, y, p, big) : 0.0;
+        f[q] = (i < SDB_N) ? sdb_drift<EXACT>(i, t, y, p, big, H) : 0.0;
     }
 }
 
@@ -180,11 +273,13 @@ __device__ __forceinline__ void dsl_em_pass(int lane, double t, double dt, doubl
                                             const DVec& nz, double (&ynew)[kEPL], bool& big) {
     double f[kEPL];
     dsl_drift_vec<EXACT>(lane, t, y, p, f, big);
+    double G[SDB_DIFF_H];
+    sdb_diffusion_pre<EXACT>(t, y, p, nz, big, G);
 #pragma unroll kDslUnroll
     for (int q = 0; q < kEPL; ++q) {
         const int i = lane + q * kL;
         if (i < SDB_N) {
-            const double g = sdb_diffusion<EXACT>(i, t, y, p, nz, big);
+            const double g = sdb_diffusion<EXACT>(i, t, y, p, nz, big, G);
             ynew[q] = __dadd_rn(__dadd_rn(y[i], __dmul_rn(f[q], dt)), __dmul_rn(sqrt_dt, g));
         } else {
             ynew[q] = 0.0;
@@ -364,12 +459,22 @@ extern "C" __global__ void __launch_bounds__(128) sdb_dsl_main(const sdeb::DslAr
 
 #if SDB_KIND == 8 || SDB_KIND == 9  // drift_eval / diffusion_eval
     bool big = false;  // evaluation is not a hot loop: always the exact form
+#if SDB_KIND == 8
+    double H[SDB_DRIFT_H];
+    sdb_drift_pre<true>(a.t, y, p, big, H);
+#else
+    double H[SDB_DIFF_H];
+    sdb_diffusion_pre<true>(a.t, y, p, nz, big, H);
+#endif
 #pragma unroll kDslUnroll
     for (int q = 0; q < kEPL; ++q) {
         const int i = lane + q * kL;
+#if SDB_KIND == 8
+        if (i < SDB_N && active) a.values[row * SDB_N + i] = sdb_drift<true>(i, a.t, y, p, big, H);
+#else
         if (i < SDB_N && active)
-            a.values[row * SDB_N + i] = SDB_KIND == 8 ? sdb_drift<true>(i, a.t, y, p, big)
-                                                      : sdb_diffusion<true>(i, a.t, y, p, nz, big);
+            a.values[row * SDB_N + i] = sdb_diffusion<true>(i, a.t, y, p, nz, big, H);
+#endif
     }
 #elif SDB_KIND >= 5  // one caller-driven step
     double ynew[kEPL];

@@ -44,15 +44,19 @@ class CompiledModel:
             nat.lib().sdb_model_free(h)
             self.handle = None
 
-    def source(self, kind: int) -> str:
-        n = nat.lib().sdb_model_source(self.handle, kind, None, 0)
+    def source(self, kind: int, factored: bool = False) -> str:
+        """Generated CUDA of one program kind (factored: the meanfield form
+        run_batch uses with coupling="meanfield")."""
+        k = kind | (256 if factored else 0)
+        n = nat.lib().sdb_model_source(self.handle, k, None, 0)
         buf = ctypes.create_string_buffer(n + 1)
-        nat.lib().sdb_model_source(self.handle, kind, buf, n + 1)
+        nat.lib().sdb_model_source(self.handle, k, buf, n + 1)
         return buf.value.decode()
 
-    def build(self, kind: int):
+    def build(self, kind: int, factored: bool = False):
         """NVRTC-compile one program kind (no GPU needed)."""
-        nat.check(nat.lib().sdb_model_build(self.handle, kind), None, "sdb_model_build")
+        nat.check(nat.lib().sdb_model_build(self.handle, kind | (256 if factored else 0)), None,
+                  "sdb_model_build")
 
 
 def compiled(nequat: int, nparams: int, nnoise: int, drift, diffusion) -> CompiledModel:

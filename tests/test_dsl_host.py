@@ -194,8 +194,11 @@ def test_lane_groups_and_state_placement(monkeypatch):
     assert "#define SDB_LANES 1" in small.source(0)
     mid = program.compiled(16, 1, 16, dsl.parse("p[0] - y[i]"), dsl.parse("n[i]"))
     assert "#define SDB_LANES 1" in mid.source(0)  # O(1) per equation: one lane
-    mid_sum = program.compiled(16, 1, 16, dsl.parse("p[0] - sum(j, y[j])"), dsl.parse("n[i]"))
+    mid_sum = program.compiled(16, 1, 16, dsl.parse("p[0] - sum(j, y[j] * y[i])"),
+                               dsl.parse("n[i]"))
     assert "#define SDB_LANES 4" in mid_sum.source(0)  # O(N) per equation: ~4 per lane
+    hoisted = program.compiled(16, 1, 16, dsl.parse("p[0] - sum(j, y[j])"), dsl.parse("n[i]"))
+    assert "#define SDB_LANES 1" in hoisted.source(0)  # the sum is computed once per step
     big = program.compiled(400, 1, 400, dsl.parse("p[0] - sum(j, y[j] - y[i])"),
                            dsl.parse("n[i]"))
     src = big.source(0)
@@ -205,3 +208,32 @@ def test_lane_groups_and_state_placement(monkeypatch):
     src = big.source(0)
     assert "#define SDB_LANES 1" in src and "#define SDB_GLOBAL_STATE 1" in src
     big.build(0)
+
+
+def test_factored_and_hoisted_code():
+    cm = program.compiled(8, 17, 8, dsl.parse(KURAMOTO_DRIFT_TEMPLATE),
+                          dsl.parse(KURAMOTO_DIFFUSION_TEMPLATE))
+    lit, fac = cm.source(0), cm.source(0, factored=True)
+    # literal: the n^2 sin terms as written; factored: one sincos pass over j,
+    # hoisted into the prologue, combined per equation by the addition formula
+    assert "dsl_sin<EXACT>(__dsub_rn(y[s_j], y[i]), big)" in lit and "dsl_sum_sincos" not in lit
+    # the equation's angle y[i] is the j-term at j = i: the pass keeps every term's
+    # (sin, cos) for the equations instead of a second sincos each
+    assert ("dsl_sum_sincos_keep<EXACT>([&](int s_j) -> double { return y[s_j]; }, big, H[0], "
+            "H[1], &H[2], &H[2 + SDB_N]);") in fac
+    assert "H[2 + SDB_N + i]" in fac and "dsl_cos<EXACT>" not in fac.split("sdb_drift(int i")[1]
+    assert "#define SDB_DRIFT_H %d" % (2 + 2 * 8) in fac and "#define SDB_DRIFT_H 1" in lit
+    # a different equation-side angle: a second sincos per equation
+    other = program.compiled(4, 1, 0, dsl.parse("sum(j, cos(y[j] - 2 * y[i]))"), None)
+    assert "dsl_sum_sincos<EXACT>" in other.source(3, factored=True)
+    # equation-independent sums are hoisted in both forms (bit-identical)
+    m = program.compiled(3, 1, 0, dsl.parse("p[0] * sum(j, y[j]) - y[i]"), None)
+    for form in (m.source(3), m.source(3, factored=True)):
+        assert "H[0] = dsl_sum([&](int s_j) -> double { return y[s_j]; });" in form
+        assert "__dmul_rn(p[0], H[0])" in form
+    # sums that read i stay per equation; sin(A - B) with both sides reading j is not factored
+    k = program.compiled(3, 1, 0, dsl.parse("sum(j, sin(y[j] - y[j] * y[i])) + sum(j, y[j] * i)"),
+                         None)
+    assert "H[0]" not in k.source(3, factored=True).split("sdb_drift(int i")[1]
+    for kind in (0, 3, 4, 8):
+        cm.build(kind, factored=True)
