@@ -547,7 +547,7 @@ sdb_status choose_layout(sdb_ctx* ctx, Slot& s, const sdb_desc& d, const double*
     }
     // stage 2: the four best re-timed on a long probe (>= 1/8 of the run and
     // >= 4 of the run's persistent slabs, persistent slabs sized as in the real
-    // run, best of 3): the short probe cannot resolve layouts a few percent
+    // run, best of 5): the short probe cannot resolve layouts a few percent
     // apart, and with short slabs it over-charges the persistent hand-offs
     std::sort(scores.begin(), scores.end());
     int64_t longest_slab = 0;  // the probe must span several real slabs
@@ -565,7 +565,7 @@ sdb_status choose_layout(sdb_ctx* ctx, Slot& s, const sdb_desc& d, const double*
         float best3 = 1e30f;
         for (size_t r = 0; r < scores.size() && r < 4; ++r) {
             float t3 = 0.f;
-            rc = timed(cands[scores[r].second], p3, &t3, 3, true);
+            rc = timed(cands[scores[r].second], p3, &t3, 5, true);
             if (rc != SDB_OK) break;
             if (trace_enabled()) {
                 const Layout& l = cands[scores[r].second];

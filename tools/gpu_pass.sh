@@ -4,7 +4,7 @@
 # `ncu --set full` capture of the cfg2 kernel at the autotuned layout.
 # usage: bash tools/gpu_pass.sh TAG [workloads...]
 TAG=${1:-pass}; shift
-WLS=${@:-cfg1 cfg3_n32 cfg3_n64 cfg3_n128 cfg3_n256 cfg4 cfg5 cfg5_coherence cfg2_codegen ou_codegen}
+WLS=${@:-cfg1 cfg3_n32 cfg3_n64 cfg3_n128 cfg3_n256 cfg4 cfg5 cfg5_coherence cfg2_codegen ou_codegen paper_n5 paper_n10 paper_n15}
 O=gpurun_out/$TAG
 mkdir -p $O
 nvidia-smi > $O/nvidia-smi.txt 2>&1
