@@ -6,6 +6,10 @@
 // fused kernel of sdeb_kuramoto.cuh.
 #include <cuda_runtime.h>
 #include <fcntl.h>
+#include <sys/mman.h>
+#if defined(__SSE2__)
+#include <emmintrin.h>
+#endif
 #include <unistd.h>
 
 #include <algorithm>
@@ -762,17 +766,88 @@ class CopyPool {
 
 // Host copy of rows [0, rows) split over up to `threads` workers (the calling
 // thread takes the first range).  Pageable numpy destinations fault their
-// pages in on first touch; spreading the copy spreads the faults too.
+// pages in on first touch; spreading the copy spreads the faults too.  Each
+// range ends with a store fence, so streaming stores (copy_bytes) are
+// globally visible before the pool reports the job done.
 template <class F>
 void parallel_rows(int64_t rows, size_t bytes, int threads, F&& fn) {
     const int64_t want = std::min<int64_t>(threads, int64_t(bytes >> 20));  // >= 1 MiB each
     const int nt = int(std::max<int64_t>(1, std::min<int64_t>(want, rows)));
+    auto part = [&](int t) {
+        fn(rows * t / nt, rows * (t + 1) / nt);
+#if defined(__SSE2__)
+        _mm_sfence();
+#endif
+    };
     if (nt == 1) {
-        fn(int64_t(0), rows);
+        part(0);
         return;
     }
-    auto part = [&](int t) { fn(rows * t / nt, rows * (t + 1) / nt); };
     CopyPool::get().run(nt, part);
+}
+
+// Bulk host copy for the staging legs.  `stream` = non-temporal stores: the
+// GB-sized legs are not re-read by the copying thread, so skipping the
+// destination's read-for-ownership and cache fill raises the copy rate
+// (B200 host, 16 threads: 72 -> 80 GB/s into touched pages, 19 -> 28 GB/s
+// into fresh 4 KiB pages; tools/host_copy_bench.cpp).  Small runs keep plain
+// memcpy so their outputs stay cache-resident for the caller.
+inline void copy_bytes(void* dst, const void* src, size_t bytes, bool stream) {
+#if defined(__SSE2__)
+    if (stream && bytes >= 256) {
+        char* d = static_cast<char*>(dst);
+        const char* s = static_cast<const char*>(src);
+        const size_t head = (16 - (reinterpret_cast<uintptr_t>(d) & 15)) & 15;
+        std::memcpy(d, s, head);
+        d += head;
+        s += head;
+        bytes -= head;
+        size_t i = 0;
+        for (; i + 64 <= bytes; i += 64) {
+            const __m128i a = _mm_loadu_si128(reinterpret_cast<const __m128i*>(s + i));
+            const __m128i b = _mm_loadu_si128(reinterpret_cast<const __m128i*>(s + i + 16));
+            const __m128i c = _mm_loadu_si128(reinterpret_cast<const __m128i*>(s + i + 32));
+            const __m128i e = _mm_loadu_si128(reinterpret_cast<const __m128i*>(s + i + 48));
+            _mm_stream_si128(reinterpret_cast<__m128i*>(d + i), a);
+            _mm_stream_si128(reinterpret_cast<__m128i*>(d + i + 16), b);
+            _mm_stream_si128(reinterpret_cast<__m128i*>(d + i + 32), c);
+            _mm_stream_si128(reinterpret_cast<__m128i*>(d + i + 48), e);
+        }
+        std::memcpy(d + i, s + i, bytes - i);
+        return;
+    }
+#endif
+    (void)stream;
+    std::memcpy(dst, src, bytes);
+}
+
+// transfers at least this large (per shard and direction) use streaming stores
+constexpr size_t kStreamCopyBytes = size_t(64) << 20;
+
+// Fault in the pages of [lo, hi) of a caller's store without changing their
+// contents (MADV_POPULATE_WRITE, Linux 5.14+), else by writing one byte per
+// page inside the range -- only ever called on rows no drain has written yet.
+// A fresh store's first-touch faults are the drain's dominant cost (the
+// pinned -> fresh copy runs at 19-38 GB/s, into touched pages at 80 GB/s);
+// doing them while the host would otherwise block on a kernel or a DMA takes
+// them off the critical path.
+void prefault_range(char* lo, char* hi) {
+    if (hi <= lo) return;
+    constexpr uintptr_t kPage = 4096;
+#ifndef MADV_POPULATE_WRITE
+#define MADV_POPULATE_WRITE 23
+#endif
+    static std::atomic<bool> no_madvise{false};
+    const uintptr_t a = (reinterpret_cast<uintptr_t>(lo) + kPage - 1) & ~(kPage - 1);
+    const uintptr_t b = reinterpret_cast<uintptr_t>(hi) & ~(kPage - 1);
+    if (b > a && !no_madvise.load(std::memory_order_relaxed)) {
+        if (::madvise(reinterpret_cast<void*>(a), b - a, MADV_POPULATE_WRITE) == 0) return;
+        if (errno == EINVAL) no_madvise.store(true, std::memory_order_relaxed);
+    }
+    for (char* q = lo; q < hi;) {
+        *reinterpret_cast<volatile char*>(q) = 0;
+        q = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(q) & ~(kPage - 1)) + kPage);
+    }
 }
 
 int host_copy_threads(int /*shards*/) {
@@ -860,8 +935,17 @@ sdb_status run_shard(sdb_ctx* ctx, Slot& s, sdb_desc d, sdb_model* m, int64_t r0
     const size_t piece_cap = size_t(std::max(1, env_int("SDEB200_PIECE_KB", 65536))) << 10;
     const size_t in_row = size_t(n + np_) * sizeof(double);
     const size_t out_row = size_t(width + 1) * sizeof(double);  // samples + fail word
-    const int64_t in_piece = std::max<int64_t>(1, int64_t(piece_cap / in_row));
-    const int64_t out_piece = std::max<int64_t>(1, int64_t(piece_cap / out_row));
+    const bool nt_in = size_t(rows) * in_row >= kStreamCopyBytes;
+    const bool nt_out = size_t(rows) * out_row >= kStreamCopyBytes;
+    // pieces of ~1/8 of a tile (4 MiB .. piece_cap): even a one-tile run then
+    // overlaps each piece's host copy with the neighbouring piece's DMA
+    auto piece_rows = [&](size_t row_bytes) {
+        const size_t tile_bytes = size_t((rows + tiles - 1) / tiles) * row_bytes;
+        const size_t want = std::min(piece_cap, std::max(size_t(4) << 20, tile_bytes / 8));
+        return std::max<int64_t>(1, int64_t(want / row_bytes));
+    };
+    const int64_t in_piece = piece_rows(in_row);
+    const int64_t out_piece = piece_rows(out_row);
     double* d_init = s.init.as<double>();
     double* d_params = s.params.as<double>();
     double* d_values = s.values.as<double>();
@@ -876,9 +960,33 @@ sdb_status run_shard(sdb_ctx* ctx, Slot& s, sdb_desc d, sdb_model* m, int64_t r0
     std::vector<Pending> pending;  // FIFO of issued output pieces
     size_t head = 0;
 
+    // Destination prefault (see prefault_range): while the next piece's DMA
+    // (or the kernel before it) is still running, fault in the store pages of
+    // rows no drain has reached yet, 32 MiB at a time.  SDEB200_PREFAULT=0 off.
+    const int64_t row_words = out_mode ? width : (k + 1) * n;
+    const bool prefault = values && nt_out && env_int("SDEB200_PREFAULT", 1) != 0;
+    const int64_t pf_rows = std::max<int64_t>(1, int64_t((size_t(32) << 20) / (row_words * 8)));
+    int64_t pf_next = 0;  // shard-local rows below this are populated (or drained)
+    double prefault_ms = 0.0;
+
     auto drain_one = [&]() -> sdb_status {
         const Pending p = pending[head++];
         PinBuf& pb = s.pin_out[p.slot];
+        if (prefault) {
+            const double f0 = now_ms();
+            pf_next = std::max(pf_next, p.a);  // rows below p.a are drained already
+            while (pf_next < rows && cudaEventQuery(pb.ev) == cudaErrorNotReady) {
+                const int64_t a = pf_next, b = std::min(rows, a + pf_rows);
+                char* base = reinterpret_cast<char*>(values + (r0 + a) * row_words);
+                const size_t span = size_t(b - a) * size_t(row_words) * sizeof(double);
+                parallel_rows(int64_t(threads), span, threads, [&](int64_t x, int64_t y) {
+                    prefault_range(base + span * size_t(x) / size_t(threads),
+                                   base + span * size_t(y) / size_t(threads));
+                });
+                pf_next = b;
+            }
+            prefault_ms += now_ms() - f0;
+        }
         const double w0 = now_ms();
         SDB_CUDA(ctx, cudaEventSynchronize(pb.ev));
         const double w1 = now_ms();
@@ -901,12 +1009,13 @@ sdb_status run_shard(sdb_ctx* ctx, Slot& s, sdb_desc d, sdb_model* m, int64_t r0
             for (int64_t r = a; r < b; ++r) {
                 const int64_t g = r0 + p.a + r;
                 if (out_mode) {
-                    std::memcpy(values + g * width, src + r * width, size_t(width) * sizeof(double));
+                    copy_bytes(values + g * width, src + r * width, size_t(width) * sizeof(double),
+                               nt_out);
                     continue;
                 }
                 double* dst = values + g * (k + 1) * n;
-                std::memcpy(dst, init + g * n, size_t(n) * sizeof(double));
-                std::memcpy(dst + n, src + r * k * n, size_t(k) * n * sizeof(double));
+                copy_bytes(dst, init + g * n, size_t(n) * sizeof(double), nt_out);
+                copy_bytes(dst + n, src + r * k * n, size_t(k) * n * sizeof(double), nt_out);
             }
         });
         std::memcpy(fail + r0 + p.a, fsrc, size_t(p.rows) * sizeof(int64_t));
@@ -929,8 +1038,9 @@ sdb_status run_shard(sdb_ctx* ctx, Slot& s, sdb_desc d, sdb_model* m, int64_t r0
             const double* h_init = init + (r0 + p0) * n;
             const double* h_par = params + (r0 + p0) * np_;
             parallel_rows(pr, size_t(pr) * in_row, threads, [&](int64_t x, int64_t y) {
-                std::memcpy(pin_init + x * n, h_init + x * n, size_t(y - x) * n * sizeof(double));
-                std::memcpy(pin_par + x * np_, h_par + x * np_, size_t(y - x) * np_ * sizeof(double));
+                copy_bytes(pin_init + x * n, h_init + x * n, size_t(y - x) * n * sizeof(double), nt_in);
+                copy_bytes(pin_par + x * np_, h_par + x * np_, size_t(y - x) * np_ * sizeof(double),
+                           nt_in);
             });
             wait_ms += w1 - w0;
             host_in_ms += now_ms() - w1;
@@ -1013,9 +1123,9 @@ sdb_status run_shard(sdb_ctx* ctx, Slot& s, sdb_desc d, sdb_model* m, int64_t r0
     if (tr) {
         std::fprintf(stderr,
                      "[sdeb200] dev %d rows %lld tiles %lld: total %.3f ms, host-in %.3f ms, "
-                     "host-out %.3f ms, waits %.3f ms (%.1f MB in, %.1f MB out)\n",
+                     "host-out %.3f ms, waits %.3f ms, prefault %.3f ms (%.1f MB in, %.1f MB out)\n",
                      s.device, (long long)rows, (long long)tiles, now_ms() - t0, host_in_ms,
-                     host_out_ms, wait_ms, double(rows) * in_row / 1e6,
+                     host_out_ms, wait_ms, prefault_ms, double(rows) * in_row / 1e6,
                      double(rows) * out_row / 1e6);
     }
     return rc;

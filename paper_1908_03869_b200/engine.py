@@ -270,7 +270,7 @@ def run_batch(model: ModelSpec, config: EngineConfig, batch: OrbitBatch, *,
 
     sample_dt = config.ksteps * config.dt
     times = np.arange(samples, dtype=np.float64) * sample_dt
-    values = np.empty((batch.orbits, samples, model.nequat), dtype=np.float64)
+    values = nat.host_empty((batch.orbits, samples, model.nequat))
     fail_step = np.empty(batch.orbits, dtype=np.int64)
     init = nat.f64(batch.init)
     params = nat.f64(batch.params)
