@@ -320,6 +320,29 @@ int smem_for_cap(int device, int cap) {
     return std::max(0, per_sm / cap - reserved - int(sdeb::kTableSmemBytes)) & ~255;
 }
 
+// Dynamic shared memory that holds a kernel at exactly `cap` CTAs per SM:
+// smem_for_cap's estimate, stepped down 256 B at a time until the occupancy
+// calculator agrees (the kernel's own static shared memory and allocation
+// granularity are not known exactly up front).  0 if no size works.
+int fit_smem_for_cap(int device, int J, int solver, int stream, int coupling, int variant,
+                     int cap) {
+    int optin = 0;
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+    for (int smem = smem_for_cap(device, cap), tries = 0; smem > 0 && tries < 16;
+         smem -= 256, ++tries) {
+        if (smem > optin) continue;
+        int got = 0;
+        if (occupancy_run(J, solver, stream, coupling, variant, size_t(smem), &got) != cudaSuccess) {
+            cudaGetLastError();  // not sticky: drop it so later launches see a clean slate
+            return 0;
+        }
+        if (got == cap) return smem;
+        if (got < cap) continue;  // still too large per CTA
+        return 0;                 // more CTAs than asked: smaller sizes only add more
+    }
+    return 0;
+}
+
 // Kernel instantiation variant: 1 padded (n < next_pow2(n)), else 0, or 2
 // for the register-capped unpadded form.
 int kernel_variant(const sdb_desc& d, int tight) {
@@ -372,17 +395,9 @@ sdb_status candidate_layouts(sdb_ctx* ctx, const Slot& s, const sdb_desc& d, int
             const double eff_cap = waves_cap / std::ceil(waves_cap);
             const double eff_occ = waves_occ / std::ceil(waves_occ);
             if (eff_cap <= eff_occ + 0.02) continue;
-            const int smem = smem_for_cap(s.device, cap);
-            int optin = 0;
-            cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, s.device);
-            if (smem <= 0 || smem > optin) continue;
-            int got = 0;
-            if (occupancy_run(J, kind_solver, kind_stream, d.coupling, padded, size_t(smem),
-                              &got) != cudaSuccess) {
-                cudaGetLastError();  // not sticky: drop it so later launches see a clean slate
-                continue;
-            }
-            if (got == cap) out->push_back(Layout{L, 0, smem, cap, 0});
+            const int smem = fit_smem_for_cap(s.device, J, kind_solver, kind_stream, d.coupling,
+                                              padded, cap);
+            if (smem > 0) out->push_back(Layout{L, 0, smem, cap, 0});
         }
       }
     }
@@ -452,8 +467,11 @@ sdb_status choose_layout(sdb_ctx* ctx, Slot& s, const sdb_desc& d, const double*
             int occ = 0;
             SDB_CUDA(ctx, occupancy_run(P / L, kind_solver, kind_stream, d.coupling,
                                         kernel_variant(d, tight), 0, &occ));
-            Layout lay{L, pers, (cap > 0 && !pers) ? smem_for_cap(s.device, cap) : 0,
-                       cap > 0 ? cap : occ, tight};
+            const int smem = (cap > 0 && !pers && cap < occ)
+                                 ? fit_smem_for_cap(s.device, P / L, kind_solver, kind_stream,
+                                                    d.coupling, kernel_variant(d, tight), cap)
+                                 : 0;
+            Layout lay{L, pers, smem, (cap > 0 && cap < occ && smem > 0) ? cap : occ, tight};
             {
                 std::lock_guard<std::mutex> lock(ctx->mu);
                 ctx->tune[key] = lay;

@@ -15,7 +15,15 @@ keys = [
     ("Kernel Name", "kernel"),
     ("gpu__time_duration.sum", "duration"),
     ("launch__registers_per_thread", "regs/thread"),
+    ("launch__block_size", "block size"),
+    ("launch__grid_size", "grid size"),
+    ("launch__shared_mem_per_block_static", "smem static"),
+    ("launch__shared_mem_per_block_dynamic", "smem dynamic"),
     ("launch__occupancy_limit_registers", "CTA limit (regs)"),
+    ("launch__occupancy_limit_shared_mem", "CTA limit (smem)"),
+    ("launch__occupancy_limit_warps", "CTA limit (warps)"),
+    ("launch__occupancy_limit_blocks", "CTA limit (blocks)"),
+    ("sm__maximum_warps_per_active_cycle_pct", "theoretical occupancy %"),
     ("sm__warps_active.avg.pct_of_peak_sustained_active", "warps active %"),
     ("launch__waves_per_multiprocessor", "waves/SM"),
     ("sm__inst_executed.sum.pct_of_peak_sustained_elapsed", "issue % (elapsed)"),
