@@ -102,9 +102,9 @@ TEMPLATES = {
 }
 
 
-SINCOS_OPS = 15      # csrc/sdeb_math.cuh sincos_tab: 5 reduction + 6 poly + 4 rotation
-SIN_OPS = 13         # the same when only sin is used (the cos rotation is dead code)
-BOX_MULLER_PAIR = 37  # uniform 1, log 13, -2*log 1, sqrt 8, angle from the word 2, sincos poly+rotation 10, 2 products
+SINCOS_OPS = 14      # csrc/sdeb_math.cuh sincos_tab: 4 reduction + 6 poly + 4 rotation
+SIN_OPS = 12         # the same when only sin is used (the cos rotation is dead code)
+BOX_MULLER_PAIR = 36  # uniform 1, -2*log 13 (the -2 folded into the table), sqrt 8, angle from the word 2, sincos poly+rotation 10, 2 products
 
 
 def template_fp64_ops(n: int, model: str, coupling: str = "meanfield") -> float:

@@ -36,8 +36,9 @@ enum MathConst : int {
     MC_S1, MC_S2, MC_S3, MC_S4, MC_S5, MC_S6,  // fdlibm k_sin.c (|r| <= pi/4)
     MC_C1, MC_C2, MC_C3, MC_C4, MC_C5, MC_C6,  // fdlibm k_cos.c
     MC_TWO_OVER_PI, MC_PIO2_1, MC_PIO2_2, MC_PIO2_3,
-    MC_LN2_HI, MC_LN2_LO, MC_U32_BIAS, MC_INV7, MC_NEG_INV6, MC_INV5, MC_INV3,
-    MC_TAB_OVER_PI, MC_PITAB_1, MC_PITAB_2, MC_PITAB_3,  // table sincos reduction (pi/512)
+    MC_M2LN2_HI, MC_M2LN2_LO, MC_U32_BIAS,               // -2 ln 2 split; uniform bias
+    MC_LB5, MC_LB4, MC_LB3, MC_LB1,                      // -2 log1p series in -2r (neg2_log_pos)
+    MC_TAB_OVER_PI, MC_PITAB_1, MC_PITAB_2,              // table sincos reduction (pi/512)
     MC_T_S3, MC_T_S5, MC_T_C4,                           // Taylor terms on |r| <= pi/1024
     MC_TURN_BIAS, MC_TWO_PI_2M32,                        // Box-Muller angle (sincos_turn)
     MC_COUNT
@@ -52,14 +53,14 @@ __constant__ static double kMC[MC_COUNT] = {  // non-const: keeps ptxas from fol
     1.5707963267948966,          // fl(pi/2)
     6.123233995736766e-17,       // fl(pi/2 - fl(pi/2))
     -1.4973849048591698e-33,     // next 53 bits of pi/2
-    6.93147180559945286227e-01,  // fl(ln 2)
-    2.31904681384629955842e-17,  // fl(ln 2 - fl(ln 2))
+    -2 * 6.93147180559945286227e-01,  // -2 fl(ln 2) (exact scaling)
+    -2 * 2.31904681384629955842e-17,  // -2 fl(ln 2 - fl(ln 2))
     1048576.0 - 2.3283064365386963e-10,  // 2^20 - 2^-32 (exact)
-    0.14285714285714285, -0.16666666666666666, 0.2, 0.3333333333333333,
+    0.14285714285714285 / 64, 0.16666666666666666 / 32,  // fl(1/7) 2^-6, fl(1/6) 2^-5
+    0.2 / 16, 0.3333333333333333 / 4,                     // fl(1/5) 2^-4, fl(1/3) 2^-2
     162.97466172610083,          // 512/pi = 4 * fl(128/pi) (exact scaling)
     0.006135923151542565,        // fl(pi/512) = fl(pi) * 2^-9
-    2.391888279584674e-19,       // (pi - fl(pi))_hi * 2^-9
-    -5.849159784606132e-36,      // next 53 bits * 2^-9
+    2.391888279584674e-19,       // fl(pi/512 - fl(pi/512)) (pi/512 = PITAB_1 + PITAB_2 + O(2^-115))
     -0.16666666666666666, 0.008333333333333333,  // -1/6, 1/120
     0.041666666666666664,                        // 1/24
     4503601774854144.0,                          // 2^52 + 2^31 (biased int -> double)
@@ -160,9 +161,10 @@ __device__ __forceinline__ void sincos_tab(double x, double& s, double& c) {
     const double t = __fma_rn(x, kMC[MC_TAB_OVER_PI], kRoundMagic);
     const int k = __double2loint(t);
     const double kd = __dsub_rn(t, kRoundMagic);
+    // two-part Cody-Waite: the split's own error, |kd| * O(2^-115) < 2^-76 for
+    // |x| < 2^29, is far below the result's ulp (a third part bought nothing)
     double r = __fma_rn(-kd, kMC[MC_PITAB_1], x);
     r = __fma_rn(-kd, kMC[MC_PITAB_2], r);
-    r = __fma_rn(-kd, kMC[MC_PITAB_3], r);
     const double2 e = sincos_entry(k);
     const double r2 = __dmul_rn(r, r);
     const double ps = __fma_rn(r2, kMC[MC_T_S5], kMC[MC_T_S3]);
@@ -236,27 +238,34 @@ __device__ __forceinline__ void sincos_vec(const double (&x)[J], double (&s)[J],
     }
 }
 
-// ln(x) for a positive normal double.
-__device__ __forceinline__ double log_pos(double x) {
+// -2 ln(x) for a positive normal double: the Box-Muller radius argument
+// (rng.py:179, -2.0 * log(u)) with the -2 folded into the table and the
+// series.  x = 2^k z, z near c_i; the table holds (-2 invc_i, -2 logc_i) and
+// r' = fma(z, -2 invc, 2) = -2 r exactly, where r = z invc - 1 (|r| < 2^-7).
+// In Horner form every intermediate of the series in r' is the series in r
+// scaled by a power of two (coefficients a_i (-1/2)^(i+1)), so rounding
+// commutes with the scaling and the result equals fl(-2 * ln_table(x)) bit
+// for bit -- one DMUL cheaper than scaling afterwards.
+__device__ __forceinline__ double neg2_log_pos(double x) {
     const uint64_t ix = uint64_t(__double_as_longlong(x));
     const uint64_t tmp = ix - kLogOff;
     const int i = int((tmp >> (52 - kLogTableBits)) & ((1u << kLogTableBits) - 1));
     const int64_t k = int64_t(tmp) >> 52;
     const double z = __longlong_as_double((long long)(ix - (tmp & (0xFFFull << 52))));
-    const double2 e = log_entry(i);  // (invc, logc)
-    const double r = __fma_rn(z, e.x, -1.0);
+    const double2 e = log_entry(i);  // (-2 invc, -2 logc)
+    const double r = __fma_rn(z, e.x, 2.0);  // -2 (z invc - 1)
     const double kd = __dsub_rn(__longlong_as_double((long long)(0x4338000000000000ll + k)),
                                 kRoundMagic);
-    // log1p(r) = r - r^2/2 + r^3/3 - ... - r^8/8, |r| < 2^-7
-    double p = __fma_rn(r, -0.125, kMC[MC_INV7]);
-    p = __fma_rn(r, p, kMC[MC_NEG_INV6]);
-    p = __fma_rn(r, p, kMC[MC_INV5]);
-    p = __fma_rn(r, p, -0.25);
-    p = __fma_rn(r, p, kMC[MC_INV3]);
-    p = __fma_rn(r, p, -0.5);
+    // -2 log1p(r/(-2)) = r' + r'^2 (1/4 + r'/12 + r'^2/32 + ...), |r'| < 2^-6
+    double p = __fma_rn(r, 0.0009765625, kMC[MC_LB5]);
+    p = __fma_rn(r, p, kMC[MC_LB4]);
+    p = __fma_rn(r, p, kMC[MC_LB3]);
+    p = __fma_rn(r, p, 0.03125);
+    p = __fma_rn(r, p, kMC[MC_LB1]);
+    p = __fma_rn(r, p, 0.25);
     const double lp = __fma_rn(__dmul_rn(r, r), p, r);
-    const double hi = __fma_rn(kd, kMC[MC_LN2_HI], e.y);
-    const double lo = __fma_rn(kd, kMC[MC_LN2_LO], lp);
+    const double hi = __fma_rn(kd, kMC[MC_M2LN2_HI], e.y);
+    const double lo = __fma_rn(kd, kMC[MC_M2LN2_LO], lp);
     return __dadd_rn(hi, lo);
 }
 

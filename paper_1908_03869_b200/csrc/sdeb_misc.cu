@@ -145,7 +145,7 @@ __global__ void math_probe_kernel(int func, const double* __restrict__ x, int64_
     switch (func) {
         case 0: sincos_any(v, s, c); r = s; break;
         case 1: sincos_any(v, s, c); r = c; break;
-        case 2: r = log_pos(v); break;
+        case 2: r = __dmul_rn(-0.5, neg2_log_pos(v)); break;  // exact rescale
         case 3: r = sqrt_nonneg(v); break;
         case 4: r = sin(v); break;
         case 5: r = cos(v); break;

@@ -53,7 +53,7 @@ __device__ __forceinline__ double to_uniform(uint32_t w) { return u32_to_uniform
 // is reduced in integer arithmetic from the word itself (sincos_turn).
 __device__ __forceinline__ void box_muller_pair(uint32_t wa, uint32_t wb, double& z0, double& z1) {
     const double ua = u32_to_uniform(wa);
-    const double r = sqrt_nonneg(__dmul_rn(-2.0, log_pos(ua)));
+    const double r = sqrt_nonneg(neg2_log_pos(ua));  // sqrt(-2 ln u)
     double s, c;
     sincos_turn(wb, s, c);
     z0 = __dmul_rn(r, c);

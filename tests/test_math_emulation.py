@@ -73,23 +73,51 @@ def emu_sincos(x):
     return s, c
 
 
-def emu_log(x):
+def emu_neg2_log(x):
+    """neg2_log_pos (sdeb_math.cuh): -2 ln x from the pre-scaled table."""
     ix = _bits(x)
     tmp = (ix - 0x3FE6000000000000) & (2 ** 64 - 1)
     i = (tmp >> 45) & 127
     k = (tmp - (2 ** 64 if tmp >= 2 ** 63 else 0)) >> 52
     z = _dbl(ix - (tmp & (0xFFF << 52)))
-    invc, logc = TAB[i]
+    m2invc, m2logc = TAB[i]
+    r = fma(z, m2invc, 2.0)
+    p = fma(r, 2.0 ** -10, C["MC_LB5"])
+    p = fma(r, p, C["MC_LB4"])
+    p = fma(r, p, C["MC_LB3"])
+    p = fma(r, p, 2.0 ** -5)
+    p = fma(r, p, C["MC_LB1"])
+    p = fma(r, p, 0.25)
+    lp = fma(r * r, p, r)
+    hi = fma(float(k), C["MC_M2LN2_HI"], m2logc)
+    lo = fma(float(k), C["MC_M2LN2_LO"], lp)
+    return hi + lo
+
+
+def emu_log(x):
+    return -0.5 * emu_neg2_log(x)  # exact rescale (the math probe's log)
+
+
+def emu_log_unscaled(x):
+    """The same table log written in r = z invc - 1 with the unscaled table
+    (invc, logc) and series 1/7, -1/6, ...: neg2_log_pos must equal -2 times
+    this bit for bit (every intermediate is a power-of-two scaling)."""
+    ix = _bits(x)
+    tmp = (ix - 0x3FE6000000000000) & (2 ** 64 - 1)
+    i = (tmp >> 45) & 127
+    k = (tmp - (2 ** 64 if tmp >= 2 ** 63 else 0)) >> 52
+    z = _dbl(ix - (tmp & (0xFFF << 52)))
+    invc, logc = -0.5 * TAB[i][0], -0.5 * TAB[i][1]
     r = fma(z, invc, -1.0)
-    p = fma(r, -0.125, C["MC_INV7"])
-    p = fma(r, p, C["MC_NEG_INV6"])
-    p = fma(r, p, C["MC_INV5"])
+    p = fma(r, -0.125, 1.0 / 7.0)
+    p = fma(r, p, -1.0 / 6.0)
+    p = fma(r, p, 0.2)
     p = fma(r, p, -0.25)
-    p = fma(r, p, C["MC_INV3"])
+    p = fma(r, p, 1.0 / 3.0)
     p = fma(r, p, -0.5)
     lp = fma(r * r, p, r)
-    hi = fma(float(k), C["MC_LN2_HI"], logc)
-    lo = fma(float(k), C["MC_LN2_LO"], lp)
+    hi = fma(float(k), math.log(2.0), logc)
+    lo = fma(float(k), 2.31904681384629955842e-17, lp)
     return hi + lo
 
 
@@ -101,9 +129,11 @@ def test_constants_are_the_intended_values():
     assert C["MC_PIO2_1"] + C["MC_PIO2_2"] == C["MC_PIO2_1"]
     assert Fraction(C["MC_PIO2_1"]) + Fraction(C["MC_PIO2_2"]) + Fraction(C["MC_PIO2_3"]) \
         != Fraction(C["MC_PIO2_1"])
-    assert C["MC_LN2_HI"] == math.log(2.0)
+    assert C["MC_M2LN2_HI"] == -2.0 * math.log(2.0)
+    assert C["MC_LB5"] == (1.0 / 7.0) / 64 and C["MC_LB4"] == (1.0 / 6.0) / 32
+    assert C["MC_LB3"] == 0.2 / 16 and C["MC_LB1"] == (1.0 / 3.0) / 4
     assert C["MC_U32_BIAS"] == 2.0 ** 20 - 2.0 ** -32
-    assert len(TAB) == 128 and TAB[79] == (1.0, 0.0) and TAB[80] == (1.0, 0.0)
+    assert len(TAB) == 128 and TAB[79] == (-2.0, 0.0) and TAB[80] == (-2.0, 0.0)  # -2 (invc, logc)
 
 
 def test_uniform_map_is_exact():
@@ -152,7 +182,6 @@ def emu_sincos_tab(x):
     kd = t - MAGIC
     r = fma(-kd, C["MC_PITAB_1"], x)
     r = fma(-kd, C["MC_PITAB_2"], r)
-    r = fma(-kd, C["MC_PITAB_3"], r)
     sa, ca = SCT[k & (len(SCT) - 1)]
     r2 = r * r
     ps = fma(r2, C["MC_T_S5"], C["MC_T_S3"])
@@ -166,8 +195,8 @@ def test_table_sincos_constants():
     from decimal import Decimal, getcontext
     getcontext().prec = 50
     pi = Decimal("3.14159265358979323846264338327950288419716939937510582097494")
-    split = Decimal(C["MC_PITAB_1"]) + Decimal(C["MC_PITAB_2"]) + Decimal(C["MC_PITAB_3"])
-    assert abs(split - pi / 512) < Decimal(10) ** -47
+    split = Decimal(C["MC_PITAB_1"]) + Decimal(C["MC_PITAB_2"])
+    assert abs(split - pi / 512) < Decimal(10) ** -34  # |kd| * err < 2^-76 for |x| < 2^29
     assert C["MC_PITAB_1"] == math.pi / 512 and C["MC_TAB_OVER_PI"] == 512 / math.pi
     assert len(SCT) == 1024 and SCT[0] == (0.0, 1.0) and SCT[256] == (1.0, 0.0)
     for k in range(1, 1024):
@@ -216,3 +245,11 @@ def test_box_muller_angle_reduction():
         ang = 2.0 * math.pi * ((w + 1.0) * 2.0 ** -32)
         s, c = emu_sincos_turn(w)
         assert abs(s - math.sin(ang)) <= 8e-16 and abs(c - math.cos(ang)) <= 8e-16, w
+
+
+def test_neg2_log_is_exact_power_of_two_scaling():
+    g = np.random.default_rng(11)
+    words = list(g.integers(0, 2 ** 32, 4000)) + [0, 1, 2 ** 31, 2 ** 32 - 2, 2 ** 32 - 1]
+    xs = [(int(w) + 1.0) * 2.0 ** -32 for w in words] + list(g.uniform(1e-3, 1e3, 2000))
+    for x in xs:
+        assert emu_neg2_log(x) == -2.0 * emu_log_unscaled(x), x
