@@ -104,7 +104,7 @@ TEMPLATES = {
 
 SINCOS_OPS = 14      # csrc/sdeb_math.cuh sincos_tab: 4 reduction + 6 poly + 4 rotation
 SIN_OPS = 12         # the same when only sin is used (the cos rotation is dead code)
-BOX_MULLER_PAIR = 36  # uniform 1, -2*log 13 (the -2 folded into the table), sqrt 8, angle from the word 2, sincos poly+rotation 10, 2 products
+BOX_MULLER_PAIR = 34  # uniform 1, -2*log 11 (the -2 folded into the table), sqrt 8, angle from the word 2, sincos poly+rotation 10, 2 products
 
 
 def template_fp64_ops(n: int, model: str, coupling: str = "meanfield") -> float:
@@ -126,15 +126,15 @@ def template_fp64_ops(n: int, model: str, coupling: str = "meanfield") -> float:
 def algorithmic_fp64_ops(n: int, solver: str, coupling: str) -> float:
     """FP64 lane-ops (DFMA/DMUL/DADD) per orbit-step of the algorithm the
     kernel runs, counted from the device code:
-    meanfield sums 20/oscillator (sincos 15, tree sums 2, S_i 3) and, for em,
-    the folded update 4 (fma(K/n*dt, S, omega*dt), 2 adds, (sqrt(dt)*s)*N) +
-    Box-Muller 42 per pair of normals; other solvers f_i = omega + K/n*S 2 more;
-    pairwise 16 per unordered pair (difference, sin 13, 2 accumulates) + 2/osc
+    meanfield sums 19/oscillator (sincos 14, tree sums 2, S_i 3) and, for em,
+    the folded update 3 (fma(K/n*dt, S, omega*dt), 1 add, fma((sqrt(dt)*s), N, .)) +
+    Box-Muller 34 per pair of normals; other solvers f_i = omega + K/n*S 2 more;
+    pairwise 15 per unordered pair (difference, sin 12, 2 accumulates) + 2/osc
     and the unfolded em update 5; RK4 4 drifts + 13/osc."""
     if coupling == "meanfield":
         sums = n * (SINCOS_OPS + 2 + 3)
         if solver == "em":
-            return sums + n * (4 + BOX_MULLER_PAIR / 2)
+            return sums + n * (3 + BOX_MULLER_PAIR / 2)
         drift = sums + 2 * n
     else:
         drift = n * (n - 1) / 2 * (1 + SIN_OPS + 2) + n * 2

@@ -405,15 +405,16 @@ __device__ __forceinline__ void run_item(const RunArgs& a, int64_t cg, uint64_t 
                 double f[J];
                 if constexpr (kStochastic && COUPLING == KC_MEANFIELD) {
                     // the meanfield form, with the step constants folded:
-                    // (y + (omega*dt + (K/n*dt)*S)) + (sqrt(dt)*s_i)*N_i -- the
-                    // reference's (y + f*dt) + sqrt(dt)*(s_i*N_i) reassociated
-                    // (a few ulp per step), 4 FP64 ops instead of 7
+                    // fma(sqrt(dt)*s_i, N_i, y + (omega*dt + (K/n*dt)*S)) -- the
+                    // reference's (y + f*dt) + sqrt(dt)*(s_i*N_i) reassociated,
+                    // the noise product unrounded (a few ulp per step, DESIGN.md
+                    // 4), 3 FP64 ops instead of 7
                     double S[J];
                     meanfield_sums<J, PADDED>(y, base, n, lanes, S);
                     step_noise_apply<J, STREAM, PADDED>(
                         a, row, orbit_g, step, base, rs, [&](int q, double z) {
-                            y[q] = __dadd_rn(__dadd_rn(y[q], __fma_rn(kndt, S[q], omdt[q])),
-                                             __dmul_rn(sgs[q], z));
+                            y[q] = __fma_rn(sgs[q], z,
+                                            __dadd_rn(y[q], __fma_rn(kndt, S[q], omdt[q])));
                         });
                 } else if constexpr (kStochastic) {
                     drift<J, COUPLING, PADDED>(y, om, kn, base, n, lanes, sh, shs, f);

@@ -37,7 +37,7 @@ enum MathConst : int {
     MC_C1, MC_C2, MC_C3, MC_C4, MC_C5, MC_C6,  // fdlibm k_cos.c
     MC_TWO_OVER_PI, MC_PIO2_1, MC_PIO2_2, MC_PIO2_3,
     MC_M2LN2_HI, MC_M2LN2_LO, MC_U32_BIAS,               // -2 ln 2 split; uniform bias
-    MC_LB5, MC_LB4, MC_LB3, MC_LB1,                      // -2 log1p series in -2r (neg2_log_pos)
+    MC_LB4, MC_LB3, MC_LB1,                              // -2 log1p series in -2r (neg2_log_pos)
     MC_TAB_OVER_PI, MC_PITAB_1, MC_PITAB_2,              // table sincos reduction (pi/512)
     MC_T_S3, MC_T_S5, MC_T_C4,                           // Taylor terms on |r| <= pi/1024
     MC_TURN_BIAS, MC_TWO_PI_2M32,                        // Box-Muller angle (sincos_turn)
@@ -56,7 +56,7 @@ __constant__ static double kMC[MC_COUNT] = {  // non-const: keeps ptxas from fol
     -2 * 6.93147180559945286227e-01,  // -2 fl(ln 2) (exact scaling)
     -2 * 2.31904681384629955842e-17,  // -2 fl(ln 2 - fl(ln 2))
     1048576.0 - 2.3283064365386963e-10,  // 2^20 - 2^-32 (exact)
-    0.14285714285714285 / 64, 0.16666666666666666 / 32,  // fl(1/7) 2^-6, fl(1/6) 2^-5
+    0.16666666666666666 / 32,                             // fl(1/6) 2^-5
     0.2 / 16, 0.3333333333333333 / 4,                     // fl(1/5) 2^-4, fl(1/3) 2^-2
     162.97466172610083,          // 512/pi = 4 * fl(128/pi) (exact scaling)
     0.006135923151542565,        // fl(pi/512) = fl(pi) * 2^-9
@@ -241,7 +241,7 @@ __device__ __forceinline__ void sincos_vec(const double (&x)[J], double (&s)[J],
 // -2 ln(x) for a positive normal double: the Box-Muller radius argument
 // (rng.py:179, -2.0 * log(u)) with the -2 folded into the table and the
 // series.  x = 2^k z, z near c_i; the table holds (-2 invc_i, -2 logc_i) and
-// r' = fma(z, -2 invc, 2) = -2 r exactly, where r = z invc - 1 (|r| < 2^-7).
+// r' = fma(z, -2 invc, 2) = -2 r exactly, where r = z invc - 1 (|r| <= 2^-9).
 // In Horner form every intermediate of the series in r' is the series in r
 // scaled by a power of two (coefficients a_i (-1/2)^(i+1)), so rounding
 // commutes with the scaling and the result equals fl(-2 * ln_table(x)) bit
@@ -256,10 +256,9 @@ __device__ __forceinline__ double neg2_log_pos(double x) {
     const double r = __fma_rn(z, e.x, 2.0);  // -2 (z invc - 1)
     const double kd = __dsub_rn(__longlong_as_double((long long)(0x4338000000000000ll + k)),
                                 kRoundMagic);
-    // -2 log1p(r/(-2)) = r' + r'^2 (1/4 + r'/12 + r'^2/32 + ...), |r'| < 2^-6
-    double p = __fma_rn(r, 0.0009765625, kMC[MC_LB5]);
-    p = __fma_rn(r, p, kMC[MC_LB4]);
-    p = __fma_rn(r, p, kMC[MC_LB3]);
+    // -2 log1p(r'/(-2)) = r' + r'^2 (1/4 + r'/12 + r'^2/32 + r'^3/80 + r'^4/192),
+    // |r'| <= 2^-8: the next term is < 2^-56.8 relative (tools/gen_log_table.py)
+    double p = __fma_rn(r, kMC[MC_LB4], kMC[MC_LB3]);
     p = __fma_rn(r, p, 0.03125);
     p = __fma_rn(r, p, kMC[MC_LB1]);
     p = __fma_rn(r, p, 0.25);

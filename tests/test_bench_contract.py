@@ -28,11 +28,11 @@ def test_reference_arm_json_line():
 def test_algorithmic_counts():
     sys.path.insert(0, ROOT)
     import bench
-    # meanfield em: sincos 14 + sums 2 + S 3 + folded update 4 + Box-Muller 36 / 2
-    assert bench.algorithmic_fp64_ops(16, "em", "meanfield") == 16 * (14 + 2 + 3 + 4 + 18)
+    # meanfield em: sincos 14 + sums 2 + S 3 + folded update 3 + Box-Muller 34 / 2
+    assert bench.algorithmic_fp64_ops(16, "em", "meanfield") == 16 * (14 + 2 + 3 + 3 + 17)
     assert bench.algorithmic_fp64_ops(8, "rk4", "meanfield") == 4 * 8 * 21 + 8 * 13
-    assert bench.template_fp64_ops(4, "ou") == 4 * (2 + 1 + 18 + 4)
+    assert bench.template_fp64_ops(4, "ou") == 4 * (2 + 1 + 17 + 4)
     assert bench.template_fp64_ops(16, "kuramoto_template", "pairwise") == \
-        16 * 16 * 14 + 16 * (3 + 1 + 18 + 4)
+        16 * 16 * 14 + 16 * (3 + 1 + 17 + 4)
     assert set(bench.WORKLOADS) >= {"cfg1", "cfg2", "cfg3_n32", "cfg3_n256", "cfg4", "cfg5",
                                     "cfg5_coherence", "cfg2_codegen", "ou_codegen"}

@@ -77,14 +77,12 @@ def emu_neg2_log(x):
     """neg2_log_pos (sdeb_math.cuh): -2 ln x from the pre-scaled table."""
     ix = _bits(x)
     tmp = (ix - 0x3FE6000000000000) & (2 ** 64 - 1)
-    i = (tmp >> 45) & 127
+    i = (tmp >> 43) & 511
     k = (tmp - (2 ** 64 if tmp >= 2 ** 63 else 0)) >> 52
     z = _dbl(ix - (tmp & (0xFFF << 52)))
     m2invc, m2logc = TAB[i]
     r = fma(z, m2invc, 2.0)
-    p = fma(r, 2.0 ** -10, C["MC_LB5"])
-    p = fma(r, p, C["MC_LB4"])
-    p = fma(r, p, C["MC_LB3"])
+    p = fma(r, C["MC_LB4"], C["MC_LB3"])
     p = fma(r, p, 2.0 ** -5)
     p = fma(r, p, C["MC_LB1"])
     p = fma(r, p, 0.25)
@@ -104,14 +102,12 @@ def emu_log_unscaled(x):
     this bit for bit (every intermediate is a power-of-two scaling)."""
     ix = _bits(x)
     tmp = (ix - 0x3FE6000000000000) & (2 ** 64 - 1)
-    i = (tmp >> 45) & 127
+    i = (tmp >> 43) & 511
     k = (tmp - (2 ** 64 if tmp >= 2 ** 63 else 0)) >> 52
     z = _dbl(ix - (tmp & (0xFFF << 52)))
     invc, logc = -0.5 * TAB[i][0], -0.5 * TAB[i][1]
     r = fma(z, invc, -1.0)
-    p = fma(r, -0.125, 1.0 / 7.0)
-    p = fma(r, p, -1.0 / 6.0)
-    p = fma(r, p, 0.2)
+    p = fma(r, -1.0 / 6.0, 0.2)
     p = fma(r, p, -0.25)
     p = fma(r, p, 1.0 / 3.0)
     p = fma(r, p, -0.5)
@@ -130,10 +126,10 @@ def test_constants_are_the_intended_values():
     assert Fraction(C["MC_PIO2_1"]) + Fraction(C["MC_PIO2_2"]) + Fraction(C["MC_PIO2_3"]) \
         != Fraction(C["MC_PIO2_1"])
     assert C["MC_M2LN2_HI"] == -2.0 * math.log(2.0)
-    assert C["MC_LB5"] == (1.0 / 7.0) / 64 and C["MC_LB4"] == (1.0 / 6.0) / 32
+    assert C["MC_LB4"] == (1.0 / 6.0) / 32
     assert C["MC_LB3"] == 0.2 / 16 and C["MC_LB1"] == (1.0 / 3.0) / 4
     assert C["MC_U32_BIAS"] == 2.0 ** 20 - 2.0 ** -32
-    assert len(TAB) == 128 and TAB[79] == (-2.0, 0.0) and TAB[80] == (-2.0, 0.0)  # -2 (invc, logc)
+    assert len(TAB) == 512 and TAB[319] == (-2.0, 0.0) and TAB[320] == (-2.0, 0.0)  # -2 (invc, logc)
 
 
 def test_uniform_map_is_exact():
