@@ -110,11 +110,12 @@ BOX_MULLER_PAIR = 34  # uniform 1, -2*log 11 (the -2 folded into the table), sqr
 def template_fp64_ops(n: int, model: str, coupling: str = "meanfield") -> float:
     """FP64 lane-ops per orbit-step of the generated program (counted from the
     generated code).  Kuramoto templates, literal form (coupling="pairwise"):
-    n^2 terms x (difference 1, sin 13, sum 1); factored form (meanfield): one
-    sincos 15 + 2 sum adds per oscillator in the prologue (its (sin, cos)
-    kept for the equations), then per equation the addition formula 3.  Both: per equation p[0]/N, *, + 3,
-    diffusion product 1, noise 18.5, update 4.  OU per equation drift 2 +
-    diffusion 1 + noise 18.5 + update 4."""
+    n^2 terms x (difference 1, sin SIN_OPS, sum 1); factored form (meanfield):
+    one sincos (SINCOS_OPS) + 2 sum adds per oscillator in the prologue (its
+    (sin, cos) kept for the equations), then per equation the addition formula
+    3.  Both: per equation p[0]/N, *, + 3, diffusion product 1, noise
+    BOX_MULLER_PAIR / 2, update 4.  OU per equation drift 2 + diffusion 1 +
+    noise + update 4."""
     tail = 1 + BOX_MULLER_PAIR / 2 + 4
     if model == "kuramoto_template":
         if coupling == "meanfield":
@@ -125,21 +126,24 @@ def template_fp64_ops(n: int, model: str, coupling: str = "meanfield") -> float:
 
 def algorithmic_fp64_ops(n: int, solver: str, coupling: str) -> float:
     """FP64 lane-ops (DFMA/DMUL/DADD) per orbit-step of the algorithm the
-    kernel runs, counted from the device code:
-    meanfield sums 19/oscillator (sincos 14, tree sums 2, S_i 3) and, for em,
-    the folded update 3 (fma(K/n*dt, S, omega*dt), 1 add, fma((sqrt(dt)*s), N, .)) +
-    Box-Muller 34 per pair of normals; other solvers f_i = omega + K/n*S 2 more;
-    pairwise 15 per unordered pair (difference, sin 12, 2 accumulates) + 2/osc
-    and the unfolded em update 5; RK4 4 drifts + 13/osc."""
+    kernel runs, counted from the device code.
+    Meanfield: sincos 14 + tree sums 2 per oscillator.  em (folded): the two
+    scaled sums 2 per orbit, increment fma(cos, K/n dt sum sin, fma(-sin, .,
+    omega dt)) 2 and update fma(sqrt(dt) s, N, y + inc) 2 per oscillator, plus
+    Box-Muller 34 per pair of normals; rk4: 4 folded drifts (2 + 2/osc on the
+    sums) + 13/osc; euler: the exact drift (S_i 3, omega + K/n S 2) + update 2.
+    Pairwise: 15 per unordered pair (difference, sin 12, 2 accumulates) + 2/osc
+    and the unfolded em update 5."""
     if coupling == "meanfield":
-        sums = n * (SINCOS_OPS + 2 + 3)
+        sums = n * (SINCOS_OPS + 2)
         if solver == "em":
-            return sums + n * (3 + BOX_MULLER_PAIR / 2)
-        drift = sums + 2 * n
-    else:
-        drift = n * (n - 1) / 2 * (1 + SIN_OPS + 2) + n * 2
-        if solver == "em":
-            return drift + n * (5 + BOX_MULLER_PAIR / 2)
+            return sums + 2 + n * (2 + 2 + BOX_MULLER_PAIR / 2)
+        if solver == "rk4":
+            return 4 * (sums + 2 + 2 * n) + n * 13
+        return sums + n * (3 + 2) + n * 2
+    drift = n * (n - 1) / 2 * (1 + SIN_OPS + 2) + n * 2
+    if solver == "em":
+        return drift + n * (5 + BOX_MULLER_PAIR / 2)
     if solver == "rk4":
         return 4 * drift + n * 13
     return drift + n * 2

@@ -147,6 +147,34 @@ __device__ __forceinline__ void drift_meanfield(const double (&y)[J], const doub
     for (int q = 0; q < J; ++q) f[q] = __dadd_rn(om[q], __dmul_rn(kn, S[q]));
 }
 
+// The stepping form: c0_i + scale*S_i with the scale folded into the two
+// group sums, fma(cos y_i, scale*sum sin, fma(-sin y_i, scale*sum cos, c0_i))
+// -- 2 FP64 ops per oscillator instead of 4 (+2 per lane).  A reassociation
+// of the reference's (ω + (K/n) S) by a few ulp (folded
+// update); drift_eval keeps the exact form above.
+template <int J, bool PADDED>
+__device__ __forceinline__ void meanfield_folded(const double (&y)[J], const double (&c0)[J],
+                                                 double scale, int base, int n, int lanes,
+                                                 double (&out)[J]) {
+    double sn[J], cs[J], ts[J], tc[J];
+    sincos_vec<J>(y, sn, cs);
+#pragma unroll
+    for (int q = 0; q < J; ++q) {
+        if (PADDED && base + q >= n) {
+            sn[q] = 0.0;
+            cs[q] = 0.0;
+        }
+        ts[q] = sn[q];
+        tc[q] = cs[q];
+    }
+    double a = lane_tree_sum<J>(ts);
+    double b = lane_tree_sum<J>(tc);
+    group_sum2(a, b, lanes);
+    const double sa = __dmul_rn(scale, a), sb = __dmul_rn(scale, b);
+#pragma unroll
+    for (int q = 0; q < J; ++q) out[q] = __fma_rn(cs[q], sa, __fma_rn(-sn[q], sb, c0[q]));
+}
+
 // PAIRWISE: S_i = sum_{j=0}^{n-1} sin(fl(y_j - y_i)), accumulated in j order.
 // The group's state is staged in shared memory sh[q][tid] (conflict-free for
 // the owner).  L == 1 uses the antisymmetric tiling (each unordered pair
@@ -204,6 +232,18 @@ __device__ __forceinline__ void drift(const double (&y)[J], const double (&om)[J
                                       double (&f)[J]) {
     if constexpr (COUPLING == KC_MEANFIELD) {
         drift_meanfield<J, PADDED>(y, om, kn, base, n, lanes, f);
+    } else {
+        drift_pairwise<J>(y, om, kn, base, n, lanes, sh, shs, f);
+    }
+}
+
+// RK4 stage drift: the folded meanfield form, or the exact pairwise one.
+template <int J, int COUPLING, bool PADDED>
+__device__ __forceinline__ void rk4_drift(const double (&y)[J], const double (&om)[J], double kn,
+                                          int base, int n, int lanes, double* sh, double* shs,
+                                          double (&f)[J]) {
+    if constexpr (COUPLING == KC_MEANFIELD) {
+        meanfield_folded<J, PADDED>(y, om, kn, base, n, lanes, f);
     } else {
         drift_pairwise<J>(y, om, kn, base, n, lanes, sh, shs, f);
     }
@@ -407,14 +447,13 @@ __device__ __forceinline__ void run_item(const RunArgs& a, int64_t cg, uint64_t 
                     // the meanfield form, with the step constants folded:
                     // fma(sqrt(dt)*s_i, N_i, y + (omega*dt + (K/n*dt)*S)) -- the
                     // reference's (y + f*dt) + sqrt(dt)*(s_i*N_i) reassociated,
-                    // the noise product unrounded (a few ulp per step, DESIGN.md
-                    // 4), 3 FP64 ops instead of 7
-                    double S[J];
-                    meanfield_sums<J, PADDED>(y, base, n, lanes, S);
+                    // (K/n)*dt folded into the sums, the noise product unrounded
+                    // (a few ulp per step): 4 FP64 ops instead of 10
+                    double inc[J];
+                    meanfield_folded<J, PADDED>(y, omdt, kndt, base, n, lanes, inc);
                     step_noise_apply<J, STREAM, PADDED>(
                         a, row, orbit_g, step, base, rs, [&](int q, double z) {
-                            y[q] = __fma_rn(sgs[q], z,
-                                            __dadd_rn(y[q], __fma_rn(kndt, S[q], omdt[q])));
+                            y[q] = __fma_rn(sgs[q], z, __dadd_rn(y[q], inc[q]));
                         });
                 } else if constexpr (kStochastic) {
                     drift<J, COUPLING, PADDED>(y, om, kn, base, n, lanes, sh, shs, f);
@@ -432,25 +471,25 @@ __device__ __forceinline__ void run_item(const RunArgs& a, int64_t cg, uint64_t 
                 }
             } else {  // KS_RK4 (solvers.py:80-88)
                 double k[J], acc[J], ys[J];
-                drift<J, COUPLING, PADDED>(y, om, kn, base, n, lanes, sh, shs, k);  // k1
+                rk4_drift<J, COUPLING, PADDED>(y, om, kn, base, n, lanes, sh, shs, k);  // k1
 #pragma unroll
                 for (int q = 0; q < J; ++q) {
                     acc[q] = k[q];
                     ys[q] = __dadd_rn(y[q], __dmul_rn(a.half_dt, k[q]));
                 }
-                drift<J, COUPLING, PADDED>(ys, om, kn, base, n, lanes, sh, shs, k);  // k2
+                rk4_drift<J, COUPLING, PADDED>(ys, om, kn, base, n, lanes, sh, shs, k);  // k2
 #pragma unroll
                 for (int q = 0; q < J; ++q) {
                     acc[q] = __dadd_rn(acc[q], __dmul_rn(2.0, k[q]));
                     ys[q] = __dadd_rn(y[q], __dmul_rn(a.half_dt, k[q]));
                 }
-                drift<J, COUPLING, PADDED>(ys, om, kn, base, n, lanes, sh, shs, k);  // k3
+                rk4_drift<J, COUPLING, PADDED>(ys, om, kn, base, n, lanes, sh, shs, k);  // k3
 #pragma unroll
                 for (int q = 0; q < J; ++q) {
                     acc[q] = __dadd_rn(acc[q], __dmul_rn(2.0, k[q]));
                     ys[q] = __dadd_rn(y[q], __dmul_rn(dt, k[q]));
                 }
-                drift<J, COUPLING, PADDED>(ys, om, kn, base, n, lanes, sh, shs, k);  // k4
+                rk4_drift<J, COUPLING, PADDED>(ys, om, kn, base, n, lanes, sh, shs, k);  // k4
 #pragma unroll
                 for (int q = 0; q < J; ++q) {
                     acc[q] = __dadd_rn(acc[q], k[q]);

@@ -28,9 +28,10 @@ def test_reference_arm_json_line():
 def test_algorithmic_counts():
     sys.path.insert(0, ROOT)
     import bench
-    # meanfield em: sincos 14 + sums 2 + S 3 + folded update 3 + Box-Muller 34 / 2
-    assert bench.algorithmic_fp64_ops(16, "em", "meanfield") == 16 * (14 + 2 + 3 + 3 + 17)
-    assert bench.algorithmic_fp64_ops(8, "rk4", "meanfield") == 4 * 8 * 21 + 8 * 13
+    # meanfield em: sincos 14 + sums 2 + increment 2 + update 2 + Box-Muller 34 / 2,
+    # and the two scaled sums per orbit
+    assert bench.algorithmic_fp64_ops(16, "em", "meanfield") == 16 * (14 + 2 + 2 + 2 + 17) + 2
+    assert bench.algorithmic_fp64_ops(8, "rk4", "meanfield") == 4 * (8 * 18 + 2) + 8 * 13
     assert bench.template_fp64_ops(4, "ou") == 4 * (2 + 1 + 17 + 4)
     assert bench.template_fp64_ops(16, "kuramoto_template", "pairwise") == \
         16 * 16 * 14 + 16 * (3 + 1 + 17 + 4)
