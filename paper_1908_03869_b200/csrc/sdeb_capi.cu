@@ -789,7 +789,7 @@ class CopyPool {
 // globally visible before the pool reports the job done.
 template <class F>
 void parallel_rows(int64_t rows, size_t bytes, int threads, F&& fn) {
-    const int64_t want = std::min<int64_t>(threads, int64_t(bytes >> 20));  // >= 1 MiB each
+    const int64_t want = std::min<int64_t>(threads, int64_t(bytes >> 18));  // >= 256 KiB each
     const int nt = int(std::max<int64_t>(1, std::min<int64_t>(want, rows)));
     auto part = [&](int t) {
         fn(rows * t / nt, rows * (t + 1) / nt);
@@ -980,9 +980,12 @@ sdb_status run_shard(sdb_ctx* ctx, Slot& s, sdb_desc d, sdb_model* m, int64_t r0
 
     // Destination prefault (see prefault_range): while the next piece's DMA
     // (or the kernel before it) is still running, fault in the store pages of
-    // rows no drain has reached yet, 32 MiB at a time.  SDEB200_PREFAULT=0 off.
+    // rows no drain has reached yet, 32 MiB at a time (stores >= 4 MiB).
+    // SDEB200_PREFAULT=0 turns it off.
     const int64_t row_words = out_mode ? width : (k + 1) * n;
-    const bool prefault = values && nt_out && env_int("SDEB200_PREFAULT", 1) != 0;
+    const size_t store_bytes = size_t(rows) * size_t(row_words) * sizeof(double);
+    const bool prefault =
+        values && store_bytes >= (size_t(4) << 20) && env_int("SDEB200_PREFAULT", 1) != 0;
     const int64_t pf_rows = std::max<int64_t>(1, int64_t((size_t(32) << 20) / (row_words * 8)));
     int64_t pf_next = 0;  // shard-local rows below this are populated (or drained)
     double prefault_ms = 0.0;
