@@ -533,7 +533,11 @@ int state_words(const sdb_model* m) {
 // sums: there the O(N^2) table reads per step compete with the state-column
 // reads for the shared-memory pipe (measured: Kuramoto templates 2.44e9 ->
 // 1.53e9 orbit-steps/s staged; the OU template 1.94e10 -> 2.26e10).
-bool stage_tables(const sdb_model* m, bool factor) { return !m->eq_sum[factor ? 1 : 0]; }
+bool stage_tables(const sdb_model* m, bool factor) {
+    // SDEB200_DSL_SMEM_TABLES=0/1 overrides (experiments)
+    if (const char* e = std::getenv("SDEB200_DSL_SMEM_TABLES")) return std::atoi(e) != 0;
+    return !m->eq_sum[factor ? 1 : 0];
+}
 
 int lanes_for(const sdb_model* m, bool factor) {
     if (const char* e = std::getenv("SDEB200_DSL_LANES")) {
