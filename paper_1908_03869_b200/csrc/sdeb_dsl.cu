@@ -1,5 +1,7 @@
 // Expression templates -> CUDA -> NVRTC (see sdeb_dsl.h).
 #include "sdeb_dsl.h"
+#include "sdeb_log_table.cuh"
+#include "sdeb_sincos_table.cuh"
 
 #include <nvrtc.h>
 
@@ -523,6 +525,9 @@ sdb_model::~sdb_model() {
 }
 
 namespace sdeb_dsl {
+
+static_assert(kTableSmem == 16 * (sdeb::kSinCosN + (1 << sdeb::kLogTableBits)),
+              "kTableSmem must match the staged tables (sdeb_math.cuh)");
 
 int state_words(const sdb_model* m) {
     const int nb = (m->nnoise + 3) / 4;

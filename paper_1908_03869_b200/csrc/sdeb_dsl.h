@@ -58,7 +58,7 @@ cudaError_t launch(sdb_model* m, int kind, const sdeb::DslArgs& a, cudaStream_t 
 
 constexpr int kBlock = 128;      // threads per CTA = 128 / lanes orbit slots
 constexpr int kSmemMax = 96 * 1024;
-constexpr size_t kTableSmem = 16 * (1024 + 128);  // sincos + log tables staged by the program
+constexpr size_t kTableSmem = 16 * (1024 + 512);  // sincos + log tables staged by the program
 constexpr int kUnrollWork = 32;  // unroll equation loops while (N / lanes) x evaluations <= this
 
 // Doubles per orbit in the shared column: y + one step's normals.
