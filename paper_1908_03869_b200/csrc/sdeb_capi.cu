@@ -872,8 +872,10 @@ int host_copy_threads(int /*shards*/) {
     const int hw = int(std::max(1u, std::thread::hardware_concurrency()));
     // every hardware thread, whatever the shard count: the copies are bound by
     // page faults / memory traffic (cfg3 n=256 e2e 393 -> 303 ms going from 8 to
-    // 16 threads on a 16-thread host), and the pool runs one piece at a time
-    return std::max(1, env_int("SDEB200_HOST_THREADS", std::min(32, hw)));
+    // 16 threads on a 16-thread host), and the pool runs one piece at a time.
+    // One process per GPU (torchrun sets LOCAL_WORLD_SIZE): a share each.
+    const int procs = std::max(1, env_int("LOCAL_WORLD_SIZE", 1));
+    return std::max(1, env_int("SDEB200_HOST_THREADS", std::min(32, std::max(1, hw / procs))));
 }
 
 // Orbit tiles of a host-buffer shard: copies of tile t+1 / t-1 overlap the
