@@ -395,6 +395,32 @@ def test_host_pipeline_tiling_bit_identical(stream, monkeypatch):
         assert np.array_equal(got.values[:, 0], batch.init)
 
 
+def test_host_pipeline_large_store_paths(monkeypatch):
+    # a store >= 64 MiB takes the streaming-store staging copies, the huge-page
+    # allocation and the destination prefault; an odd n makes every row start
+    # 8 bytes off a 16-byte boundary.  Same bits as the small-transfer path
+    # (plain memcpy into np.empty), reached by running orbit slices
+    n, m = 33, 13000
+    batch = sdb.sample_kuramoto_batch(n, m, (0.2, 0.4), (0.01, 0.1), 0.3, seed=21)
+    params = batch.params.copy()
+    params[7777, 1 + 3] = np.inf  # a failing orbit in the middle of a piece
+    batch = OrbitBatch(init=batch.init, params=params)
+    cfg = EngineConfig(dt=1e-2, tspan=0.2, ksteps=1, orbits=m, seed=4, stream="philox",
+                       max_store_bytes=1 << 34)
+    model = sdb.kuramoto_model(n)
+    big = run_batch(model, cfg, batch)
+    assert big.values.nbytes >= 64 << 20
+    assert big.failures and big.failures[0].orbit == 7777
+    monkeypatch.setenv("SDEB200_PREFAULT", "0")
+    assert sdb.store_hash(run_batch(model, cfg, batch)) == sdb.store_hash(big)
+    parts = []
+    for lo in range(0, m, 3250):
+        part = OrbitBatch(init=batch.init[lo:lo + 3250], params=batch.params[lo:lo + 3250])
+        parts.append(run_batch(model, dataclasses.replace(cfg, orbits=3250), part,
+                               orbit_offset=lo).values)
+    assert np.array_equal(np.concatenate(parts), big.values, equal_nan=True)
+
+
 @pytest.mark.parametrize("stream", ["philox", "sfc64"])
 def test_lane_layouts_bit_identical_huge_phases(stream):
     # phases beyond 2^29 take the exact (Payne-Hanek) reduction branch; it must
