@@ -959,9 +959,11 @@ sdb_status run_shard(sdb_ctx* ctx, Slot& s, sdb_desc d, sdb_model* m, int64_t r0
     const bool nt_out = size_t(rows) * out_row >= kStreamCopyBytes;
     // pieces of ~1/8 of a tile (4 MiB .. piece_cap): even a one-tile run then
     // overlaps each piece's host copy with the neighbouring piece's DMA
+    const size_t piece_div = size_t(std::max(1, env_int("SDEB200_PIECE_DIV", 8)));
     auto piece_rows = [&](size_t row_bytes) {
         const size_t tile_bytes = size_t((rows + tiles - 1) / tiles) * row_bytes;
-        const size_t want = std::min(piece_cap, std::max(size_t(4) << 20, tile_bytes / 8));
+        const size_t want =
+            std::min(piece_cap, std::max(size_t(4) << 20, tile_bytes / piece_div));
         return std::max<int64_t>(1, int64_t(want / row_bytes));
     };
     const int64_t in_piece = piece_rows(in_row);
