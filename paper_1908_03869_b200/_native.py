@@ -9,7 +9,6 @@ becomes per-device host threads inside the library).
 from __future__ import annotations
 
 import ctypes
-import mmap
 import os
 import threading
 
@@ -201,21 +200,95 @@ def f64(a) -> np.ndarray:
 #: stores at least this large get transparent-huge-page backing (host_empty)
 HUGE_STORE_BYTES = 64 << 20
 
+_PROT_RW = 0x1 | 0x2                # PROT_READ | PROT_WRITE
+_MAP_PRIVATE_ANON = 0x02 | 0x20     # MAP_PRIVATE | MAP_ANONYMOUS (Linux)
+_MADV_HUGEPAGE = 14
+_libc = None
+_pool_lock = threading.Lock()
+_pool: dict[int, list[int]] = {}    # mapping size -> addresses of free, populated mappings
+_pool_bytes = 0
+
+
+def _libc_fns():
+    global _libc
+    if _libc is None:
+        c = ctypes.CDLL(None, use_errno=True)
+        c.mmap.restype = ctypes.c_void_p
+        c.mmap.argtypes = [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_int,
+                           ctypes.c_int, ctypes.c_long]
+        c.munmap.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
+        c.madvise.argtypes = [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int]
+        _libc = c
+    return _libc
+
+
+def _pool_cap() -> int:
+    """Bytes of released store mappings kept for reuse: SDEB200_HOST_POOL_MB,
+    default min(16 GiB, 1/8 of physical memory); 0 disables the pool."""
+    env = os.environ.get("SDEB200_HOST_POOL_MB")
+    if env is not None:
+        return int(env) << 20
+    try:
+        ram = os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES")
+    except (ValueError, OSError):
+        ram = 8 << 30
+    return min(16 << 30, ram // 8)
+
+
+class _StoreMapping:
+    """Owner of one anonymous mapping behind a large store.  It is the base of
+    the ctypes buffer the ndarray views, so it dies only after the last view;
+    its pages (already faulted in) then go back to the pool for the next run's
+    store of the same size, else are unmapped."""
+
+    __slots__ = ("addr", "nbytes")
+
+    def __init__(self, addr: int, nbytes: int):
+        self.addr, self.nbytes = addr, nbytes
+
+    def __del__(self):
+        global _pool_bytes
+        try:
+            with _pool_lock:
+                if _pool_bytes + self.nbytes <= _pool_cap():
+                    _pool.setdefault(self.nbytes, []).append(self.addr)
+                    _pool_bytes += self.nbytes
+                    return
+            _libc_fns().munmap(self.addr, self.nbytes)
+        except Exception:  # interpreter shutdown: the OS reclaims the mapping
+            pass
+
+
+def _take_mapping(nbytes: int) -> int:
+    global _pool_bytes
+    with _pool_lock:
+        free = _pool.get(nbytes)
+        if free:
+            _pool_bytes -= nbytes
+            return free.pop()
+    c = _libc_fns()
+    addr = c.mmap(None, nbytes, _PROT_RW, _MAP_PRIVATE_ANON, -1, 0)
+    if addr is None or addr == ctypes.c_void_p(-1).value:
+        raise MemoryError("mmap of a %d-byte store failed (errno %d)" % (nbytes, ctypes.get_errno()))
+    c.madvise(addr, nbytes, _MADV_HUGEPAGE)  # best effort: THP may be disabled
+    return addr
+
 
 def host_empty(shape, dtype=np.float64) -> np.ndarray:
-    """``np.empty`` for a large run output, backed by an anonymous mapping
-    advised MADV_HUGEPAGE.  The pipeline's drain threads first-touch every
-    page of a fresh store; with 2 MiB pages that costs 512x fewer faults
-    (pinned -> fresh copy 19-28 -> 38.5 GB/s with 16 threads on the B200
-    host, tools/host_copy_bench.cpp).  An ordinary writable ndarray; the
-    mapping lives as long as the array does."""
+    """``np.empty`` for a large run output.  Below HUGE_STORE_BYTES a plain
+    ``np.empty``; above, an anonymous mapping advised MADV_HUGEPAGE, recycled
+    through a process-wide pool once the store is dropped.  The pipeline's
+    drain threads write every byte of a store; into a fresh mapping that costs
+    a page fault per page (pinned -> fresh copy 19-28 GB/s with 4 KiB pages,
+    38 GB/s with 2 MiB pages, into resident pages 80 GB/s on the B200 host,
+    tools/host_copy_bench.cpp), so repeated runs reuse populated mappings the
+    way a caching allocator does.  The array is an ordinary writable ndarray
+    (slicing, pickling, ctypes); its memory lives as long as any view of it."""
     dtype = np.dtype(dtype)
     nbytes = int(np.prod(shape, dtype=np.int64)) * dtype.itemsize
-    if nbytes < HUGE_STORE_BYTES or not hasattr(mmap, "MADV_HUGEPAGE"):
+    if nbytes < HUGE_STORE_BYTES:
         return np.empty(shape, dtype)
-    buf = mmap.mmap(-1, nbytes, flags=mmap.MAP_PRIVATE | mmap.MAP_ANONYMOUS)
-    try:
-        buf.madvise(mmap.MADV_HUGEPAGE)
-    except OSError:  # THP disabled: still a valid (4 KiB-page) mapping
-        pass
+    addr = _take_mapping(nbytes)
+    buf = (ctypes.c_char * nbytes).from_address(addr)
+    buf._owner = _StoreMapping(addr, nbytes)  # ctypes buffers take attributes
     return np.frombuffer(buf, dtype=dtype).reshape(shape)

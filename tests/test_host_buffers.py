@@ -33,3 +33,34 @@ def test_int_dtype():
     a = nat.host_empty((nat.HUGE_STORE_BYTES // 8,), np.int64)
     a[-1] = 7
     assert a.dtype == np.int64 and a[-1] == 7
+
+
+def test_large_store_mapping_recycled_only_after_last_view(monkeypatch):
+    import gc
+    monkeypatch.setenv("SDEB200_HOST_POOL_MB", "1024")
+    shape = (nat.HUGE_STORE_BYTES // 8 + 512,)
+    a = nat.host_empty(shape)
+    addr = a.ctypes.data
+    a[:] = 3.0
+    view = a[10:20]
+    del a
+    gc.collect()
+    b = nat.host_empty(shape)  # the first mapping is still referenced by `view`
+    b_addr = b.ctypes.data
+    assert b_addr != addr and float(view.sum()) == 30.0
+    del view, b
+    gc.collect()
+    c = nat.host_empty(shape)  # a released mapping of this size is reused
+    assert c.ctypes.data in (addr, b_addr)
+    del c
+    gc.collect()
+
+
+def test_pool_disabled(monkeypatch):
+    import gc
+    monkeypatch.setenv("SDEB200_HOST_POOL_MB", "0")
+    a = nat.host_empty((nat.HUGE_STORE_BYTES // 8,))
+    a[-1] = 1.0
+    del a
+    gc.collect()
+    assert nat._pool_bytes <= 1024 << 20
