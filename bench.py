@@ -445,6 +445,7 @@ def run_ours(args, w, world, rank, local, dist):
     lay = [ctypes.c_int32() for _ in range(5)]
     lib.sdb_last_layout(ctx, *(ctypes.byref(v) for v in lay))
     lanes, persistent, ctas_per_sm, variant, _ = (int(v.value) for v in lay)
+    lane_width = int(lib.sdb_last_lane_width(ctx))
     launches_per_step = int(lib.sdb_last_launch_count(ctx))
 
     clocks = ClockSampler(local)
@@ -532,7 +533,8 @@ def run_ours(args, w, world, rank, local, dist):
             "config": {"workload": args.workload, "desc": w["desc"], "n": n,
                        "orbits_per_gpu": m, "sde_steps": steps, "ksteps": w["ksteps"],
                        "solver": w["solver"], "stream": w["stream"], "coupling": args.coupling,
-                       "lanes_per_orbit": lanes, "persistent_grid": bool(persistent),
+                       "lanes_per_orbit": lanes, "oscillators_per_lane": lane_width,
+                       "persistent_grid": bool(persistent),
                        "ctas_per_sm": ctas_per_sm, "register_capped": bool(variant),
                        "template_model": w.get("model"),
                        "parallelism": "orbit-shard x%d" % world,

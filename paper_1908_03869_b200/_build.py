@@ -21,7 +21,7 @@ OBJ = os.path.join(PKG, "_obj")
 LIB = os.path.join(PKG, "libsdeb200.so")
 
 SOURCES = (["sdeb_capi.cu", "sdeb_misc.cu", "sdeb_dsl.cu"]
-           + ["sdeb_kuramoto_j%d.cu" % j for j in (1, 2, 4, 8, 16)])
+           + ["sdeb_kuramoto_j%d.cu" % j for j in (1, 2, 4, 5, 8, 10, 16)])
 HEADERS = sorted(f for f in os.listdir(CSRC) if f.endswith((".cuh", ".h")))
 # device headers the NVRTC-compiled expression-template programs include; they
 # are embedded into the library (no source tree needed at run time)

@@ -119,6 +119,7 @@ struct Slot {
     int32_t persistent = 0;
     int32_t ctas_per_sm = 0;
     int32_t tight = 0;
+    int32_t lane_width = 0;  // oscillators per lane (J) of the last launch
     int32_t tiles = 0;  // orbit tiles of the last host-buffer run
     std::string error;
 };
@@ -132,6 +133,7 @@ struct Layout {
     int smem = 0;
     int ctas_per_sm = 0;
     int tight = 0;  // register-capped kernel variant (unpadded meanfield, J in {4, 8})
+    int J = 0;      // oscillators per lane; 0 = next_pow2(n) / lanes
 };
 
 using TuneKey = std::tuple<int, int, int, int, int, int64_t, int, int>;
@@ -146,6 +148,7 @@ struct sdb_ctx {
     int32_t last_persistent = 0;
     int32_t last_ctas_per_sm = 0;
     int32_t last_tight = 0;
+    int32_t last_lane_width = 0;
     int32_t last_tiles = 0;
     std::map<TuneKey, Layout> tune;
     std::mutex mu;  // guards tune and error: shard threads of one run share the context
@@ -196,7 +199,9 @@ cudaError_t launch_run(const sdeb::RunArgs& a, int J, int solver, int stream, in
         case 1: return sdeb::launch_kuramoto_j<1>(a, solver, stream, coupling, padded, st);
         case 2: return sdeb::launch_kuramoto_j<2>(a, solver, stream, coupling, padded, st);
         case 4: return sdeb::launch_kuramoto_j<4>(a, solver, stream, coupling, padded, st);
+        case 5: return sdeb::launch_kuramoto_j<5>(a, solver, stream, coupling, padded, st);
         case 8: return sdeb::launch_kuramoto_j<8>(a, solver, stream, coupling, padded, st);
+        case 10: return sdeb::launch_kuramoto_j<10>(a, solver, stream, coupling, padded, st);
         case 16: return sdeb::launch_kuramoto_j<16>(a, solver, stream, coupling, padded, st);
         default: return cudaErrorInvalidValue;
     }
@@ -208,7 +213,9 @@ cudaError_t occupancy_run(int J, int solver, int stream, int coupling, int padde
         case 1: return sdeb::occupancy_kuramoto_j<1>(solver, stream, coupling, padded, smem, blocks);
         case 2: return sdeb::occupancy_kuramoto_j<2>(solver, stream, coupling, padded, smem, blocks);
         case 4: return sdeb::occupancy_kuramoto_j<4>(solver, stream, coupling, padded, smem, blocks);
+        case 5: return sdeb::occupancy_kuramoto_j<5>(solver, stream, coupling, padded, smem, blocks);
         case 8: return sdeb::occupancy_kuramoto_j<8>(solver, stream, coupling, padded, smem, blocks);
+        case 10: return sdeb::occupancy_kuramoto_j<10>(solver, stream, coupling, padded, smem, blocks);
         case 16: return sdeb::occupancy_kuramoto_j<16>(solver, stream, coupling, padded, smem, blocks);
         default: return cudaErrorInvalidValue;
     }
@@ -345,9 +352,27 @@ int fit_smem_for_cap(int device, int J, int solver, int stream, int coupling, in
 
 // Kernel instantiation variant: 1 padded (n < next_pow2(n)), else 0, or 2
 // for the register-capped unpadded form.
-int kernel_variant(const sdb_desc& d, int tight) {
-    if (d.nequat < next_pow2(d.nequat)) return 1;
+int kernel_variant(const sdb_desc& d, int lanes, int J, int tight) {
+    if (d.nequat < lanes * J) return 1;
     return tight ? 2 : 0;
+}
+
+// Oscillators per lane of a layout.
+int layout_J(const sdb_desc& d, const Layout& l) {
+    return l.J ? l.J : next_pow2(d.nequat) / l.lanes;
+}
+
+// n = 5 and n = 10 (the paper's N = 5, 10 protocol sizes) also run one lane
+// per orbit with J = n: no padded oscillators (a power-of-two J wastes 3/8
+// of the sincos, sums and updates).  Same bits as the padded layouts: the
+// stride-doubling lane tree over n leaves associates exactly like the
+// canonical tree over next_pow2(n) leaves with zero padding, and the noise
+// blocks and Box-Muller pairs are the same.
+int exact_J(const sdb_desc& d) {
+    const bool fits = d.nequat == 5 || d.nequat == 10;
+    return (fits && d.coupling == SDB_COUPLING_MEANFIELD && (d.lanes == 0 || d.lanes == 1))
+               ? d.nequat
+               : 0;
 }
 
 int64_t cta_groups(const sdb_desc& d, int lanes) {
@@ -376,18 +401,24 @@ sdb_status candidate_layouts(sdb_ctx* ctx, const Slot& s, const sdb_desc& d, int
     } else {
         for (int L : candidate_lanes(d.nequat)) lanes_list.push_back(L);
     }
-    for (int L : lanes_list) {
-      const int J = P / L;
+    // (L, J) pairs: the power-of-two span for every lane count, plus the exact
+    // one-lane layout where n has one (exact_J)
+    std::vector<std::pair<int, int>> shapes;
+    for (int L : lanes_list) shapes.emplace_back(L, P / L);
+    if (const int XJ = exact_J(d)) shapes.emplace_back(1, XJ);
+    for (const auto& shape : shapes) {
+      const int L = shape.first, J = shape.second;
+      const int XJ = J == P / L ? 0 : J;  // Layout::J (0 = the power-of-two span)
       const bool can_tight = d.nequat == P && d.coupling == SDB_COUPLING_MEANFIELD &&
                              (J == 4 || J == 8);
       for (int tight = 0; tight <= (can_tight ? 1 : 0); ++tight) {
-        const int padded = kernel_variant(d, tight);
+        const int padded = kernel_variant(d, L, J, tight);
         int occ = 0;
         SDB_CUDA(ctx, occupancy_run(J, kind_solver, kind_stream, d.coupling, padded, 0, &occ));
         if (occ < 1) continue;
         const int64_t ctas = cta_groups(d, L);
-        out->push_back(Layout{L, 0, 0, occ, tight});
-        if (ctas > int64_t(sms) * occ) out->push_back(Layout{L, 1, 0, occ, tight});
+        out->push_back(Layout{L, 0, 0, occ, tight, XJ});
+        if (ctas > int64_t(sms) * occ) out->push_back(Layout{L, 1, 0, occ, tight, XJ});
         if (tight) continue;
         for (int cap = occ - 1; cap >= 1 && cap >= occ - 4; --cap) {
             const double waves_cap = double(ctas) / (double(sms) * cap);
@@ -397,7 +428,7 @@ sdb_status candidate_layouts(sdb_ctx* ctx, const Slot& s, const sdb_desc& d, int
             if (eff_cap <= eff_occ + 0.02) continue;
             const int smem = fit_smem_for_cap(s.device, J, kind_solver, kind_stream, d.coupling,
                                               padded, cap);
-            if (smem > 0) out->push_back(Layout{L, 0, smem, cap, 0});
+            if (smem > 0) out->push_back(Layout{L, 0, smem, cap, 0, XJ});
         }
       }
     }
@@ -461,17 +492,19 @@ sdb_status choose_layout(sdb_ctx* ctx, Slot& s, const sdb_desc& d, const double*
     // (profiling runs must not capture autotune probes); ctas_per_sm 0 =
     // natural occupancy.
     if (const char* env = std::getenv("SDEB200_LAYOUT")) {
-        int L = 0, pers = 0, cap = 0, tight = 0;
-        if (std::sscanf(env, "%d,%d,%d,%d", &L, &pers, &cap, &tight) >= 1 && L > 0) {
-            const int P = next_pow2(d.nequat);
+        int L = 0, pers = 0, cap = 0, tight = 0, xj = 0;
+        if (std::sscanf(env, "%d,%d,%d,%d,%d", &L, &pers, &cap, &tight, &xj) >= 1 && L > 0) {
+            // 5th field: J (only the exact one-lane layout, J == n, is accepted)
+            xj = (xj > 0 && L == 1 && xj == exact_J(d)) ? xj : 0;
+            const int J = xj ? xj : next_pow2(d.nequat) / L;
+            const int var = kernel_variant(d, L, J, tight);
             int occ = 0;
-            SDB_CUDA(ctx, occupancy_run(P / L, kind_solver, kind_stream, d.coupling,
-                                        kernel_variant(d, tight), 0, &occ));
+            SDB_CUDA(ctx, occupancy_run(J, kind_solver, kind_stream, d.coupling, var, 0, &occ));
             const int smem = (cap > 0 && !pers && cap < occ)
-                                 ? fit_smem_for_cap(s.device, P / L, kind_solver, kind_stream,
-                                                    d.coupling, kernel_variant(d, tight), cap)
+                                 ? fit_smem_for_cap(s.device, J, kind_solver, kind_stream,
+                                                    d.coupling, var, cap)
                                  : 0;
-            Layout lay{L, pers, smem, (cap > 0 && cap < occ && smem > 0) ? cap : occ, tight};
+            Layout lay{L, pers, smem, (cap > 0 && cap < occ && smem > 0) ? cap : occ, tight, xj};
             {
                 std::lock_guard<std::mutex> lock(ctx->mu);
                 ctx->tune[key] = lay;
@@ -508,7 +541,6 @@ sdb_status choose_layout(sdb_ctx* ctx, Slot& s, const sdb_desc& d, const double*
     SDB_CUDA(ctx, cudaEventCreate(&e1));
     float best = 1e30f;
     Layout best_l = cands[0];
-    const int P = next_pow2(d.nequat);
     // reps launches of `steps` steps, best time; real_slabs: persistent slabs
     // sized as a real run of that length would size them
     auto timed = [&](const Layout& lay, int64_t steps, float* ms_out, int reps = 2,
@@ -531,8 +563,9 @@ sdb_status choose_layout(sdb_ctx* ctx, Slot& s, const sdb_desc& d, const double*
             if (r2 != SDB_OK) return r2;
             if (a.persistent && !real_slabs) a.slab_steps = std::max<int64_t>(16, p1 / 2);
             cudaEventRecord(e0, st);
-            cudaError_t e = launch_run(a, P / lay.lanes, kind_solver, kind_stream, d.coupling,
-                                       kernel_variant(d, lay.tight), st);
+            const int J = layout_J(d, lay);
+            cudaError_t e = launch_run(a, J, kind_solver, kind_stream, d.coupling,
+                                       kernel_variant(d, lay.lanes, J, lay.tight), st);
             cudaEventRecord(e1, st);
             if (e == cudaSuccess) e = cudaEventSynchronize(e1);
             if (e != cudaSuccess) return cuda_fail(ctx, e, "autotune launch");
@@ -559,8 +592,8 @@ sdb_status choose_layout(sdb_ctx* ctx, Slot& s, const sdb_desc& d, const double*
         }
         scores.emplace_back(score, ci);
         if (trace_enabled())
-            std::fprintf(stderr, "[sdeb200] tune n=%d L=%d pers=%d ctas=%d tight=%d: %.4f ms/%lld steps\n",
-                         d.nequat, lay.lanes, lay.persistent, lay.ctas_per_sm, lay.tight, score,
+            std::fprintf(stderr, "[sdeb200] tune n=%d L=%d J=%d pers=%d ctas=%d tight=%d: %.4f ms/%lld steps\n",
+                         d.nequat, lay.lanes, layout_J(d, lay), lay.persistent, lay.ctas_per_sm, lay.tight, score,
                          (long long)(p2 - p1 > 0 ? p2 - p1 : p1));
         if (score < best) {
             best = score;
@@ -591,8 +624,8 @@ sdb_status choose_layout(sdb_ctx* ctx, Slot& s, const sdb_desc& d, const double*
             if (rc != SDB_OK) break;
             if (trace_enabled()) {
                 const Layout& l = cands[scores[r].second];
-                std::fprintf(stderr, "[sdeb200] tune stage 2 L=%d pers=%d ctas=%d tight=%d: %.4f ms/%lld steps\n",
-                             l.lanes, l.persistent, l.ctas_per_sm, l.tight, t3, (long long)p3);
+                std::fprintf(stderr, "[sdeb200] tune stage 2 L=%d J=%d pers=%d ctas=%d tight=%d: %.4f ms/%lld steps\n",
+                             l.lanes, layout_J(d, l), l.persistent, l.ctas_per_sm, l.tight, t3, (long long)p3);
             }
             if (t3 < best3) {
                 best3 = t3;
@@ -660,6 +693,7 @@ sdb_status launch_model(sdb_ctx* ctx, Slot& s, const sdb_desc& d, sdb_model* m,
     s.persistent = 0;
     s.ctas_per_sm = 0;
     s.tight = 0;
+    s.lane_width = 0;
     return SDB_OK;
 }
 
@@ -692,19 +726,20 @@ sdb_status launch_device(sdb_ctx* ctx, Slot& s, const sdb_desc& d, sdb_model* m,
     a.rng_state = s.rng.as<uint64_t>();
     rc = configure_layout(ctx, s, s.work, d, lay, d.chunks * d.ksteps, st, &a);
     if (rc != SDB_OK) return rc;
-    const int P = next_pow2(d.nequat);
-    int variant = kernel_variant(d, out_mode ? 0 : lay.tight);
+    const int J = layout_J(d, lay);
+    int variant = kernel_variant(d, lay.lanes, J, out_mode ? 0 : lay.tight);
     if (out_mode) {
         variant += sdeb::kVarCoherence;  // same layout, order-parameter samples
         a.vstride = d.chunks + 1;
     }
-    cudaError_t e = launch_run(a, P / lay.lanes, kind_solver, kind_stream, d.coupling, variant, st);
+    cudaError_t e = launch_run(a, J, kind_solver, kind_stream, d.coupling, variant, st);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "kuramoto_run_kernel launch");
     s.launches += 1;
     s.lanes = lay.lanes;
     s.persistent = lay.persistent;
     s.ctas_per_sm = lay.ctas_per_sm;
     s.tight = lay.tight;
+    s.lane_width = J;
     return SDB_OK;
 }
 
@@ -1234,6 +1269,7 @@ sdb_status run_host(sdb_ctx* ctx, const sdb_desc& d, sdb_model* m, const double*
     ctx->last_persistent = ctx->slots[0].persistent;
     ctx->last_ctas_per_sm = ctx->slots[0].ctas_per_sm;
     ctx->last_tight = ctx->slots[0].tight;
+    ctx->last_lane_width = ctx->slots[0].lane_width;
     ctx->last_tiles = ctx->slots[0].tiles;
     for (int64_t g = 0; g < used; ++g)
         if (status[g] != SDB_OK) return status[g];
@@ -1256,6 +1292,7 @@ sdb_status run_dev(sdb_ctx* ctx, const sdb_desc& d, sdb_model* m, const double* 
     ctx->last_persistent = s.persistent;
     ctx->last_ctas_per_sm = s.ctas_per_sm;
     ctx->last_tight = s.tight;
+    ctx->last_lane_width = s.lane_width;
     ctx->last_tiles = 0;
     return rc;
 }
@@ -1374,6 +1411,8 @@ const char* sdb_last_error(const sdb_ctx* ctx) {
 
 int64_t sdb_last_launch_count(const sdb_ctx* ctx) { return ctx ? ctx->launches : 0; }
 int32_t sdb_last_lanes(const sdb_ctx* ctx) { return ctx ? ctx->last_lanes : 0; }
+
+int32_t sdb_last_lane_width(const sdb_ctx* ctx) { return ctx ? ctx->last_lane_width : 0; }
 
 void sdb_last_layout(const sdb_ctx* ctx, int32_t* lanes, int32_t* persistent,
                      int32_t* ctas_per_sm, int32_t* variant, int32_t* tiles) {

@@ -271,9 +271,11 @@ __device__ __forceinline__ void group_order_param(const double (&y)[J], int base
 
 // ---- noise for one step (rng.py:150-188 / DESIGN.md streams) ---------------
 
+// Noise blocks a lane draws per step.  J in {5, 10} (the exact layouts of
+// n = 5, 10, one lane per orbit) end in a partial block.
 template <int J>
 __host__ __device__ constexpr int blocks_per_lane() {
-    return J >= 4 ? J / 4 : 1;
+    return J >= 4 ? (J + 3) / 4 : 1;
 }
 
 // Draws the step's normals pair by pair and hands each to apply(q, z) as
@@ -294,10 +296,14 @@ __device__ __forceinline__ void step_noise_apply(const RunArgs& a, int64_t row, 
         const uint32_t step_hi = uint32_t(step >> 32), step_lo = uint32_t(step);
         const int nn = a.nnoise;
         if constexpr (J >= 4) {
+            // unpadded with J % 4 == 0: n = L*J, whole blocks, no checks.  J in
+            // {5, 10} (lane 0 of a one-lane orbit) ends in a partial block: the
+            // reference draws it whole and keeps the first n normals
+            constexpr bool kWhole = !PADDED && J % 4 == 0;
 #pragma unroll
-            for (int t = 0; t < J / 4; ++t) {
+            for (int t = 0; t < blocks_per_lane<J>(); ++t) {
                 const int b = base / 4 + t;
-                if (!PADDED || 4 * b < nn) {  // unpadded: n = L*J >= 4, whole blocks
+                if (kWhole || 4 * b < nn) {
                     Words4 w;
                     if constexpr (STREAM == KS_PHILOX) {
                         w = philox4x32_10(seed_hi, step_hi, step_lo, uint32_t(b), seed_lo, orbit_g);
@@ -307,11 +313,11 @@ __device__ __forceinline__ void step_noise_apply(const RunArgs& a, int64_t row, 
                     double z0, z1;
                     box_muller_pair(w.w0, w.w1, z0, z1);
                     apply(4 * t, z0);
-                    apply(4 * t + 1, z1);
-                    if (!PADDED || 4 * b + 2 < nn) {
+                    if (4 * t + 1 < J) apply(4 * t + 1, z1);
+                    if (4 * t + 2 < J && (kWhole || 4 * b + 2 < nn)) {
                         box_muller_pair(w.w2, w.w3, z0, z1);
                         apply(4 * t + 2, z0);
-                        apply(4 * t + 3, z1);
+                        if (4 * t + 3 < J) apply(4 * t + 3, z1);
                     }
                 }
             }

@@ -324,8 +324,9 @@ def test_launch_accounting():
     assert info["launches"] == 1 and info["lanes"] == 2
 
 
-def _run_pinned(layout, n, batch, cfg):
-    """run_batch through a fresh context with SDEB200_LAYOUT pinned."""
+def _run_pinned(layout, n, batch, cfg, info=None):
+    """run_batch through a fresh context with SDEB200_LAYOUT pinned (info, if
+    given, receives the lane width the launch ran with)."""
     import ctypes
     import os
 
@@ -342,10 +343,44 @@ def _run_pinned(layout, n, batch, cfg):
         init, params = nat.f64(batch.init), nat.f64(batch.params)
         nat.check(nat.lib().sdb_run(ctx, desc, nat.dptr(init), nat.dptr(params),
                                     nat.dptr(values), nat.i64ptr(fail)), ctx)
+        if info is not None:
+            info["lane_width"] = int(nat.lib().sdb_last_lane_width(ctx))
         nat.lib().sdb_close(ctx)
         return values, fail
     finally:
         del os.environ["SDEB200_LAYOUT"]
+
+
+@pytest.mark.parametrize("stream", ["philox", "sfc64", "xoshiro256pp"])
+@pytest.mark.parametrize("n", [5, 10])
+def test_exact_lane_width_layouts_bit_identical(n, stream):
+    # n = 5, 10 also run J = n oscillators in one lane (no padded slots): the
+    # lane tree over n leaves must associate exactly like the canonical tree
+    # over next_pow2(n) zero-padded leaves, and the partial last noise block
+    # must give the same normals -- same bits as every power-of-two layout
+    m = 700
+    batch = sdb.sample_kuramoto_batch(n, m, (0.2, 0.4), (0.01, 0.1), 0.3, seed=9)
+    params = batch.params.copy()
+    params[11, 1 + n - 1] = np.inf  # the last oscillator (partial block) fails
+    params[12, 1 + 2] = 1e12       # huge phases: the exact-reduction branch
+    batch = OrbitBatch(init=batch.init, params=params)
+    cfg = EngineConfig(dt=1e-2, tspan=1.5, ksteps=25, orbits=m, seed=3, stream=stream)
+    info = {}
+    ref, ref_fail = _run_pinned("1,0,0,0", n, batch, cfg, info)
+    assert info["lane_width"] == (8 if n == 5 else 16)
+    for lay in ("1,0,0,0,%d" % n, "1,1,0,0,%d" % n, "2,0,0,0"):
+        got, got_fail = _run_pinned(lay, n, batch, cfg, info)
+        if lay.endswith(",%d" % n):
+            assert info["lane_width"] == n
+        assert np.array_equal(ref, got, equal_nan=True), lay
+        assert np.array_equal(ref_fail, got_fail), lay
+    assert ref_fail[11] >= 0 and ref_fail[12] < 0
+    # the default autotuned run and the fused coherence run agree too
+    auto = run_batch(sdb.kuramoto_model(n), cfg, batch)
+    assert np.array_equal(auto.values, ref, equal_nan=True)
+    coh = sdb.run_coherence(sdb.kuramoto_model(n), cfg, batch)
+    series = sdb.coherence_series(auto)
+    np.testing.assert_array_equal(coh.r, series.r)
 
 
 @pytest.mark.parametrize("stream", ["philox", "sfc64"])
