@@ -108,7 +108,8 @@ int32_t sdb_last_lanes(const sdb_ctx* ctx);
 void sdb_last_layout(const sdb_ctx* ctx, int32_t* lanes, int32_t* persistent,
                      int32_t* ctas_per_sm, int32_t* variant, int32_t* tiles);
 /* Oscillators per lane (J) of the last Kuramoto launch: next_pow2(n) / lanes,
- * or n itself for the exact one-lane layouts of n = 5 and n = 10 (meanfield);
+ * or n itself for the exact one-lane layouts of non-power-of-two n <= 16
+ * (meanfield);
  * SDEB200_LAYOUT's optional 5th field pins it ("1,1,0,0,5"). */
 int32_t sdb_last_lane_width(const sdb_ctx* ctx);
 

@@ -20,8 +20,11 @@ CSRC = os.path.join(PKG, "csrc")
 OBJ = os.path.join(PKG, "_obj")
 LIB = os.path.join(PKG, "libsdeb200.so")
 
+# stepper instantiations: power-of-two lane widths J, plus every other J <= 16
+# for the exact one-lane layouts of n = J (sdeb_capi.cu exact_J)
+EXACT_J = (3, 5, 6, 7, 9, 10, 11, 12, 13, 14, 15)
 SOURCES = (["sdeb_capi.cu", "sdeb_misc.cu", "sdeb_dsl.cu"]
-           + ["sdeb_kuramoto_j%d.cu" % j for j in (1, 2, 4, 5, 8, 10, 16)])
+           + ["sdeb_kuramoto_j%d.cu" % j for j in (1, 2, 4, 8, 16) + EXACT_J])
 HEADERS = sorted(f for f in os.listdir(CSRC) if f.endswith((".cuh", ".h")))
 # device headers the NVRTC-compiled expression-template programs include; they
 # are embedded into the library (no source tree needed at run time)

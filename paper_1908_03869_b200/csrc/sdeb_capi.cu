@@ -199,10 +199,19 @@ cudaError_t launch_run(const sdeb::RunArgs& a, int J, int solver, int stream, in
         case 1: return sdeb::launch_kuramoto_j<1>(a, solver, stream, coupling, padded, st);
         case 2: return sdeb::launch_kuramoto_j<2>(a, solver, stream, coupling, padded, st);
         case 4: return sdeb::launch_kuramoto_j<4>(a, solver, stream, coupling, padded, st);
-        case 5: return sdeb::launch_kuramoto_j<5>(a, solver, stream, coupling, padded, st);
         case 8: return sdeb::launch_kuramoto_j<8>(a, solver, stream, coupling, padded, st);
-        case 10: return sdeb::launch_kuramoto_j<10>(a, solver, stream, coupling, padded, st);
         case 16: return sdeb::launch_kuramoto_j<16>(a, solver, stream, coupling, padded, st);
+        case 3: return sdeb::launch_kuramoto_j<3>(a, solver, stream, coupling, padded, st);
+        case 5: return sdeb::launch_kuramoto_j<5>(a, solver, stream, coupling, padded, st);
+        case 6: return sdeb::launch_kuramoto_j<6>(a, solver, stream, coupling, padded, st);
+        case 7: return sdeb::launch_kuramoto_j<7>(a, solver, stream, coupling, padded, st);
+        case 9: return sdeb::launch_kuramoto_j<9>(a, solver, stream, coupling, padded, st);
+        case 10: return sdeb::launch_kuramoto_j<10>(a, solver, stream, coupling, padded, st);
+        case 11: return sdeb::launch_kuramoto_j<11>(a, solver, stream, coupling, padded, st);
+        case 12: return sdeb::launch_kuramoto_j<12>(a, solver, stream, coupling, padded, st);
+        case 13: return sdeb::launch_kuramoto_j<13>(a, solver, stream, coupling, padded, st);
+        case 14: return sdeb::launch_kuramoto_j<14>(a, solver, stream, coupling, padded, st);
+        case 15: return sdeb::launch_kuramoto_j<15>(a, solver, stream, coupling, padded, st);
         default: return cudaErrorInvalidValue;
     }
 }
@@ -213,10 +222,19 @@ cudaError_t occupancy_run(int J, int solver, int stream, int coupling, int padde
         case 1: return sdeb::occupancy_kuramoto_j<1>(solver, stream, coupling, padded, smem, blocks);
         case 2: return sdeb::occupancy_kuramoto_j<2>(solver, stream, coupling, padded, smem, blocks);
         case 4: return sdeb::occupancy_kuramoto_j<4>(solver, stream, coupling, padded, smem, blocks);
-        case 5: return sdeb::occupancy_kuramoto_j<5>(solver, stream, coupling, padded, smem, blocks);
         case 8: return sdeb::occupancy_kuramoto_j<8>(solver, stream, coupling, padded, smem, blocks);
-        case 10: return sdeb::occupancy_kuramoto_j<10>(solver, stream, coupling, padded, smem, blocks);
         case 16: return sdeb::occupancy_kuramoto_j<16>(solver, stream, coupling, padded, smem, blocks);
+        case 3: return sdeb::occupancy_kuramoto_j<3>(solver, stream, coupling, padded, smem, blocks);
+        case 5: return sdeb::occupancy_kuramoto_j<5>(solver, stream, coupling, padded, smem, blocks);
+        case 6: return sdeb::occupancy_kuramoto_j<6>(solver, stream, coupling, padded, smem, blocks);
+        case 7: return sdeb::occupancy_kuramoto_j<7>(solver, stream, coupling, padded, smem, blocks);
+        case 9: return sdeb::occupancy_kuramoto_j<9>(solver, stream, coupling, padded, smem, blocks);
+        case 10: return sdeb::occupancy_kuramoto_j<10>(solver, stream, coupling, padded, smem, blocks);
+        case 11: return sdeb::occupancy_kuramoto_j<11>(solver, stream, coupling, padded, smem, blocks);
+        case 12: return sdeb::occupancy_kuramoto_j<12>(solver, stream, coupling, padded, smem, blocks);
+        case 13: return sdeb::occupancy_kuramoto_j<13>(solver, stream, coupling, padded, smem, blocks);
+        case 14: return sdeb::occupancy_kuramoto_j<14>(solver, stream, coupling, padded, smem, blocks);
+        case 15: return sdeb::occupancy_kuramoto_j<15>(solver, stream, coupling, padded, smem, blocks);
         default: return cudaErrorInvalidValue;
     }
 }
@@ -362,14 +380,14 @@ int layout_J(const sdb_desc& d, const Layout& l) {
     return l.J ? l.J : next_pow2(d.nequat) / l.lanes;
 }
 
-// n = 5 and n = 10 (the paper's N = 5, 10 protocol sizes) also run one lane
-// per orbit with J = n: no padded oscillators (a power-of-two J wastes 3/8
-// of the sincos, sums and updates).  Same bits as the padded layouts: the
-// stride-doubling lane tree over n leaves associates exactly like the
-// canonical tree over next_pow2(n) leaves with zero padding, and the noise
-// blocks and Box-Muller pairs are the same.
+// n <= 16 that is not a power of two (e.g. the paper's N = 5, 10, 15) also
+// runs one lane per orbit with J = n: no padded oscillators (n = 5 in a
+// power-of-two span wastes 3/8 of the sincos, sums and updates).  Same bits
+// as the padded layouts: the stride-doubling lane tree over n leaves
+// associates exactly like the canonical tree over next_pow2(n) leaves with
+// zero padding, and the noise blocks and Box-Muller pairs are the same.
 int exact_J(const sdb_desc& d) {
-    const bool fits = d.nequat == 5 || d.nequat == 10;
+    const bool fits = d.nequat >= 3 && d.nequat <= kMaxJ && d.nequat != next_pow2(d.nequat);
     return (fits && d.coupling == SDB_COUPLING_MEANFIELD && (d.lanes == 0 || d.lanes == 1))
                ? d.nequat
                : 0;

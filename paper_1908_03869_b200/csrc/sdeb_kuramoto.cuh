@@ -271,11 +271,11 @@ __device__ __forceinline__ void group_order_param(const double (&y)[J], int base
 
 // ---- noise for one step (rng.py:150-188 / DESIGN.md streams) ---------------
 
-// Noise blocks a lane draws per step.  J in {5, 10} (the exact layouts of
-// n = 5, 10, one lane per orbit) end in a partial block.
+// Noise blocks a lane draws per step.  J not a power of two (the exact
+// one-lane layouts of n <= 16) ends in a partial block.
 template <int J>
 __host__ __device__ constexpr int blocks_per_lane() {
-    return J >= 4 ? (J + 3) / 4 : 1;
+    return J >= 3 ? (J + 3) / 4 : 1;
 }
 
 // Draws the step's normals pair by pair and hands each to apply(q, z) as
@@ -295,10 +295,10 @@ __device__ __forceinline__ void step_noise_apply(const RunArgs& a, int64_t row, 
         const uint32_t seed_lo = uint32_t(a.seed), seed_hi = uint32_t(a.seed >> 32);
         const uint32_t step_hi = uint32_t(step >> 32), step_lo = uint32_t(step);
         const int nn = a.nnoise;
-        if constexpr (J >= 4) {
-            // unpadded with J % 4 == 0: n = L*J, whole blocks, no checks.  J in
-            // {5, 10} (lane 0 of a one-lane orbit) ends in a partial block: the
-            // reference draws it whole and keeps the first n normals
+        if constexpr (J >= 3) {
+            // unpadded with J % 4 == 0: n = L*J, whole blocks, no checks.  Any
+            // other J >= 3 (lane 0 of a one-lane orbit, J == n) ends in a partial
+            // block: the reference draws it whole and keeps the first n normals
             constexpr bool kWhole = !PADDED && J % 4 == 0;
 #pragma unroll
             for (int t = 0; t < blocks_per_lane<J>(); ++t) {

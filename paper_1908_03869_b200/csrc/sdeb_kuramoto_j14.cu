@@ -1,0 +1,9 @@
+// Instantiates the fused stepper for J = 14 oscillators per lane (the exact one-lane layout of n = 14).
+// the stepper reads the sincos / log tables from shared memory (sdeb_math.cuh)
+#define SDEB_SMEM_TABLES 1
+#include "sdeb_kuramoto_inst.cuh"
+
+namespace sdeb {
+template cudaError_t launch_kuramoto_j<14>(const RunArgs&, int, int, int, int, cudaStream_t);
+template cudaError_t occupancy_kuramoto_j<14>(int, int, int, int, size_t, int*);
+}  // namespace sdeb

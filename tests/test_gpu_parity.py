@@ -352,9 +352,9 @@ def _run_pinned(layout, n, batch, cfg, info=None):
 
 
 @pytest.mark.parametrize("stream", ["philox", "sfc64", "xoshiro256pp"])
-@pytest.mark.parametrize("n", [5, 10])
+@pytest.mark.parametrize("n", [3, 5, 6, 7, 10, 12, 15])
 def test_exact_lane_width_layouts_bit_identical(n, stream):
-    # n = 5, 10 also run J = n oscillators in one lane (no padded slots): the
+    # n <= 16 not a power of two also runs J = n oscillators in one lane (no padded slots): the
     # lane tree over n leaves must associate exactly like the canonical tree
     # over next_pow2(n) zero-padded leaves, and the partial last noise block
     # must give the same normals -- same bits as every power-of-two layout
@@ -367,7 +367,7 @@ def test_exact_lane_width_layouts_bit_identical(n, stream):
     cfg = EngineConfig(dt=1e-2, tspan=1.5, ksteps=25, orbits=m, seed=3, stream=stream)
     info = {}
     ref, ref_fail = _run_pinned("1,0,0,0", n, batch, cfg, info)
-    assert info["lane_width"] == (8 if n == 5 else 16)
+    assert info["lane_width"] == 1 << (n - 1).bit_length()
     for lay in ("1,0,0,0,%d" % n, "1,1,0,0,%d" % n, "2,0,0,0"):
         got, got_fail = _run_pinned(lay, n, batch, cfg, info)
         if lay.endswith(",%d" % n):
