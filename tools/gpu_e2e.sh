@@ -12,5 +12,5 @@ timeout 600 python bench.py --no-cpu-baseline > $O/bench_cfg2.log 2>&1; echo "be
 for wl in cfg5 cfg3_n32 cfg3_n256; do
   timeout 400 python bench.py --workload $wl --no-cpu-baseline --steps 3 > $O/bench_$wl.log 2>&1; echo "bench $wl rc=$?" >> $O/status.txt
 done
-ARGS=$(python -c "import json;c=json.loads(open('$O/bench_cfg2.log').read().strip().splitlines()[-1])['config'];print('--lanes %d --persistent %d --ctas %d --tight %d' % (c['lanes_per_orbit'], c.get('persistent_grid',0), c.get('ctas_per_sm',0), c.get('register_capped',0)))" 2>/dev/null || echo "--lanes 4")
+ARGS=$(python -c "import json;c=json.loads(open('$O/bench_cfg2.log').read().strip().splitlines()[-1])['config'];print('--lanes %d --persistent %d --ctas %d --tight %d --width %d' % (c['lanes_per_orbit'], c.get('persistent_grid',0), c.get('ctas_per_sm',0), c.get('register_capped',0), c.get('oscillators_per_lane',0)))" 2>/dev/null || echo "--lanes 4")
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:kuramoto_run -c 1 -o $O/prof_cfg2 python tools/profile_run.py --workload cfg2 $ARGS > $O/ncu_full.log 2>&1; echo "ncu full rc=$? $ARGS" >> $O/status.txt

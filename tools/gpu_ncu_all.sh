@@ -14,7 +14,7 @@ summarize() {
 }
 for wl in $WLS; do
   timeout 300 python bench.py --workload $wl --no-cpu-baseline --steps 2 --warmup 3 > $O/bench_$wl.log 2>&1
-  ARGS=$(python -c "import json;c=json.loads(open('$O/bench_$wl.log').read().strip().splitlines()[-1])['config'];print('--lanes %d --persistent %d --ctas %d --tight %d' % (c['lanes_per_orbit'], c.get('persistent_grid',0), c.get('ctas_per_sm',0), c.get('register_capped',0)))" 2>/dev/null || echo "--lanes 2")
+  ARGS=$(python -c "import json;c=json.loads(open('$O/bench_$wl.log').read().strip().splitlines()[-1])['config'];print('--lanes %d --persistent %d --ctas %d --tight %d --width %d' % (c['lanes_per_orbit'], c.get('persistent_grid',0), c.get('ctas_per_sm',0), c.get('register_capped',0), c.get('oscillators_per_lane',0)))" 2>/dev/null || echo "--lanes 2")
   timeout 900 ncu --set full --import-source on --clock-control none -k regex:kuramoto_run -c 1 -o $O/prof_$wl python tools/profile_run.py --workload $wl $ARGS > $O/ncu_$wl.log 2>&1
   echo "$wl ncu rc=$? $ARGS" >> $O/status.txt
   summarize $wl

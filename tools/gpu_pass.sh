@@ -18,5 +18,5 @@ for wl in $WLS; do
 done
 timeout 300 python bench.py --coupling pairwise --no-cpu-baseline --steps 2 > $O/bench_cfg2_pairwise.log 2>&1; echo "bench pairwise rc=$?" >> $O/status.txt
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_cfg2.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline > $O/ncu_launches.log 2>&1; echo "ncu launches rc=$?" >> $O/status.txt
-ARGS=$(python -c "import json;c=json.loads(open('$O/bench_cfg2.log').read().strip().splitlines()[-1])['config'];print('--lanes %d --persistent %d --ctas %d --tight %d' % (c['lanes_per_orbit'], c.get('persistent_grid',0), c.get('ctas_per_sm',0), c.get('register_capped',0)))" 2>/dev/null || echo "--lanes 2")
+ARGS=$(python -c "import json;c=json.loads(open('$O/bench_cfg2.log').read().strip().splitlines()[-1])['config'];print('--lanes %d --persistent %d --ctas %d --tight %d --width %d' % (c['lanes_per_orbit'], c.get('persistent_grid',0), c.get('ctas_per_sm',0), c.get('register_capped',0), c.get('oscillators_per_lane',0)))" 2>/dev/null || echo "--lanes 2")
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:kuramoto_run -c 1 -o $O/prof_cfg2 python tools/profile_run.py --workload cfg2 $ARGS > $O/ncu_full.log 2>&1; echo "ncu full rc=$? $ARGS" >> $O/status.txt

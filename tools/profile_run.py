@@ -34,10 +34,11 @@ def main():
     ap.add_argument("--persistent", type=int, default=0)
     ap.add_argument("--ctas", type=int, default=0)
     ap.add_argument("--tight", type=int, default=0)
+    ap.add_argument("--width", type=int, default=0, help="oscillators per lane (exact layouts)")
     args = ap.parse_args()
     if args.lanes:
-        os.environ["SDEB200_LAYOUT"] = "%d,%d,%d,%d" % (args.lanes, args.persistent, args.ctas,
-                                                        args.tight)
+        os.environ["SDEB200_LAYOUT"] = "%d,%d,%d,%d,%d" % (args.lanes, args.persistent, args.ctas,
+                                                           args.tight, args.width)
     w = dict(bench.WORKLOADS[args.workload])
     if args.steps:
         w["steps"] = args.steps
