@@ -300,26 +300,27 @@ __device__ __forceinline__ void step_noise_apply(const RunArgs& a, int64_t row, 
             // other J >= 3 (lane 0 of a one-lane orbit, J == n) ends in a partial
             // block: the reference draws it whole and keeps the first n normals
             constexpr bool kWhole = !PADDED && J % 4 == 0;
-            // all of the step's Philox blocks first: independent integer chains
-            // side by side, then the Box-Muller pairs (paper N=10 -4 %, cfg3
-            // and cfg5 -0.2..0.5 %; a surplus block of a padded lane is unused)
+            // all of the step's blocks first: independent integer chains side
+            // by side, then the Box-Muller pairs (Philox: paper N=10 -4 %, cfg3
+            // / cfg5 -0.2..0.5 %; sfc64: cfg2 at L=2 -3 %).  A padded lane's
+            // surplus Philox block is unused; a stream block past the last noise
+            // term holds a zero state that is never saved, so advancing it is
+            // harmless.
             Words4 ws[blocks_per_lane<J>()];
-            if constexpr (STREAM == KS_PHILOX) {
 #pragma unroll
-                for (int t = 0; t < blocks_per_lane<J>(); ++t)
+            for (int t = 0; t < blocks_per_lane<J>(); ++t) {
+                if constexpr (STREAM == KS_PHILOX) {
                     ws[t] = philox4x32_10(seed_hi, step_hi, step_lo, uint32_t(base / 4 + t), seed_lo,
                                           orbit_g);
+                } else {
+                    ws[t] = stream_block<STREAM>(rs[t]);
+                }
             }
 #pragma unroll
             for (int t = 0; t < blocks_per_lane<J>(); ++t) {
                 const int b = base / 4 + t;
                 if (kWhole || 4 * b < nn) {
-                    Words4 w;
-                    if constexpr (STREAM == KS_PHILOX) {
-                        w = ws[t];
-                    } else {
-                        w = stream_block<STREAM>(rs[t]);
-                    }
+                    const Words4 w = ws[t];
                     double z0, z1;
                     box_muller_pair(w.w0, w.w1, z0, z1);
                     apply(4 * t, z0);
