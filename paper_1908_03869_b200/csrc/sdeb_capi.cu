@@ -933,16 +933,21 @@ int host_copy_threads(int /*shards*/) {
 
 // Orbit tiles of a host-buffer shard: copies of tile t+1 / t-1 overlap the
 // kernel of tile t.  A tile must keep the kernel well fed (>= ~8 waves of
-// resident threads at a typical lanes-per-orbit) and be worth a pipeline
-// stage (>= 32 MB of transfers); at most 8.  SDEB200_TILES overrides.
+// resident threads at a typical lanes-per-orbit, 2 for transfer-heavy runs)
+// and be worth a pipeline stage (>= 32 MB of transfers); at most 8.
+// SDEB200_TILES overrides.
 int64_t shard_tiles(const sdb_desc& d, int64_t rows, int device) {
     const int forced = env_int("SDEB200_TILES", 0);
     if (forced > 0) return std::min<int64_t>(forced, rows);
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     const int64_t lanes_est = std::min(32, std::max(1, next_pow2(d.nequat) / 4));
-    const int64_t min_rows = int64_t(8) * sms * 768 / lanes_est;
     const double io = double(rows) * double(d.nequat + d.nparams + d.chunks * d.nequat) * 8.0;
+    // transfer-heavy runs (>= 1 GB moved) accept tiles of >= 2 waves: hiding the
+    // kernel under the transfers pays more than a short tile's tail (cfg5
+    // e2e 95 -> 86-90 ms at 4 tiles); otherwise >= 8 waves per tile
+    const int64_t waves = io >= 1e9 ? 2 : 8;
+    const int64_t min_rows = waves * sms * 768 / lanes_est;
     int64_t t = std::min<int64_t>(rows / std::max<int64_t>(1, min_rows), int64_t(io / 32e6));
     return std::max<int64_t>(1, std::min<int64_t>(8, t));
 }
