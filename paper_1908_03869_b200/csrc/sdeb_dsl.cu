@@ -600,7 +600,11 @@ std::string program_source(const sdb_model* m, int kind, int lanes, bool factor)
                   global_state(m, lanes) ? 1 : 0, m->drift_h[factor ? 1 : 0],
                   m->diffusion_h[factor ? 1 : 0],
                   stage_tables(m, factor) ? "#define SDEB_SMEM_TABLES 1\n" : "");
-    return std::string("// generated by sdeb200 from expression templates\n") + head +
+    // SDEB200_DSL_MINB=b: __launch_bounds__(128, b) for the generated kernel
+    // (experiments: caps registers so b CTAs fit per SM)
+    std::string minb;
+    if (const char* e = std::getenv("SDEB200_DSL_MINB")) minb = std::string("#define SDB_MINB ") + e + "\n";
+    return std::string("// generated by sdeb200 from expression templates\n") + head + minb +
            "#include \"sdeb_dsl_kernel.cuh\"\n\n// drift: " + m->drift_text +
            (factor ? "  (sums factored)" : "") + "\n" + m->drift_cu[factor ? 1 : 0] +
            "\n// diffusion: " + m->diffusion_text + "\n" + m->diffusion_cu[factor ? 1 : 0];

@@ -425,7 +425,10 @@ __device__ __forceinline__ void dsl_commit(int lane, const DVec& y, double (&yne
 // threads past the last orbit mirror it into their own column and write
 // nothing, so every warp runs the same sequence of __syncwarp.
 
-extern "C" __global__ void __launch_bounds__(128) sdb_dsl_main(const sdeb::DslArgs a) {
+#ifndef SDB_MINB
+#define SDB_MINB 1
+#endif
+extern "C" __global__ void __launch_bounds__(128, SDB_MINB) sdb_dsl_main(const sdeb::DslArgs a) {
     using namespace sdeb;
     extern __shared__ double dsl_smem[];
     constexpr int kSlots = 128 / kL;
