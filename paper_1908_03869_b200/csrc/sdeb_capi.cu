@@ -1013,7 +1013,9 @@ sdb_status run_shard(sdb_ctx* ctx, Slot& s, sdb_desc d, sdb_model* m, int64_t r0
     const size_t piece_cap = size_t(std::max(1, env_int("SDEB200_PIECE_KB", 65536))) << 10;
     const size_t in_row = size_t(n + np_) * sizeof(double);
     const size_t out_row = size_t(width + 1) * sizeof(double);  // samples + fail word
-    const bool nt_in = size_t(rows) * in_row >= kStreamCopyBytes;
+    // pinned input staging is only ever read by the DMA engine: streaming stores
+    // always (SDEB200_NT_IN=0 restores the size threshold, for A/B runs)
+    const bool nt_in = env_int("SDEB200_NT_IN", 1) != 0 || size_t(rows) * in_row >= kStreamCopyBytes;
     const bool nt_out = size_t(rows) * out_row >= kStreamCopyBytes;
     // pieces of ~1/8 of a tile (4 MiB .. piece_cap): even a one-tile run then
     // overlaps each piece's host copy with the neighbouring piece's DMA
