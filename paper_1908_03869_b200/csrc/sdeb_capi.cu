@@ -1044,7 +1044,8 @@ sdb_status run_shard(sdb_ctx* ctx, Slot& s, sdb_desc d, sdb_model* m, int64_t r0
 
     // Destination prefault (see prefault_range): while the next piece's DMA
     // (or the kernel before it) is still running, fault in the store pages of
-    // rows no drain has reached yet, 32 MiB at a time (stores >= 4 MiB).
+    // rows no drain has reached yet, 32 MiB at a time (stores >= 4 MiB), and
+    // write their sample 0 (the initial state, host data).
     // SDEB200_PREFAULT=0 turns it off.
     const int64_t row_words = out_mode ? width : (k + 1) * n;
     const size_t store_bytes = size_t(rows) * size_t(row_words) * sizeof(double);
@@ -1052,6 +1053,7 @@ sdb_status run_shard(sdb_ctx* ctx, Slot& s, sdb_desc d, sdb_model* m, int64_t r0
         values && store_bytes >= (size_t(4) << 20) && env_int("SDEB200_PREFAULT", 1) != 0;
     const int64_t pf_rows = std::max<int64_t>(1, int64_t((size_t(32) << 20) / (row_words * 8)));
     int64_t pf_next = 0;  // shard-local rows below this are populated (or drained)
+    int64_t init_next = 0;  // shard-local rows below this have sample 0 written
     double prefault_ms = 0.0;
 
     auto drain_one = [&]() -> sdb_status {
@@ -1068,6 +1070,15 @@ sdb_status run_shard(sdb_ctx* ctx, Slot& s, sdb_desc d, sdb_model* m, int64_t r0
                     prefault_range(base + span * size_t(x) / size_t(threads),
                                    base + span * size_t(y) / size_t(threads));
                 });
+                if (!out_mode) {  // sample 0 (the initial state) needs no device data
+                    parallel_rows(b - a, size_t(b - a) * n * sizeof(double), threads,
+                                  [&](int64_t x, int64_t y) {
+                        for (int64_t r = a + x; r < a + y; ++r)
+                            copy_bytes(values + (r0 + r) * row_words, init + (r0 + r) * n,
+                                       size_t(n) * sizeof(double), nt_out);
+                    });
+                    init_next = b;
+                }
                 pf_next = b;
             }
             prefault_ms += now_ms() - f0;
@@ -1099,7 +1110,8 @@ sdb_status run_shard(sdb_ctx* ctx, Slot& s, sdb_desc d, sdb_model* m, int64_t r0
                     continue;
                 }
                 double* dst = values + g * (k + 1) * n;
-                copy_bytes(dst, init + g * n, size_t(n) * sizeof(double), nt_out);
+                if (p.a + r >= init_next)  // else written while the host waited
+                    copy_bytes(dst, init + g * n, size_t(n) * sizeof(double), nt_out);
                 copy_bytes(dst + n, src + r * k * n, size_t(k) * n * sizeof(double), nt_out);
             }
         });
