@@ -310,7 +310,7 @@ def barrier(dist):
 
 def cpu_sample_rate(w, seconds: float, threads: int, stream_override=None):
     """orbit-steps/s of the oracle port (numpy restatement of the reference's
-    run_batch, engine.py:221-314) on M_cpu orbits x S_cpu steps of workload w."""
+    run_batch, engine.py:184-277) on M_cpu orbits x S_cpu steps of workload w."""
     from oracle import sdeb_oracle as O
     n = w["n"]
     m_cpu = min(w["orbits"], 8192 if n <= 32 else 1024)

@@ -29,7 +29,7 @@ extern "C" {
 
 typedef enum sdb_status {
     SDB_OK = 0,
-    SDB_ERR_CONFIG = 1,      /* maps to ConfigError (engine.py:77) */
+    SDB_ERR_CONFIG = 1,      /* maps to ConfigError (engine.py:40) */
     SDB_ERR_UNSUPPORTED = 2, /* maps to NotImplementedError */
     SDB_ERR_CUDA = 3,        /* maps to RuntimeError */
     SDB_ERR_ARGUMENT = 4     /* maps to ValueError */
@@ -47,9 +47,9 @@ enum { SDB_COUPLING_MEANFIELD = 0, SDB_COUPLING_PAIRWISE = 1 };
 typedef struct sdb_ctx sdb_ctx;
 typedef struct sdb_model sdb_model;
 
-/* One integration run: the fields of EngineConfig (engine.py:81-101) that the
- * device needs, after the host has validated them (engine.py:103-117,
- * 229-245) and computed chunks = iteration_count(...) (engine.py:163-179). */
+/* One integration run: the fields of EngineConfig (engine.py:44-64) that the
+ * device needs, after the host has validated them (engine.py:66-80,
+ * 192-208) and computed chunks = iteration_count(...) (engine.py:126-142). */
 typedef struct sdb_desc {
     int32_t model;        /* SDB_MODEL_KURAMOTO, or SDB_MODEL_EXPRESSION for sdb_run_model */
     int32_t nequat;       /* n oscillators */
@@ -61,7 +61,7 @@ typedef struct sdb_desc {
     int32_t lanes;        /* lanes per orbit (power of two, <= 32); 0 = autotune */
     uint64_t seed;        /* EngineConfig.seed reduced mod 2**64 (rng.py:145-147) */
     double dt;
-    int64_t ksteps;       /* steps per chunk; one sample per chunk (engine.py:268-299) */
+    int64_t ksteps;       /* steps per chunk; one sample per chunk (engine.py:231-262) */
     int64_t chunks;       /* k; samples = k + 1 */
     int64_t orbits;       /* rows in this call */
     int64_t orbit_offset; /* global orbit id of row 0 (noise is keyed by it) */
@@ -72,17 +72,17 @@ int sdb_device_count(void);
 
 /* Context over a list of devices; orbits of one run are sharded across them
  * in contiguous ranges (the analogue of partition_orbits + the worker pool,
- * engine.py:182-187, 302-311).  A device id may repeat (two shards on one GPU). */
+ * engine.py:145-150, 265-274).  A device id may repeat (two shards on one GPU). */
 sdb_status sdb_open(const int* devices, int ndevices, sdb_ctx** out);
 void sdb_close(sdb_ctx* ctx);
 const char* sdb_last_error(const sdb_ctx* ctx);
 
-/* Replaces run_batch's integration (engine.py:221-314).
+/* Replaces run_batch's integration (engine.py:184-277).
  * init:   [orbits][nequat]   params: [orbits][nparams]
  * values: [orbits][chunks+1][nequat], caller-allocated; sample 0 is written
- *         as a verbatim copy of init (engine.py:251), samples 1..k by the device.
+ *         as a verbatim copy of init (engine.py:214), samples 1..k by the device.
  * fail_step: [orbits]; absolute step index of the orbit's first non-finite
- *         state (engine.py:281-298) or -1.  Rows of failed orbits are NaN from
+ *         state (engine.py:244-261) or -1.  Rows of failed orbits are NaN from
  *         that step on. */
 sdb_status sdb_run(sdb_ctx* ctx, const sdb_desc* desc, const double* init,
                    const double* params, double* values, int64_t* fail_step);

@@ -112,7 +112,7 @@ def gaussian_from_words(w0, w1, w2, w3, m):
 
 def normals_for_orbits(seed, orbits, chunk, step, m):
     """Per-step Philox normals; rng.py:150-188 (engine passes chunk=step>>32,
-    step=step&mask, engine.py:273-277)."""
+    step=step&mask, engine.py:236-240)."""
     orbits = np.asarray(orbits, dtype=np.uint32)
     if m == 0:
         return np.empty((orbits.size, 0), dtype=np.float64)
@@ -303,7 +303,7 @@ def rk4_step(y, p, dt):
 
 
 def iteration_count(tspan, dt, ksteps, pad=False):
-    """engine.py:163-179."""
+    """engine.py:126-142."""
     ratio = tspan / (dt * ksteps)
     k = round(ratio)
     if k >= 1 and abs(ratio - k) <= 1e-9 * max(1.0, abs(ratio)):
@@ -314,18 +314,18 @@ def iteration_count(tspan, dt, ksteps, pad=False):
 
 
 # ---------------------------------------------------------------------------
-# The restated run loop (engine.py:221-314)
+# The restated run loop (engine.py:184-277)
 
 def integrate(init, params, *, dt, ksteps, chunks, seed=0, solver="em", nnoise=None,
               stream="philox", orbit_ids=None, threads=1, group=None, drift=None,
               diffusion=None):
     """Restated ``run_batch`` inner loop for global ``orbit_ids``.
 
-    engine.py:260-300 (integrate_group) with the stepper of engine.py:190-218.
+    engine.py:223-263 (integrate_group) with the stepper of engine.py:153-181.
     Returns (times, values, failures) where failures are
-    (orbit, chunk, step, time, reason) tuples sorted by orbit (engine.py:312).
+    (orbit, chunk, step, time, reason) tuples sorted by orbit (engine.py:275).
     ``threads``/``group`` mirror the reference's pool over contiguous orbit
-    groups (engine.py:302-311); they never change the result.  ``drift(t, y,
+    groups (engine.py:265-274); they never change the result.  ``drift(t, y,
     p)`` / ``diffusion(t, y, p, noise)`` default to the Kuramoto system; pass
     :func:`expression_model` functions for a template model.
     """

@@ -1,13 +1,16 @@
 """Builds libsdeb200.so in-tree with nvcc for sm_100a (no JIT, no torch build).
 
 ``python -m paper_1908_03869_b200._build`` or ``__graft_entry__.build()``.
-Objects compile in parallel; the shared library links cudart statically so
+Objects compile in parallel and are rebuilt when their content key changes
+(sha256 of the source, every header, the flags and nvcc's version; stored
+next to each object as ``<obj>.key``).  The shared library links cudart statically so
 it loads (and exports every include/sdeb200.h symbol) on a machine without a
 GPU, which the CPU test tier checks.
 """
 
 from __future__ import annotations
 
+import hashlib
 import os
 import shutil
 import subprocess
@@ -54,12 +57,50 @@ def _mtime(path: str) -> float:
     return os.path.getmtime(path) if os.path.exists(path) else -1.0
 
 
+_TOOLCHAIN = None
+
+
+def toolchain_id() -> str:
+    """nvcc's version banner: part of every build key, so a different toolkit
+    rebuilds everything."""
+    global _TOOLCHAIN
+    if _TOOLCHAIN is None:
+        res = subprocess.run([nvcc(), "--version"], capture_output=True, text=True)
+        _TOOLCHAIN = res.stdout.strip()
+    return _TOOLCHAIN
+
+
+def _digest(*parts) -> str:
+    h = hashlib.sha256()
+    for part in parts:
+        if isinstance(part, str) and os.path.isfile(part):
+            with open(part, "rb") as f:
+                h.update(f.read())
+        else:
+            h.update(repr(part).encode())
+        h.update(b"\0")
+    return h.hexdigest()
+
+
+def _stamp_ok(target: str, key: str) -> bool:
+    """The target exists and was built from exactly this key (content hash of
+    sources, headers, flags and toolchain -- not modification times, which do
+    not survive a copy of the tree)."""
+    try:
+        with open(target + ".key") as f:
+            return os.path.exists(target) and f.read().strip() == key
+    except OSError:
+        return False
+
+
+def _write_stamp(target: str, key: str) -> None:
+    with open(target + ".key", "w") as f:
+        f.write(key + "\n")
+
+
 def _write_rtc_headers() -> None:
     """sdeb_rtc_headers.inc: {name, raw text} of every header a generated
-    program includes (rewritten only when a header changed)."""
-    if os.path.exists(RTC_INC) and _mtime(RTC_INC) >= max(
-            _mtime(os.path.join(CSRC, h)) for h in RTC_HEADERS):
-        return
+    program includes (rewritten only when its content changes)."""
     parts = ["const RtcHeader kRtcHeaders[] = {"]
     for h in RTC_HEADERS:
         with open(os.path.join(CSRC, h)) as f:
@@ -70,9 +111,14 @@ def _write_rtc_headers() -> None:
         body = "\n".join('R"SDEBRTC(%s)SDEBRTC"' % c for c in chunks)
         parts.append('    {"%s",\n%s},' % (h, body))
     parts.append("};")
+    text = "\n".join(parts) + "\n"
+    if os.path.exists(RTC_INC):
+        with open(RTC_INC) as f:
+            if f.read() == text:
+                return
     tmp = RTC_INC + ".tmp"
     with open(tmp, "w") as f:
-        f.write("\n".join(parts) + "\n")
+        f.write(text)
     os.replace(tmp, RTC_INC)
 
 
@@ -82,13 +128,15 @@ def _compile(src: str, log: list) -> str:
     if src == "sdeb_dsl.cu":
         deps.append(RTC_INC)
     deps.append(os.path.join(ROOT, "include", "sdeb200.h"))
-    if _mtime(obj) >= max(_mtime(d) for d in deps):
+    key = _digest(toolchain_id(), NVCC_FLAGS, src, *deps)
+    if _stamp_ok(obj, key):
         return obj
     cmd = [nvcc()] + NVCC_FLAGS + ["-c", os.path.join(CSRC, src), "-o", obj]
     res = subprocess.run(cmd, capture_output=True, text=True)
     log.append((src, res.stdout + res.stderr))
     if res.returncode != 0:
         raise RuntimeError("nvcc failed for %s:\n%s" % (src, res.stdout + res.stderr))
+    _write_stamp(obj, key)
     return obj
 
 
@@ -101,12 +149,14 @@ def build(verbose: bool = False, force: bool = False) -> str:
     log: list = []
     with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as pool:
         objs = list(pool.map(lambda s: _compile(s, log), SOURCES))
-    if force or _mtime(LIB) < max(_mtime(o) for o in objs):
-        cmd = ([nvcc()] + ARCH + ["-shared", "-cudart", "static", "-o", LIB] + objs
-               + ["-L", CUDA_LIB, "-lnvrtc", "-Xlinker", "-rpath=" + CUDA_LIB])
+    cmd = ([nvcc()] + ARCH + ["-shared", "-cudart", "static", "-o", LIB] + objs
+           + ["-L", CUDA_LIB, "-lnvrtc", "-Xlinker", "-rpath=" + CUDA_LIB])
+    lib_key = _digest(toolchain_id(), cmd, *objs)
+    if force or not _stamp_ok(LIB, lib_key):
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
             raise RuntimeError("link failed:\n" + res.stdout + res.stderr)
+        _write_stamp(LIB, lib_key)
     if verbose:
         for src, text in log:
             sys.stdout.write("== %s\n%s" % (src, text))

@@ -2,7 +2,7 @@
 
 There is deliberately no fallback: if the library is missing, or no CUDA
 device is visible, every device entry point raises.  ctypes releases the GIL
-for the duration of each call (the reference's worker pool, engine.py:302-311,
+for the duration of each call (the reference's worker pool, engine.py:265-274,
 becomes per-device host threads inside the library).
 """
 
@@ -108,7 +108,7 @@ SIGNATURES = {
 }
 
 _lib = None
-_lib_lock = threading.Lock()
+_lib_lock = threading.RLock()
 _contexts: dict = {}
 
 
@@ -163,18 +163,27 @@ def device_count() -> int:
 
 
 def context(devices=None):
-    """Cached sdb_ctx for a device tuple (default: SDEB200_DEVICES or (0,))."""
+    """Cached sdb_ctx for a device tuple (default: SDEB200_DEVICES or (0,)).
+
+    Shared by every caller in the process.  The library serialises the public
+    calls on one context (sdb_ctx::call_mu) and reports errors per calling
+    thread, so concurrent run_batch calls from several Python threads are
+    safe; device-buffer calls on different streams are ordered after each
+    other's use of the context's scratch buffers."""
     if devices is None:
         env = os.environ.get("SDEB200_DEVICES")
         devices = tuple(int(d) for d in env.split(",")) if env else (0,)
     devices = tuple(int(d) for d in devices)
     ctx = _contexts.get(devices)
     if ctx is None:
-        arr = (ctypes.c_int * len(devices))(*devices)
-        out = ctypes.c_void_p()
-        check(lib().sdb_open(arr, len(devices), ctypes.byref(out)), None, "sdb_open")
-        ctx = out.value
-        _contexts[devices] = ctx
+        with _lib_lock:  # one context per device tuple, also under concurrent first calls
+            ctx = _contexts.get(devices)
+            if ctx is None:
+                arr = (ctypes.c_int * len(devices))(*devices)
+                out = ctypes.c_void_p()
+                check(lib().sdb_open(arr, len(devices), ctypes.byref(out)), None, "sdb_open")
+                ctx = out.value
+                _contexts[devices] = ctx
     return ctx
 
 

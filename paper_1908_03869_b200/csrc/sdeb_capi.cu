@@ -1,7 +1,7 @@
 // C ABI (include/sdeb200.h): contexts, validation, sharding, layout
 // autotune, host<->device staging.  The reference equivalent is run_batch's
-// driver (engine.py:221-314) and its thread pool over contiguous orbit
-// groups (engine.py:182-187, 302-311): here the groups are per-device shards
+// driver (engine.py:184-277) and its thread pool over contiguous orbit
+// groups (engine.py:145-150, 265-274): here the groups are per-device shards
 // driven by one host thread each, and the per-group Python step loop is the
 // fused kernel of sdeb_kuramoto.cuh.
 #include <cuda_runtime.h>
@@ -121,6 +121,10 @@ struct Slot {
     int32_t tight = 0;
     int32_t lane_width = 0;  // oscillators per lane (J) of the last launch
     int32_t tiles = 0;  // orbit tiles of the last host-buffer run
+    // end of the last launch that used this slot's scratch (state, rng, work),
+    // and the stream it ran on: a launch on another stream waits for it first
+    cudaEvent_t done = nullptr;
+    cudaStream_t done_stream = nullptr;
     std::string error;
 };
 
@@ -152,6 +156,11 @@ struct sdb_ctx {
     int32_t last_tiles = 0;
     std::map<TuneKey, Layout> tune;
     std::mutex mu;  // guards tune and error: shard threads of one run share the context
+    // Serialises the public entry points on one context: its slots' device
+    // buffers and pinned staging are reused by every call, so two host
+    // threads calling sdb_run* at once must take turns (the reference's
+    // run_batch is reentrant; so is this one, per context).
+    std::mutex call_mu;
 };
 
 namespace {
@@ -169,6 +178,21 @@ sdb_status fail_with(sdb_ctx* ctx, sdb_status st, const char* fmt, ...) {
     g_thread_error = buf;
     return st;
 }
+
+// Held for the duration of one public call on a context (sdb_ctx::call_mu);
+// starts the call with no error recorded for this thread or the context.
+struct CallScope {
+    std::unique_lock<std::mutex> lock;
+    explicit CallScope(sdb_ctx* ctx) : lock(ctx->call_mu) {
+        g_thread_error.clear();
+        std::lock_guard<std::mutex> l(ctx->mu);
+        ctx->error.clear();
+    }
+};
+
+#define SDB_ENTRY(ctx)                                                               \
+    if (!(ctx)) return fail_with(nullptr, SDB_ERR_ARGUMENT, "null context");        \
+    CallScope call_scope__(ctx)
 
 sdb_status cuda_fail(sdb_ctx* ctx, cudaError_t e, const char* what) {
     return fail_with(ctx, SDB_ERR_CUDA, "%s: %s (%s)", what, cudaGetErrorString(e),
@@ -715,12 +739,32 @@ sdb_status launch_model(sdb_ctx* ctx, Slot& s, const sdb_desc& d, sdb_model* m,
     return SDB_OK;
 }
 
+sdb_status launch_device_ordered(sdb_ctx* ctx, Slot& s, const sdb_desc& d, sdb_model* m,
+                                 const double* d_init, const double* d_params, double* d_values,
+                                 int64_t* d_fail, cudaStream_t st, int out_mode);
+
 // out_mode 0: samples of the state, d_values [orbits][chunks][n]; 1 (Kuramoto
 // only): the order parameter, d_values [orbits][2][chunks + 1] (r, Phi planes)
 // with sample 0.
 sdb_status launch_device(sdb_ctx* ctx, Slot& s, const sdb_desc& d, sdb_model* m,
                          const double* d_init, const double* d_params, double* d_values,
                          int64_t* d_fail, cudaStream_t st, int out_mode = 0) {
+    // the slot's scratch (continuation state, stream states, persistent
+    // counters, autotune buffers) may still be in use by a launch on another
+    // stream: order this one after it
+    if (!s.done) SDB_CUDA(ctx, cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming));
+    if (s.done_stream != nullptr && s.done_stream != st) SDB_CUDA(ctx, cudaStreamWaitEvent(st, s.done, 0));
+    sdb_status rc0 = launch_device_ordered(ctx, s, d, m, d_init, d_params, d_values, d_fail, st,
+                                           out_mode);
+    if (rc0 != SDB_OK) return rc0;
+    SDB_CUDA(ctx, cudaEventRecord(s.done, st));
+    s.done_stream = st;
+    return SDB_OK;
+}
+
+sdb_status launch_device_ordered(sdb_ctx* ctx, Slot& s, const sdb_desc& d, sdb_model* m,
+                                 const double* d_init, const double* d_params, double* d_values,
+                                 int64_t* d_fail, cudaStream_t st, int out_mode) {
     if (m) {
         if (out_mode != 0)
             return fail_with(ctx, SDB_ERR_UNSUPPORTED,
@@ -957,7 +1001,7 @@ int64_t shard_tiles(const sdb_desc& d, int64_t rows, int device) {
 //   inputs  host rows -> pinned slot (parallel memcpy) -> DMA on s.h2d
 //   kernel  tile t on s.stream after its inputs landed
 //   outputs DMA on s.d2h after the tile's kernel -> pinned slot -> host rows,
-//           written as [init row | samples 1..k] (engine.py:250-251)
+//           written as [init row | samples 1..k] (engine.py:213-214)
 // Pinned slots alternate (kPinSlots each way); a slot is refilled only after
 // the DMA that last used it completed.  Input staging of tile t+1 is issued
 // before the outputs of tile t are drained, so host copies, both DMA
@@ -1308,8 +1352,14 @@ sdb_status run_host(sdb_ctx* ctx, const sdb_desc& d, sdb_model* m, const double*
     ctx->last_tight = ctx->slots[0].tight;
     ctx->last_lane_width = ctx->slots[0].lane_width;
     ctx->last_tiles = ctx->slots[0].tiles;
-    for (int64_t g = 0; g < used; ++g)
-        if (status[g] != SDB_OK) return status[g];
+    for (int64_t g = 0; g < used; ++g) {
+        if (status[g] != SDB_OK) {
+            // a shard thread recorded the message: make it this thread's too
+            std::lock_guard<std::mutex> lock(ctx->mu);
+            g_thread_error = ctx->error;
+            return status[g];
+        }
+    }
     return SDB_OK;
 }
 
@@ -1434,6 +1484,7 @@ void sdb_close(sdb_ctx* ctx) {
             b->release();
         for (PinBuf* b : {&s.pin_in[0], &s.pin_in[1], &s.pin_out[0], &s.pin_out[1]}) b->release();
         if (s.ev_in) cudaEventDestroy(s.ev_in);
+        if (s.done) cudaEventDestroy(s.done);
         for (cudaEvent_t e : s.ev_tile) cudaEventDestroy(e);
         for (cudaStream_t st : {s.stream, s.h2d, s.d2h})
             if (st) cudaStreamDestroy(st);
@@ -1441,9 +1492,11 @@ void sdb_close(sdb_ctx* ctx) {
     delete ctx;
 }
 
+// The calling thread's last error (every failing call records it there, also
+// when a shard thread failed); the context's as a fallback.
 const char* sdb_last_error(const sdb_ctx* ctx) {
-    if (ctx && !ctx->error.empty()) return ctx->error.c_str();
-    return g_thread_error.c_str();
+    if (!g_thread_error.empty() || !ctx) return g_thread_error.c_str();
+    return ctx->error.c_str();
 }
 
 int64_t sdb_last_launch_count(const sdb_ctx* ctx) { return ctx ? ctx->launches : 0; }
@@ -1462,8 +1515,7 @@ void sdb_last_layout(const sdb_ctx* ctx, int32_t* lanes, int32_t* persistent,
 
 sdb_status sdb_run(sdb_ctx* ctx, const sdb_desc* desc, const double* init, const double* params,
                    double* values, int64_t* fail_step) {
-    if (!ctx) return fail_with(nullptr, SDB_ERR_ARGUMENT, "null context");
-    ctx->error.clear();
+    SDB_ENTRY(ctx);
     sdb_status rc = validate(ctx, desc);
     if (rc != SDB_OK) return rc;
     return run_host(ctx, *desc, nullptr, init, params, values, fail_step);
@@ -1472,8 +1524,7 @@ sdb_status sdb_run(sdb_ctx* ctx, const sdb_desc* desc, const double* init, const
 sdb_status sdb_run_device(sdb_ctx* ctx, const sdb_desc* desc, const double* d_init,
                           const double* d_params, double* d_values, int64_t* d_fail_step,
                           void* stream) {
-    if (!ctx) return fail_with(nullptr, SDB_ERR_ARGUMENT, "null context");
-    ctx->error.clear();
+    SDB_ENTRY(ctx);
     sdb_status rc = validate(ctx, desc);
     if (rc != SDB_OK) return rc;
     return run_dev(ctx, *desc, nullptr, d_init, d_params, d_values, d_fail_step, stream);
@@ -1484,8 +1535,7 @@ sdb_status sdb_run_device(sdb_ctx* ctx, const sdb_desc* desc, const double* d_in
 sdb_status sdb_run_to_file(sdb_ctx* ctx, sdb_model* model, const sdb_desc* desc,
                            const double* init, const double* params, const char* path,
                            int64_t offset, int64_t* fail_step) {
-    if (!ctx) return fail_with(nullptr, SDB_ERR_ARGUMENT, "null context");
-    ctx->error.clear();
+    SDB_ENTRY(ctx);
     sdb_status rc = model ? validate_model(ctx, desc, model) : validate(ctx, desc);
     if (rc != SDB_OK) return rc;
     if (!path || offset < 0) return fail_with(ctx, SDB_ERR_ARGUMENT, "bad store file arguments");
@@ -1501,8 +1551,7 @@ sdb_status sdb_run_to_file(sdb_ctx* ctx, sdb_model* model, const sdb_desc* desc,
 
 sdb_status sdb_run_coherence(sdb_ctx* ctx, const sdb_desc* desc, const double* init,
                              const double* params, double* r_phi, int64_t* fail_step) {
-    if (!ctx) return fail_with(nullptr, SDB_ERR_ARGUMENT, "null context");
-    ctx->error.clear();
+    SDB_ENTRY(ctx);
     sdb_status rc = validate(ctx, desc);
     if (rc != SDB_OK) return rc;
     return run_host(ctx, *desc, nullptr, init, params, r_phi, fail_step, 1);
@@ -1511,8 +1560,7 @@ sdb_status sdb_run_coherence(sdb_ctx* ctx, const sdb_desc* desc, const double* i
 sdb_status sdb_run_coherence_device(sdb_ctx* ctx, const sdb_desc* desc, const double* d_init,
                                     const double* d_params, double* d_r_phi, int64_t* d_fail_step,
                                     void* stream) {
-    if (!ctx) return fail_with(nullptr, SDB_ERR_ARGUMENT, "null context");
-    ctx->error.clear();
+    SDB_ENTRY(ctx);
     sdb_status rc = validate(ctx, desc);
     if (rc != SDB_OK) return rc;
     return run_dev(ctx, *desc, nullptr, d_init, d_params, d_r_phi, d_fail_step, stream, 1);
@@ -1520,6 +1568,7 @@ sdb_status sdb_run_coherence_device(sdb_ctx* ctx, const sdb_desc* desc, const do
 
 sdb_status sdb_order_parameter(sdb_ctx* ctx, int32_t n, int64_t rows, const double* phases,
                                double* r, double* phi) {
+    SDB_ENTRY(ctx);
     sdb_status rc = utility_prologue(ctx);
     if (rc != SDB_OK) return rc;
     if (n < 1 || rows < 0 || !phases || !r || !phi)
@@ -1593,8 +1642,7 @@ sdb_status sdb_model_build(sdb_model* m, int32_t kind) {
 
 sdb_status sdb_run_model(sdb_ctx* ctx, sdb_model* m, const sdb_desc* desc, const double* init,
                          const double* params, double* values, int64_t* fail_step) {
-    if (!ctx) return fail_with(nullptr, SDB_ERR_ARGUMENT, "null context");
-    ctx->error.clear();
+    SDB_ENTRY(ctx);
     sdb_status rc = validate_model(ctx, desc, m);
     if (rc != SDB_OK) return rc;
     return run_host(ctx, *desc, m, init, params, values, fail_step);
@@ -1603,8 +1651,7 @@ sdb_status sdb_run_model(sdb_ctx* ctx, sdb_model* m, const sdb_desc* desc, const
 sdb_status sdb_run_model_device(sdb_ctx* ctx, sdb_model* m, const sdb_desc* desc,
                                 const double* d_init, const double* d_params, double* d_values,
                                 int64_t* d_fail_step, void* stream) {
-    if (!ctx) return fail_with(nullptr, SDB_ERR_ARGUMENT, "null context");
-    ctx->error.clear();
+    SDB_ENTRY(ctx);
     sdb_status rc = validate_model(ctx, desc, m);
     if (rc != SDB_OK) return rc;
     return run_dev(ctx, *desc, m, d_init, d_params, d_values, d_fail_step, stream);
@@ -1612,6 +1659,7 @@ sdb_status sdb_run_model_device(sdb_ctx* ctx, sdb_model* m, const sdb_desc* desc
 
 sdb_status sdb_model_eval(sdb_ctx* ctx, sdb_model* m, int32_t which, double t, int64_t count,
                           const double* y, const double* p, const double* noise, double* out) {
+    SDB_ENTRY(ctx);
     if (!m) return fail_with(ctx, SDB_ERR_ARGUMENT, "null model");
     if (which != 0 && which != 1) return fail_with(ctx, SDB_ERR_ARGUMENT, "which must be 0 or 1");
     if (which == 1 && m->nnoise > 0 && !noise)
@@ -1623,6 +1671,7 @@ sdb_status sdb_model_eval(sdb_ctx* ctx, sdb_model* m, int32_t which, double t, i
 sdb_status sdb_model_step(sdb_ctx* ctx, sdb_model* m, int32_t solver, double t, double dt,
                           int64_t count, const double* y, const double* p, const double* noise,
                           double* out) {
+    SDB_ENTRY(ctx);
     if (!m) return fail_with(ctx, SDB_ERR_ARGUMENT, "null model");
     if (!(dt > 0.0)) return fail_with(ctx, SDB_ERR_ARGUMENT, "dt must be positive");
     int kind;
@@ -1641,6 +1690,7 @@ sdb_status sdb_model_step(sdb_ctx* ctx, sdb_model* m, int32_t solver, double t, 
 }
 
 sdb_status sdb_philox_words(sdb_ctx* ctx, const uint32_t* in, int64_t count, uint32_t* out) {
+    SDB_ENTRY(ctx);
     sdb_status rc = utility_prologue(ctx);
     if (rc != SDB_OK) return rc;
     if (count <= 0) return SDB_OK;
@@ -1656,6 +1706,7 @@ sdb_status sdb_philox_words(sdb_ctx* ctx, const uint32_t* in, int64_t count, uin
 
 sdb_status sdb_normals(sdb_ctx* ctx, int32_t stream, uint64_t seed, const uint32_t* orbits,
                        int64_t count, uint32_t chunk, uint32_t step, int32_t m, double* out) {
+    SDB_ENTRY(ctx);
     sdb_status rc = utility_prologue(ctx);
     if (rc != SDB_OK) return rc;
     if (stream < SDB_STREAM_PHILOX || stream > SDB_STREAM_XOSHIRO256PP)
@@ -1677,6 +1728,7 @@ sdb_status sdb_normals(sdb_ctx* ctx, int32_t stream, uint64_t seed, const uint32
 
 sdb_status sdb_stream_raw(sdb_ctx* ctx, int32_t stream, uint64_t seed, uint64_t orbit,
                           uint64_t block, int64_t count, uint64_t* out) {
+    SDB_ENTRY(ctx);
     sdb_status rc = utility_prologue(ctx);
     if (rc != SDB_OK) return rc;
     if (stream != SDB_STREAM_SFC64 && stream != SDB_STREAM_XOSHIRO256PP)
@@ -1692,6 +1744,7 @@ sdb_status sdb_stream_raw(sdb_ctx* ctx, int32_t stream, uint64_t seed, uint64_t 
 
 sdb_status sdb_sampling_uniforms(sdb_ctx* ctx, uint64_t seed, const uint32_t* orbits,
                                  int64_t count, int32_t ncols, double* out) {
+    SDB_ENTRY(ctx);
     sdb_status rc = utility_prologue(ctx);
     if (rc != SDB_OK) return rc;
     if (ncols < 0) return fail_with(ctx, SDB_ERR_ARGUMENT, "count must be >= 0");
@@ -1709,6 +1762,7 @@ sdb_status sdb_sampling_uniforms(sdb_ctx* ctx, uint64_t seed, const uint32_t* or
 sdb_status sdb_sample_kuramoto(sdb_ctx* ctx, int32_t n, uint64_t seed, const uint32_t* orbits,
                                int64_t count, double omega_lo, double omega_hi, double noise_lo,
                                double noise_hi, double coupling, double* init, double* params) {
+    SDB_ENTRY(ctx);
     sdb_status rc = utility_prologue(ctx);
     if (rc != SDB_OK) return rc;
     if (n < 1) return fail_with(ctx, SDB_ERR_ARGUMENT, "need at least one oscillator");
@@ -1732,6 +1786,7 @@ static sdb_status per_step(sdb_ctx* ctx, int kind_solver, int kind_stream, int32
                            int32_t nparams, int32_t nnoise, int32_t coupling, int64_t count,
                            double dt, const double* y, const double* p, const double* noise,
                            double* out) {
+    SDB_ENTRY(ctx);
     sdb_status rc = utility_prologue(ctx);
     if (rc != SDB_OK) return rc;
     if (n < 1 || n > kMaxN) return fail_with(ctx, SDB_ERR_UNSUPPORTED, "nequat=%d unsupported", n);
@@ -1797,6 +1852,7 @@ sdb_status sdb_step(sdb_ctx* ctx, int32_t solver, int32_t n, int32_t nparams, in
 }
 
 sdb_status sdb_fp64_peak(sdb_ctx* ctx, double* ops_per_s, double* ms_out) {
+    SDB_ENTRY(ctx);
     sdb_status rc = utility_prologue(ctx);
     if (rc != SDB_OK) return rc;
     int sms = 0;
@@ -1830,6 +1886,7 @@ sdb_status sdb_fp64_peak(sdb_ctx* ctx, double* ops_per_s, double* ms_out) {
 
 sdb_status sdb_math_probe(sdb_ctx* ctx, int32_t func, const double* x, int64_t count,
                           double* out) {
+    SDB_ENTRY(ctx);
     sdb_status rc = utility_prologue(ctx);
     if (rc != SDB_OK) return rc;
     if (func < 0 || func > 8) return fail_with(ctx, SDB_ERR_ARGUMENT, "unknown math probe %d", func);

@@ -1,6 +1,6 @@
 // Fused Kuramoto ensemble stepper for sm_100a.
 //
-// Replaces the reference's chunk x step loop (engine.py:260-300) with the
+// Replaces the reference's chunk x step loop (engine.py:223-263) with the
 // noise draw (rng.py:150-188), the drift (model.py:188-196), the diffusion
 // (model.py:199-201) and the em/euler/rk4 update (solvers.py:63-88) fused
 // into ONE persistent-per-orbit kernel: state, parameters and stateful RNG
@@ -514,7 +514,7 @@ __device__ __forceinline__ void run_item(const RunArgs& a, int64_t cg, uint64_t 
                 }
             }
             // isfinite(y).all(-1) per orbit; first failure recorded, row -> NaN
-            // (engine.py:281-298).  Lanes record independently; the group
+            // (engine.py:244-261).  Lanes record independently; the group
             // minimum is the orbit's first failing step.  Padding oscillators
             // stay 0, so no validity predicate is needed.
             bool bad = false;
@@ -531,7 +531,7 @@ __device__ __forceinline__ void run_item(const RunArgs& a, int64_t cg, uint64_t 
             }
             }
             if (step == next_sample) {
-                // one sample per chunk (engine.py:299)
+                // one sample per chunk (engine.py:262)
                 next_sample += ks;
                 const int64_t gf = group_fail(fail, lanes);
                 if (gf >= 0 && a.check_finite) {

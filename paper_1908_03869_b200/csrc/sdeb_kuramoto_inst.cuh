@@ -24,10 +24,23 @@ static cudaError_t launch_one(const RunArgs& a, cudaStream_t st) {
     return cudaGetLastError();
 }
 
+// Largest shared memory one CTA may use on the current device (opt-in).
+static inline size_t smem_optin_bytes() {
+    int dev = 0, optin = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess)
+        return 48 * 1024;
+    return size_t(optin);
+}
+
 template <int J, int S, int R, int C, int P>
 static cudaError_t occupancy_one(size_t smem, int* blocks) {
     const size_t need = pairwise_smem_bytes(J, C);
     if (smem < need) smem = need;
+    if (smem + kStaticSmemBytes > smem_optin_bytes()) {  // cannot launch: no resident CTA
+        *blocks = 0;
+        return cudaSuccess;
+    }
     if (smem + kStaticSmemBytes > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(kuramoto_run_kernel<J, S, R, C, P>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -3,7 +3,7 @@
 
 ``run_batch`` keeps the reference's signature, validation order, error
 messages, store layout and failure semantics; the chunk x step loop
-(engine.py:260-300) runs as one fused CUDA kernel per device shard behind
+(engine.py:223-263) runs as one fused CUDA kernel per device shard behind
 the C ABI ``sdb_run`` (include/sdeb200.h).
 
 Noise is addressed by the absolute step index exactly as in the reference
@@ -45,12 +45,12 @@ _MASK64 = 0xFFFFFFFFFFFFFFFF
 
 
 class ConfigError(ValueError):
-    """A run configuration that cannot be executed as requested (engine.py:77-78)."""
+    """A run configuration that cannot be executed as requested (engine.py:40-41)."""
 
 
 @dataclass(frozen=True)
 class EngineConfig:
-    """Description of one integration run (engine.py:81-122)."""
+    """Description of one integration run (engine.py:44-85)."""
 
     dt: float
     tspan: float
@@ -99,7 +99,7 @@ class EngineConfig:
             object.__setattr__(self, "devices", devs)
 
     def worker_count(self) -> int:
-        """engine.py:119-122 (a scheduling hint only; never changes results)."""
+        """engine.py:82-85 (a scheduling hint only; never changes results)."""
         if self.threads == "all":
             return os.cpu_count() or 1
         return self.threads
@@ -107,7 +107,7 @@ class EngineConfig:
 
 @dataclass(frozen=True)
 class OrbitFailure:
-    """First solver failure of one orbit; the rest of its row is NaN (engine.py:125-133)."""
+    """First solver failure of one orbit; the rest of its row is NaN (engine.py:88-96)."""
 
     orbit: int
     chunk: int
@@ -118,7 +118,7 @@ class OrbitFailure:
 
 @dataclass
 class TrajectoryStore:
-    """Sampled states of every orbit (engine.py:136-160): ``values`` is
+    """Sampled states of every orbit (engine.py:99-123): ``values`` is
     (orbits, samples, nequat), sample 0 the initial state verbatim."""
 
     times: np.ndarray
@@ -141,7 +141,7 @@ class TrajectoryStore:
 
 
 def iteration_count(tspan: float, dt: float, ksteps: int, pad: bool = False) -> int:
-    """Number of chunks k = tspan / (dt * ksteps) (engine.py:163-179)."""
+    """Number of chunks k = tspan / (dt * ksteps) (engine.py:126-142)."""
     if dt <= 0 or tspan <= 0 or ksteps < 1:
         raise ConfigError("tspan, dt and ksteps must be positive")
     ratio = tspan / (dt * ksteps)
@@ -156,7 +156,7 @@ def iteration_count(tspan: float, dt: float, ksteps: int, pad: bool = False) -> 
 
 
 def partition_orbits(orbits: int, chunk_group: int) -> list[range]:
-    """Contiguous orbit ranges of width chunk_group (engine.py:182-187)."""
+    """Contiguous orbit ranges of width chunk_group (engine.py:145-150)."""
     if orbits < 1 or chunk_group < 1:
         raise ConfigError("orbits and chunk_group must be >= 1")
     return [range(start, min(start + chunk_group, orbits))
@@ -164,7 +164,7 @@ def partition_orbits(orbits: int, chunk_group: int) -> list[range]:
 
 
 def _check_stepper(model: ModelSpec, config: EngineConfig):
-    """engine.py:190-197: a deterministic solver on a noisy model is an error."""
+    """engine.py:153-160: a deterministic solver on a noisy model is an error."""
     info = get_solver(config.solver)
     if not info.stochastic and model.nnoise > 0:
         raise ConfigError(
@@ -204,7 +204,7 @@ def make_desc(model: ModelSpec, config: EngineConfig, chunks: int, orbits: int,
 def failures_from_steps(fail_step: np.ndarray, ksteps: int, dt: float,
                         orbit_offset: int = 0) -> list[OrbitFailure]:
     """Per-orbit first-failure steps -> OrbitFailure records sorted by orbit
-    (engine.py:294-298, 312)."""
+    (engine.py:257-261, 275)."""
     out = []
     for idx in np.nonzero(fail_step >= 0)[0]:
         s = int(fail_step[idx])
@@ -224,7 +224,7 @@ def shard_bounds(orbits: int, world: int, rank: int) -> tuple[int, int]:
 
 def validate_run(model: ModelSpec, config: EngineConfig, batch: OrbitBatch, orbit_offset: int = 0,
                  store_cap: bool = True) -> int:
-    """run_batch's checks in the reference's order (engine.py:229-247); returns
+    """run_batch's checks in the reference's order (engine.py:192-210); returns
     the chunk count.  ``store_cap=False`` skips the trajectory-store size cap
     (runs that never materialise the store, e.g. analysis.run_coherence)."""
     batch.check_against(model)
@@ -253,7 +253,7 @@ def validate_run(model: ModelSpec, config: EngineConfig, batch: OrbitBatch, orbi
 def run_batch(model: ModelSpec, config: EngineConfig, batch: OrbitBatch, *,
               orbit_offset: int = 0) -> TrajectoryStore:
     """Integrate every orbit of the batch on the GPU and sample once per chunk
-    (engine.py:221-314).  Validation happens before any device allocation,
+    (engine.py:184-277).  Validation happens before any device allocation,
     in the reference's order.
 
     ``orbit_offset`` (keyword, default 0 = the reference's numbering) is the
@@ -296,11 +296,19 @@ def run_batch_sharded(model: ModelSpec, config: EngineConfig, batch: OrbitBatch,
     ``gather`` (e.g. a torch.distributed all_gather_object wrapper) may
     assemble the full store on the host afterwards.  The assembled store is
     bit-identical to a single-process run (noise is keyed by global id)."""
+    # every rank validates the whole run first: a bad configuration raises on
+    # all ranks alike, before any of them reaches the collective in ``gather``
+    chunks = validate_run(model, config, batch)
     lo, hi = shard_bounds(batch.orbits, world, rank)
-    part = OrbitBatch(init=batch.init[lo:hi], params=batch.params[lo:hi])
-    cfg = dataclasses.replace(config, orbits=hi - lo,
-                              devices=devices if devices is not None else config.devices)
-    store = run_batch(model, cfg, part, orbit_offset=lo)
+    if hi > lo:
+        part = OrbitBatch(init=batch.init[lo:hi], params=batch.params[lo:hi])
+        cfg = dataclasses.replace(config, orbits=hi - lo,
+                                  devices=devices if devices is not None else config.devices)
+        store = run_batch(model, cfg, part, orbit_offset=lo)
+    else:  # more ranks than orbits: this rank's shard is empty, it still joins the gather
+        times = np.arange(chunks + 1, dtype=np.float64) * (config.ksteps * config.dt)
+        store = TrajectoryStore(times=times, values=np.empty((0, chunks + 1, model.nequat)),
+                                model_name=model.name, config=config, failures=[])
     if gather is None:
         return store
     parts = gather((lo, store.values, store.failures))

@@ -79,14 +79,20 @@ def philox_block(ck: CounterKey) -> tuple[int, int, int, int]:
 
 
 def to_uniform(word):
-    """(word + 1) / 2**32 on (0, 1] (rng.py:121-129)."""
+    """(word + 1) / 2**32 on (0, 1] (rng.py:121-129).
+
+    Like ``box_muller`` below, a scalar helper of the reference's public API
+    (its tests use them as the scalar oracle of the normal transform), kept
+    on the host: one exact addition and scaling, never on the run path --
+    the stepper forms the same uniform on the device (csrc/sdeb_math.cuh)."""
     if isinstance(word, np.ndarray):
         return (word.astype(np.float64) + 1.0) * _TWO_NEG_32
     return (float(word) + 1.0) * _TWO_NEG_32
 
 
 def box_muller(u1: float, u2: float) -> tuple[float, float]:
-    """Scalar Box-Muller (rng.py:132-142)."""
+    """Scalar Box-Muller (rng.py:132-142); host scalar helper (see to_uniform).
+    Batched normals come from the device (``normals_for_orbits``)."""
     if u1 <= 0.0:
         raise ValueError("box_muller requires u1 > 0, got %r" % (u1,))
     r = math.sqrt(-2.0 * math.log(u1))

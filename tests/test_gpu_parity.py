@@ -471,3 +471,36 @@ def test_lane_layouts_bit_identical_huge_phases(stream):
               for L in _lane_options(n)]
     assert len({sdb.store_hash(s) for s in stores}) == 1
     assert {f.orbit for f in stores[0].failures} == set(range(1, m, 5))
+
+
+def test_concurrent_calls_on_one_context_are_serialised():
+    # the cached context is shared by every caller; two host threads
+    # running at once must each get exactly their single-threaded result
+    import threading
+    n, m = 16, 20000
+    model = sdb.kuramoto_model(n)
+    batches = [sdb.sample_kuramoto_batch(n, m, (0.2, 0.4), (0.01, 0.1), 0.3, seed=s)
+               for s in (1, 2, 3, 4)]
+    cfg = EngineConfig(dt=1e-3, tspan=0.2, ksteps=50, orbits=m, seed=9)
+    want = [sdb.store_hash(run_batch(model, cfg, b)) for b in batches]
+    got = [None] * len(batches)
+
+    def work(i):
+        got[i] = sdb.store_hash(run_batch(model, cfg, batches[i]))
+    threads = [threading.Thread(target=work, args=(i,)) for i in range(len(batches))]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert got == want
+
+
+def test_kuramoto_diffusion_eval_on_device_is_the_rounded_product():
+    n = 12
+    g = np.random.default_rng(4)
+    y = g.uniform(-3, 3, (7, n))
+    p = g.uniform(-1, 1, (7, 2 * n + 1))
+    z = g.standard_normal((7, n))
+    want = np.multiply(p[:, n + 1:], z)
+    assert np.array_equal(sdb.diffusion_eval(sdb.kuramoto_model(n), 0.0, y, p, z), want)
+    assert np.array_equal(sdb.model._kuramoto_diffusion(0.0, y, p, z), want)

@@ -4,6 +4,7 @@ messages -- /root/reference/pkg/tests/test_engine.py:23-97), the C-ABI
 library loading and symbol exports, and loud failure without a GPU."""
 
 import ctypes
+import dataclasses
 import os
 import re
 
@@ -172,3 +173,53 @@ def test_device_path_fails_loudly_without_gpu():
         run_batch(m, cfg, OrbitBatch(init=np.zeros((1, 2)), params=np.zeros((1, 5))))
     with pytest.raises(RuntimeError):
         sdb.rng.normals_for_step(0, 0, 0, 0, 4)
+
+
+def test_kuramoto_recognised_by_identity_not_name():
+    # a user's own callables that happen to share the built-in names (e.g. a
+    # phase-lag variant in their own model.py) must not be routed to the stepper
+    def _kuramoto_drift(t, y, p):
+        return y
+
+    def _kuramoto_diffusion(t, y, p, noise):
+        return noise
+    _kuramoto_drift.__module__ = _kuramoto_diffusion.__module__ = "model"
+    user = ModelSpec(name="lag", nequat=4, nparams=9, nnoise=4, drift=_kuramoto_drift,
+                     diffusion=_kuramoto_diffusion)
+    assert kuramoto_signature(user) is None
+    with pytest.raises(NotImplementedError):
+        sdb.model.require_device_model(user)
+
+
+def test_sharded_run_with_more_ranks_than_orbits_gives_empty_shards():
+    # world > orbits: the ranks with nothing to do still join the gather with
+    # an empty part instead of raising before the collective (a hang)
+    m = sdb.kuramoto_model(3)
+    cfg = EngineConfig(dt=0.5, tspan=1.0, ksteps=1, orbits=3)
+    batch = OrbitBatch(init=np.zeros((3, 3)), params=np.zeros((3, 7)))
+    seen = []
+
+    def gather(part):
+        seen.append(part)
+        return [part]
+    store = sdb.engine.run_batch_sharded(m, cfg, batch, world=4, rank=0, gather=gather)
+    assert sdb.engine.shard_bounds(3, 4, 0) == (0, 0)
+    assert store.values.shape == (0, 3, 3) and store.failures == []
+    assert seen and seen[0][0] == 0 and seen[0][1].shape == (0, 3, 3)
+    # an invalid configuration raises on every rank before the collective
+    with pytest.raises(sdb.ConfigError):
+        sdb.engine.run_batch_sharded(m, dataclasses.replace(cfg, orbits=4), batch, world=4,
+                                     rank=0, gather=gather)
+    assert len(seen) == 1
+
+
+def test_run_batch_to_file_checks_indices_before_touching_the_file(tmp_path):
+    from paper_1908_03869_b200 import dsl, storage
+    path = tmp_path / "keep.sdb1"
+    path.write_bytes(b"existing store")
+    bad = sdb.model_from_dsl("oob", 2, 1, 0, "p[i] * y[i]", "0")  # p has 1 column, i reaches 1
+    cfg = EngineConfig(dt=0.1, tspan=0.2, ksteps=1, orbits=2, solver="euler")
+    with pytest.raises(dsl.DomainError):
+        storage.run_batch_to_file(bad, cfg, OrbitBatch(init=np.zeros((2, 2)),
+                                                       params=np.zeros((2, 1))), path)
+    assert path.read_bytes() == b"existing store"
