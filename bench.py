@@ -2,37 +2,59 @@
 """Benchmark: orbit-steps/s of stochastic Kuramoto Euler-Maruyama on B200.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload cfg2] [--coupling meanfield|pairwise]
+                    [--workload cfg3] [--coupling meanfield|pairwise]
 
-One "step" = one complete run of the workload (all orbits x all SDE steps)
-through the fused kernel.  Default workload = BASELINE.json configs[1]
-(cfg2): n=16, 65,536 orbits over a 256 K x 256 sigma grid, sfc64 streams,
-dt=1e-3, 10^4 steps, final state only.  Multi-GPU (torchrun): each rank
-integrates its own 65,536-orbit shard with global orbit ids
-[rank*M, (rank+1)*M) -- weak scaling, no data-path collective (the path is
-embarrassingly parallel); timing is max over ranks.
+BASELINE.json's metric is "orbit-steps/s ... 1/2/4/8 B200"; the config it
+names at 1/2/4/8 GPUs is configs[2] (cfg3): stochastic Kuramoto n = 32, 64,
+128, 256, 2^20 orbits each, Philox, dt = 1e-3, final state.  The default
+workload "cfg3" runs all four sizes; the headline line is the largest
+(n = 256, 100 steps), the other sizes are under "sizes", and cfg2
+(BASELINE configs[1], n = 16, 65,536 orbits, sfc64, 10^4 steps) is under
+"secondary".
 
-  value    device-resident inputs (sdb_run_device), CUDA events around each
-           kernel launch, L2 flushed (512 MiB memset) between timed steps
-           outside the event pairs.
-  e2e      the public API run_batch() with numpy host buffers: H2D of
-           init/params and D2H of the store inside every timed step.
-  roofline FP64 pipe: algorithmic FP64 lane-ops of the kernel's algorithm
-            / kernel time, against the FP64 DFMA peak
-           measured live (sdb_fp64_peak; MEASURED_PEAKS.json has no FP64 figure).
-  cpu_baseline  the oracle port (numpy restatement of the reference's
-           run_batch, same op order, same thread pool) on a bounded sample.
---impl reference times that CPU implementation alone (rank 0).
+One "step" = one complete run of the workload (all orbits x all SDE steps).
+Scaling is STRONG: the fixed batch of the workload is split into contiguous
+orbit shards [g*M/N, (g+1)*M/N) with their global orbit ids,
+so the results are bit-identical for any N.  N GPUs:
+  * under torchrun (WORLD_SIZE = N): one process per GPU, rank r runs shard
+    r on LOCAL_RANK; time = max over ranks (NCCL all-reduce of one float,
+    timing only -- the data path has no collective);
+  * without torchrun, --gpus N > 1: one process drives N devices, the
+    device-resident leg launches every shard on its own device's stream, the
+    e2e leg is run_batch with EngineConfig(devices=range(N)) (the drop-in
+    path: one host thread per device inside libsdeb200).
+
+  value     device-resident inputs (sdb_run_device), CUDA events on the launch
+            stream around each launch, L2 flushed (512 MiB memset) between
+            timed steps outside the event pairs; max over GPUs per step.
+  e2e       the public API run_batch() with numpy host buffers: H2D of
+            init/params and D2H of the store inside every timed step.
+  cold_e2e  the first run_batch() call of a fresh process (its own subprocess,
+            empty layout cache): everything a one-shot CLI call pays.
+  roofline  FP64 pipe: "frac" = the kernel's own algorithmic FP64 lane-ops
+            (the O(n) meanfield form) / kernel time, against the
+            FP64 DFMA peak measured live (sdb_fp64_peak; MEASURED_PEAKS.json
+            has no FP64 figure); "w_em_frac" = the same time against SURVEY.md
+            8d's W_EM(n) = 9n(n-1) + 41n of the reference's O(n^2) algorithm.
+  cpu_baseline  the UNMODIFIED reference (sdebatch.run_batch from
+            baseline/_ref, its own bench.time_run protocol) on a bounded
+            sample, threads = 1 and threads = "all", best chunk_group of
+            {M_cpu, M_cpu/threads, 8192, 512} each; the oracle
+            port only if baseline/_ref is absent ("kind" says which).
+--impl reference times that reference alone (rank 0, all host threads).
 """
 
 from __future__ import annotations
 
 import argparse
+import gc
 import hashlib
 import json
 import os
+import platform
 import subprocess
 import sys
+import tempfile
 import threading
 import time
 
@@ -42,9 +64,15 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+REF_PATH = os.path.join(ROOT, "baseline", "_ref")
 
 WORKLOADS = {
-    # BASELINE.json configs[1] -- the headline
+    # BASELINE.json configs[2] -- the headline (the config stated at 1/2/4/8 GPUs)
+    "cfg3": dict(sizes=("cfg3_n32", "cfg3_n64", "cfg3_n128", "cfg3_n256"),
+                 headline="cfg3_n256", secondary=("cfg2",),
+                 desc="stochastic Kuramoto size sweep n=32..256, 2^20 orbits, Philox, "
+                      "E-M dt=1e-3, final state (headline: n=256)"),
+    # BASELINE.json configs[1]
     "cfg2": dict(n=16, orbits=65536, dt=1e-3, steps=10000, ksteps=10000, stream="sfc64",
                  solver="em", batch="kgrid",
                  desc="stochastic Kuramoto n=16, 65,536 orbits (256 K x 256 sigma grid), sfc64, "
@@ -93,6 +121,7 @@ WORKLOADS = {
                        desc="Ornstein-Uhlenbeck template model (drift p[0]*(p[1]-y[i]), "
                             "diffusion p[2+i]*n[i]), n=16, 65,536 orbits, 10 samples"),
 }
+DEFAULT_WORKLOAD = "cfg3"
 
 # expression-template workloads: (drift, diffusion, nparams(n))
 TEMPLATES = {
@@ -164,40 +193,56 @@ def pairwise_equivalent_ops(n: int) -> float:
 
 
 # ---------------------------------------------------------------------------
+# workload construction (shards: rows [lo, hi) of the workload, global ids)
 
-def make_batch(sdb, w, orbit_offset: int, seed: int = 20260809):
-    n, m = w["n"], w["orbits"]
-    local = np.arange(m)
-    if w["batch"] == "speed":
-        return sdb.sample_kuramoto_batch(n, m, (0.01, 0.03), (0.001, 0.003), 1.0, seed,
-                                         orbit_offset=orbit_offset)
-    if w["batch"] == "kgrid":
-        b = sdb.sample_kuramoto_batch(n, m, (0.2, 0.4), (0.01, 0.03), 0.0, seed,
-                                      orbit_offset=orbit_offset)
+SEED = 20260809
+
+
+def _shape_batch(make, w, lo, hi, sample):
+    """The workload's batch rows [lo, hi).  ``sample(count, omega, noise, K,
+    first)`` draws rows [first, first + count) of the counter-based Kuramoto
+    sampler (model.py:242-270; bit-exact on the device), ``make(init,
+    params)`` builds the OrbitBatch."""
+    n = w["n"]
+    rows = np.arange(lo, hi)
+    m = hi - lo
+    if w["batch"] == "speed":  # speed_protocol_batch (model.py:273-277)
+        b = sample(m, (0.01, 0.03), (0.001, 0.003), 1.0, lo)
+        return make(b.init, b.params)
+    if w["batch"] == "kgrid":  # SURVEY.md 8d cfg2: 256 K x 256 sigma
+        b = sample(m, (0.2, 0.4), (0.01, 0.03), 0.0, lo)
         params = b.params.copy()
-        params[:, 0] = np.linspace(0.0, 0.5, 256)[(local // 256) % 256]
-        params[:, n + 1:] = np.geomspace(1e-3, 1e-1, 256)[local % 256][:, None]
-        return sdb.OrbitBatch(init=b.init, params=params)
+        params[:, 0] = np.linspace(0.0, 0.5, 256)[(rows // 256) % 256]
+        params[:, n + 1:] = np.geomspace(1e-3, 1e-1, 256)[rows % 256][:, None]
+        return make(b.init, params)
     if w["batch"] == "kgrid_ode":  # cfg4: 512 K x 512 omega draws, zero diffusion
-        b = sdb.sample_kuramoto_batch(n, m, (0.2, 0.4), (0.0, 0.0), 0.0, seed,
-                                      orbit_offset=orbit_offset)
+        b = sample(m, (0.2, 0.4), (0.0, 0.0), 0.0, lo)
         params = b.params.copy()
-        params[:, 0] = np.linspace(0.0, 2.0, 512)[(local // 512) % 512]
-        return sdb.OrbitBatch(init=b.init, params=params)
-    if w["batch"] == "resample":  # cfg5: 512 sets x 256 realisations
-        sets = m // 256
-        b = sdb.sample_kuramoto_batch(n, sets, (0.2, 0.4), (0.01, 0.03), 0.0, seed,
-                                      orbit_offset=orbit_offset // 256)
+        params[:, 0] = np.linspace(0.0, 2.0, 512)[(rows // 512) % 512]
+        return make(b.init, params)
+    if w["batch"] == "resample":  # cfg5: 512 parameter sets x 256 realisations
+        s0, s1 = lo // 256, (hi - 1) // 256 + 1
+        b = sample(s1 - s0, (0.2, 0.4), (0.01, 0.03), 0.0, s0)
         params = b.params.copy()
-        params[:, 0] = np.linspace(0.05, 0.8, 16)[np.arange(sets) % 16]
-        return sdb.OrbitBatch(init=np.repeat(b.init, 256, axis=0),
-                              params=np.repeat(params, 256, axis=0))
+        params[:, 0] = np.linspace(0.05, 0.8, 16)[np.arange(s0, s1) % 16]
+        cut = slice(lo - s0 * 256, hi - s0 * 256)
+        return make(np.repeat(b.init, 256, axis=0)[cut], np.repeat(params, 256, axis=0)[cut])
     if w["batch"] == "uniform":  # generic template models: seeded uniform draws
-        g = np.random.default_rng(seed + orbit_offset)
+        g = np.random.default_rng(SEED)
         nparams = TEMPLATES[w["model"]][2](n)
-        return sdb.OrbitBatch(init=g.uniform(-1.0, 1.0, (m, n)),
-                              params=g.uniform(0.05, 0.5, (m, nparams)))
+        init = g.uniform(-1.0, 1.0, (w["orbits"], n))
+        params = g.uniform(0.05, 0.5, (w["orbits"], nparams))
+        return make(init[lo:hi], params[lo:hi])
     raise ValueError(w["batch"])
+
+
+def make_batch(sdb, w, lo: int = 0, hi: int | None = None):
+    """Rows [lo, hi) of workload w's batch (default: all), drawn on the GPU."""
+    hi = w["orbits"] if hi is None else hi
+
+    def sample(count, omega, noise, k, first):
+        return sdb.sample_kuramoto_batch(w["n"], count, omega, noise, k, SEED, orbit_offset=first)
+    return _shape_batch(lambda i, p: sdb.OrbitBatch(init=i, params=p), w, lo, hi, sample)
 
 
 def make_model(sdb, w):
@@ -212,7 +257,8 @@ def make_model(sdb, w):
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks / throttle reasons sampled during the timed regions
+    (start() / pause() around each; summary() over every sample taken)."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
@@ -227,26 +273,30 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), "--query-gpu=" + self.FIELDS,
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread = threading.Thread(target=self._read, args=(self.proc,), daemon=True)
             self.thread.start()
         except (OSError, FileNotFoundError):
             self.proc = None
 
-    def _read(self):
-        for line in self.proc.stdout:
+    def _read(self, proc):
+        for line in proc.stdout:
             self.lines.append(line.strip())
 
-    def stop(self):
+    def pause(self):
         if self.proc is None:
-            return None
+            return
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
         except subprocess.TimeoutExpired:
             self.proc.kill()
         self.thread.join(timeout=2)
+        self.proc = None
+
+    def summary(self):
+        self.pause()
         sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in self.lines:
@@ -267,14 +317,213 @@ class ClockSampler:
                 "samples": len(sm), "reasons": sorted(reasons)}
 
 
+# ---------------------------------------------------------------------------
+# CPU side: the unmodified reference (baseline/_ref) on a bounded sample
+
+def load_reference():
+    """``sdebatch`` installed unmodified into baseline/_ref, or
+    None when that install is absent (the oracle port is then timed)."""
+    if not os.path.isdir(os.path.join(REF_PATH, "sdebatch")):
+        return None
+    if REF_PATH not in sys.path:
+        sys.path.insert(0, REF_PATH)
+    import sdebatch
+    return sdebatch
+
+
+def cpu_model_name() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return platform.processor() or "unknown"
+
+
+def _ref_workload(ref, w, m_cpu):
+    """The reference's model and the workload's first m_cpu rows, built with
+    the reference's own constructors and sampler (model.py:204-277, 291-309)."""
+    n = w["n"]
+    if "model" in w:
+        drift, diffusion, nparams = TEMPLATES[w["model"]]
+        model = ref.model_from_dsl(w["model"], n, nparams(n), n, drift, diffusion)
+    elif w["solver"] == "rk4":
+        model = ref.ModelSpec(name="kuramoto-ode:%d" % n, nequat=n, nparams=2 * n + 1, nnoise=0,
+                              drift=ref.model._kuramoto_drift)
+    else:
+        model = ref.kuramoto_model(n)
+
+    def sample(count, omega, noise, k, first):
+        assert first == 0
+        return ref.sample_kuramoto_batch(n, count, omega, noise, k, SEED)
+    batch = _shape_batch(lambda i, p: ref.OrbitBatch(init=np.ascontiguousarray(i),
+                                                     params=np.ascontiguousarray(p)),
+                         w, 0, m_cpu, sample)
+    return model, batch
+
+
+def _ref_config(ref, w, m, steps, threads, group):
+    # the reference has one noise generator (Philox, rng.py); every other field
+    # is the workload's own
+    return ref.EngineConfig(dt=w["dt"], tspan=w["dt"] * steps, ksteps=steps, orbits=m,
+                            solver=w["solver"], chunk_group=group, seed=SEED, threads=threads,
+                            max_store_bytes=1 << 40)
+
+
+def reference_leg(ref, w, threads, run_seconds: float, repeats: int = 2, warmup: int = 1):
+    """One timed leg of the reference: probe the per-orbit-step cost, size a
+    sample of M_cpu orbits x S_cpu steps for ~run_seconds per run, pick the
+    best chunk_group of {M_cpu, M_cpu/threads, 8192, 512} on a one-step probe,
+    then the reference's own bench.time_run (warm-up + timed repeats with a
+    store-hash check, bench.py:72-105)."""
+    nthreads = (os.cpu_count() or 1) if threads == "all" else threads
+    n = w["n"]
+    # cost probe: min(M, 256) orbits x 1 step, one group per thread
+    m0 = min(w["orbits"], max(nthreads, 256))
+    model, batch = _ref_workload(ref, w, m0)
+    cfg = _ref_config(ref, w, m0, 1, threads, max(1, m0 // nthreads))
+    ref.run_batch(model, cfg, batch)
+    t0 = time.perf_counter()
+    ref.run_batch(model, cfg, batch)
+    per = (time.perf_counter() - t0) / m0  # seconds per orbit-step
+    # sample: as many orbits as the budget allows (<= the workload's, <= 2^16,
+    # the (G, n, n) drift temporaries <= ~4 GiB), then steps to fill the run
+    budget = run_seconds / per
+    m_cap = min(w["orbits"], 1 << 16, max(nthreads, int((4 << 30) / (8 * n * n))))
+    m_cpu = int(max(min(m0, m_cap), min(m_cap, budget / 2)))
+    m_cpu = max(nthreads, m_cpu - m_cpu % nthreads) if m_cpu >= nthreads else m_cpu
+    s_cpu = int(max(1, min(w["steps"], budget / m_cpu)))
+    model, batch = _ref_workload(ref, w, m_cpu)
+    groups = sorted({max(1, min(m_cpu, g)) for g in (m_cpu, m_cpu // nthreads, 8192, 512)})
+    probe = {}
+    for g in groups:
+        cfg = _ref_config(ref, w, m_cpu, 1, threads, g)
+        t0 = time.perf_counter()
+        ref.run_batch(model, cfg, batch)
+        probe[g] = time.perf_counter() - t0
+    group = min(probe, key=probe.get)
+    cfg = _ref_config(ref, w, m_cpu, s_cpu, threads, group)
+    for _ in range(max(0, warmup - 1)):
+        ref.run_batch(model, cfg, batch)
+    point = ref.bench.time_run(model, cfg, batch, repeats=repeats, warmup=warmup > 0)
+    return {"threads": threads, "threads_used": nthreads, "chunk_group": group,
+            "chunk_group_probe_s": {str(k): round(v, 4) for k, v in probe.items()},
+            "orbits": m_cpu, "steps": s_cpu, "runtimes_s": point.runtimes,
+            "value": m_cpu * s_cpu / point.mean, "point": point}
+
+
+def port_leg(w, threads, run_seconds: float, repeats: int = 2):
+    """Fallback when baseline/_ref is absent: the oracle port of run_batch
+    (numpy restatement, reference op order, same thread pool)."""
+    from oracle import sdeb_oracle as O
+    nthreads = (os.cpu_count() or 1) if threads == "all" else threads
+    n = w["n"]
+    m_cpu = min(w["orbits"], 8192 if n <= 32 else 1024)
+    init, params = O.sample_kuramoto_batch(n, m_cpu, (0.2, 0.4), (0.01, 0.03), 0.3, SEED)
+    nnoise = 0 if w["solver"] == "rk4" else n
+    group = max(1, m_cpu // nthreads)
+
+    def run(steps):
+        t0 = time.perf_counter()
+        O.integrate(init, params, dt=w["dt"], ksteps=steps, chunks=1, seed=1,
+                    solver=w["solver"], nnoise=nnoise, threads=nthreads, group=group)
+        return time.perf_counter() - t0
+    per = run(2) / 2
+    s_cpu = int(max(1, min(w["steps"], run_seconds / per)))
+    times = [run(s_cpu) for _ in range(repeats)]
+    return {"threads": threads, "threads_used": nthreads, "chunk_group": group,
+            "orbits": m_cpu, "steps": s_cpu, "runtimes_s": times,
+            "value": m_cpu * s_cpu / float(np.mean(times))}
+
+
+def cpu_baseline(w, run_seconds: float):
+    """threads=1 and threads="all" legs of the reference (BASELINE.md 3);
+    value = the better leg."""
+    ref = load_reference()
+    legs = []
+    for threads in (1, "all"):
+        leg = (reference_leg(ref, w, threads, run_seconds) if ref is not None
+               else port_leg(w, threads, run_seconds))
+        leg.pop("point", None)
+        legs.append(leg)
+    best = max(legs, key=lambda l: l["value"])
+    return {"value": best["value"], "unit": "orbit-steps/s", "cores": best["threads_used"],
+            "kind": "reference" if ref is not None else "port",
+            "sample": "%s %s, %d orbits x %d steps of %s, threads=%s, chunk_group=%d "
+                      "(best of the thread legs and chunk_group probes), %d host threads "
+                      "available (%s)"
+                      % ("unmodified sdebatch.run_batch (baseline/_ref) under its own "
+                         "bench.time_run" if ref is not None else "oracle port of run_batch",
+                         "(Philox: the reference's only generator)", best["orbits"],
+                         best["steps"], w["desc"].split(",")[0], best["threads"],
+                         best["chunk_group"], os.cpu_count() or 1, cpu_model_name()),
+            "legs": legs}
+
+
+def run_reference_arm(args, w, world, rank):
+    """--impl reference: the reference's own CPU path, all host threads, on
+    this arm's config and metric; rank 0 alone runs (the others exit)."""
+    if rank != 0:
+        return
+    ref = load_reference()
+    total = max(1, args.steps + args.warmup)
+    run_seconds = min(args.ref_seconds, max(0.3, 150.0 / total))
+    if ref is not None:
+        leg = reference_leg(ref, w, "all", run_seconds, repeats=args.steps, warmup=args.warmup)
+        point = leg.pop("point")
+        times = point.runtimes
+        kind = "reference"
+        how = ("unmodified sdebatch.run_batch from baseline/_ref through sdebatch.bench.time_run "
+               "(%d warm-up, %d timed repeats, store hash checked)" % (args.warmup, args.steps))
+    else:
+        leg = port_leg(w, "all", run_seconds, repeats=args.steps)
+        times = leg["runtimes_s"]
+        kind = "port"
+        how = "oracle port of run_batch (baseline/_ref absent)"
+    ms = 1e3 * float(np.mean(times))
+    value = leg["orbits"] * leg["steps"] / (ms * 1e-3)
+    line = {
+        "impl": "reference", "metric": "orbit-steps/s", "value": value, "unit": "orbit-steps/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (the reference's own sampler, speed/grid presets of the workload)",
+        "config": {"workload": args.workload, "headline": w.get("name"), "desc": w["desc"],
+                   "n": w["n"], "cpu_sample_orbits": leg["orbits"], "cpu_sample_steps": leg["steps"],
+                   "threads": "all", "chunk_group": leg["chunk_group"],
+                   "chunk_group_probe_s": leg.get("chunk_group_probe_s")},
+        "cpu_baseline": {"value": value, "unit": "orbit-steps/s", "cores": leg["threads_used"],
+                         "kind": kind,
+                         "sample": "%s; %d orbits x %d SDE steps per bench step, threads=all "
+                                   "(%d), chunk_group=%d, %s"
+                                   % (how, leg["orbits"], leg["steps"], leg["threads_used"],
+                                      leg["chunk_group"], cpu_model_name())},
+        "e2e": {"value": value, "unit": "orbit-steps/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# multi-GPU plumbing
+
 def dist_setup(want_gpus: int):
+    """torchrun (WORLD_SIZE > 1): one rank per GPU over NCCL; --gpus must
+    equal the world size.  Otherwise a single process (which drives --gpus
+    devices itself)."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     dist = None
     if world > 1:
+        if want_gpus not in (1, world):
+            raise SystemExit("--gpus %d but torchrun started %d ranks" % (want_gpus, world))
         import torch
         import torch.distributed as dist_mod
+        # this rank's device is the default context's too (batch sampling,
+        # per-step utilities): nothing lands on GPU 0 by accident
+        os.environ["SDEB200_DEVICES"] = str(local)
         torch.cuda.set_device(local)
         dist_mod.init_process_group("nccl", device_id=torch.device("cuda", local))
         dist = dist_mod
@@ -305,247 +554,333 @@ def barrier(dist):
         dist.barrier()
 
 
-# ---------------------------------------------------------------------------
-# CPU side: the oracle port (reference algorithm) on a bounded sample
-
-def cpu_sample_rate(w, seconds: float, threads: int, stream_override=None):
-    """orbit-steps/s of the oracle port (numpy restatement of the reference's
-    run_batch, engine.py:184-277) on M_cpu orbits x S_cpu steps of workload w."""
-    from oracle import sdeb_oracle as O
-    n = w["n"]
-    m_cpu = min(w["orbits"], 8192 if n <= 32 else 1024)
-    init, params = O.sample_kuramoto_batch(n, m_cpu, (0.2, 0.4), (0.01, 0.03), 0.3, 20260809)
-    if w["solver"] == "rk4":
-        params[:, n + 1:] = 0.0
-    stream = stream_override or w["stream"]
-    group = max(1, m_cpu // threads)
-    nnoise = 0 if w["solver"] == "rk4" else n
-    fns = {}
-    if "model" in w:  # the reference's interpreter, restated (oracle.expression_model)
-        drift_t, diffusion_t, nparams = TEMPLATES[w["model"]]
-        fns = dict(zip(("drift", "diffusion"), O.expression_model(drift_t, diffusion_t)))
-        g = np.random.default_rng(1)
-        params = g.uniform(0.05, 0.5, (m_cpu, nparams(n)))
-
-    def run(steps):
-        t0 = time.perf_counter()
-        O.integrate(init, params, dt=w["dt"], ksteps=steps, chunks=1, seed=1,
-                    solver=w["solver"], nnoise=nnoise, stream=stream, threads=threads, group=group,
-                    **fns)
-        return time.perf_counter() - t0
-
-    probe = 3
-    dt_probe = run(probe)
-    s_cpu = int(max(probe, min(100000, seconds / max(dt_probe / probe, 1e-9))))
-    return m_cpu, s_cpu, group, run
-
-
-def cpu_baseline(w, seconds: float):
-    threads = os.cpu_count() or 1
-    m_cpu, s_cpu, group, run = cpu_sample_rate(w, seconds, threads, "philox")
-    elapsed = run(s_cpu)
-    return {"value": m_cpu * s_cpu / elapsed, "unit": "orbit-steps/s", "cores": threads,
-            "kind": "port",
-            "sample": "oracle port of run_batch (numpy, reference op order, %s stream), "
-                      "%d orbits x %d steps of %s, ThreadPool(%d) over groups of %d, %.1f s"
-                      % ("philox (the reference's own generator)" if w["solver"] == "em" else "no", m_cpu, s_cpu,
-                         w["desc"].split(",")[0], threads, group, elapsed)}
-
-
-def run_reference_arm(args, w, world, rank):
-    if rank != 0:
-        return
-    threads = os.cpu_count() or 1
-    m_cpu, s_cpu, group, run = cpu_sample_rate(w, args.ref_seconds, threads, "philox")
-    for _ in range(args.warmup):
-        run(max(1, s_cpu // 10))
-    times = [run(s_cpu) for _ in range(args.steps)]
-    ms = 1e3 * float(np.mean(times))
-    value = m_cpu * s_cpu / (ms * 1e-3)
-    line = {
-        "impl": "reference", "metric": "orbit-steps/s", "value": value, "unit": "orbit-steps/s",
-        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (sampled batch, reference sampler)",
-        "config": {"workload": args.workload, "desc": w["desc"], "n": w["n"],
-                   "cpu_sample_orbits": m_cpu, "cpu_sample_steps": s_cpu},
-        "cpu_baseline": {"value": value, "unit": "orbit-steps/s", "cores": threads,
-                         "kind": "port",
-                         "sample": "%d orbits x %d SDE steps per bench step, oracle port of "
-                                   "run_batch (reference is pure Python: no compiled _ref), "
-                                   "ThreadPool(%d) over groups of %d" % (m_cpu, s_cpu, threads,
-                                                                         group)},
-        "e2e": {"value": value, "unit": "orbit-steps/s", "h2d_bytes_per_step": 0,
-                "d2h_bytes_per_step": 0},
-    }
-    print(json.dumps(line), flush=True)
+def plan_shards(orbits: int, world: int, rank: int, local: int, gpus: int, devices=None):
+    """[(device, lo, hi)] this process integrates: its torchrun shard, or one
+    shard per device when one process drives --gpus devices (``devices``
+    overrides the ids, e.g. 0,0,0,0 to exercise N shards on one GPU)."""
+    from paper_1908_03869_b200.engine import shard_bounds
+    if world > 1:
+        return [(local,) + shard_bounds(orbits, world, rank)]
+    devs = list(devices) if devices else list(range(gpus))
+    return [(d,) + shard_bounds(orbits, len(devs), g) for g, d in enumerate(devs)]
 
 
 # ---------------------------------------------------------------------------
+# GPU side
 
-def run_ours(args, w, world, rank, local, dist):
+def measure(args, name, w, shards, world, dist, clocks, e2e_steps, peak_ops):
+    """Device-resident and end-to-end orbit-steps/s of one workload over
+    ``shards`` (this process's (device, lo, hi) list)."""
     import torch
 
     import paper_1908_03869_b200 as sdb
     from paper_1908_03869_b200 import _native as nat
     from paper_1908_03869_b200.engine import make_desc
 
-    torch.cuda.set_device(local)
     if w.get("model") == "kuramoto_template":
         os.environ["SDEB200_NO_NATIVE_KURAMOTO"] = "1"  # the generated program, not the stepper
-    n, m, steps = w["n"], w["orbits"], w["steps"]
+    else:
+        os.environ.pop("SDEB200_NO_NATIVE_KURAMOTO", None)
+    n, m_total, steps = w["n"], w["orbits"], w["steps"]
     chunks = steps // w["ksteps"]
-    model = make_model(sdb, w)
-    offset = rank * m
-    batch = make_batch(sdb, w, offset)
-    cfg = sdb.EngineConfig(dt=w["dt"], tspan=w["dt"] * steps, ksteps=w["ksteps"], orbits=m,
-                           solver=w["solver"], seed=20260809, stream=w["stream"],
-                           coupling=args.coupling, devices=(local,),
-                           max_store_bytes=1 << 40)
-    assert sdb.iteration_count(cfg.tspan, cfg.dt, cfg.ksteps) == chunks
-    ctx = nat.context((local,))
-    lib = nat.lib()
-    desc = make_desc(model, cfg, chunks, m, orbit_offset=offset)
-
-    d_init = torch.from_numpy(np.ascontiguousarray(batch.init)).cuda()
-    d_params = torch.from_numpy(np.ascontiguousarray(batch.params)).cuda()
     coherence = bool(w.get("coherence"))
-    d_values = (torch.empty((m, 2, chunks + 1), dtype=torch.float64, device="cuda") if coherence
-                else torch.empty((m, chunks, n), dtype=torch.float64, device="cuda"))
-    d_fail = torch.empty(m, dtype=torch.int64, device="cuda")
-    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
-    stream = torch.cuda.current_stream()
-
+    model = make_model(sdb, w)
+    devices = tuple(d for d, _, _ in shards)
+    lib = nat.lib()
     program_handle = None
-    if desc.model == nat.SDB_MODEL_EXPRESSION:
+    if "model" in w:
         from paper_1908_03869_b200 import program
         program_handle = program.model_program(model).handle
 
-    def launch():
-        if coherence:
-            nat.check(lib.sdb_run_coherence_device(ctx, desc, d_init.data_ptr(),
-                                                   d_params.data_ptr(), d_values.data_ptr(),
-                                                   d_fail.data_ptr(), stream.cuda_stream),
-                      ctx, "sdb_run_coherence_device")
-            return
-        if program_handle is not None:
-            nat.check(lib.sdb_run_model_device(ctx, program_handle, desc, d_init.data_ptr(),
-                                               d_params.data_ptr(), d_values.data_ptr(),
-                                               d_fail.data_ptr(), stream.cuda_stream),
-                      ctx, "sdb_run_model_device")
-            return
-        nat.check(lib.sdb_run_device(ctx, desc, d_init.data_ptr(), d_params.data_ptr(),
-                                     d_values.data_ptr(), d_fail.data_ptr(), stream.cuda_stream),
-                  ctx, "sdb_run_device")
+    legs = []
+    for dev, lo, hi in shards:
+        torch.cuda.set_device(dev)
+        rows = hi - lo
+        batch = make_batch(sdb, w, lo, hi)
+        cfg = sdb.EngineConfig(dt=w["dt"], tspan=w["dt"] * steps, ksteps=w["ksteps"], orbits=rows,
+                               solver=w["solver"], seed=SEED, stream=w["stream"],
+                               coupling=args.coupling, devices=(dev,), max_store_bytes=1 << 40)
+        assert sdb.iteration_count(cfg.tspan, cfg.dt, cfg.ksteps) == chunks
+        leg = dict(dev=dev, lo=lo, hi=hi, rows=rows, batch=batch, ctx=nat.context((dev,)),
+                   desc=make_desc(model, cfg, chunks, rows, orbit_offset=lo),
+                   init=torch.from_numpy(np.ascontiguousarray(batch.init)).cuda(dev),
+                   params=torch.from_numpy(np.ascontiguousarray(batch.params)).cuda(dev),
+                   values=(torch.empty((rows, 2, chunks + 1), dtype=torch.float64, device=dev)
+                           if coherence else
+                           torch.empty((rows, chunks, n), dtype=torch.float64, device=dev)),
+                   fail=torch.empty(rows, dtype=torch.int64, device=dev),
+                   flush=torch.empty(512 << 20, dtype=torch.uint8, device=dev),
+                   stream=torch.cuda.current_stream(dev))
+        legs.append(leg)
 
+    def launch(leg):
+        torch.cuda.set_device(leg["dev"])
+        ctx, desc, st = leg["ctx"], leg["desc"], leg["stream"].cuda_stream
+        ptrs = (leg["init"].data_ptr(), leg["params"].data_ptr(), leg["values"].data_ptr(),
+                leg["fail"].data_ptr())
+        if coherence:
+            nat.check(lib.sdb_run_coherence_device(ctx, desc, *ptrs, st), ctx,
+                      "sdb_run_coherence_device")
+        elif program_handle is not None:
+            nat.check(lib.sdb_run_model_device(ctx, program_handle, desc, *ptrs, st), ctx,
+                      "sdb_run_model_device")
+        else:
+            nat.check(lib.sdb_run_device(ctx, desc, *ptrs, st), ctx, "sdb_run_device")
+
+    def sync_all():
+        for leg in legs:
+            torch.cuda.synchronize(leg["dev"])
+
+    # warm-up (the first call per shape also picks the lane layout)
     for _ in range(max(args.warmup, 3)):
-        launch()
-    torch.cuda.synchronize()
+        for leg in legs:
+            launch(leg)
+    sync_all()
     import ctypes
     lay = [ctypes.c_int32() for _ in range(5)]
-    lib.sdb_last_layout(ctx, *(ctypes.byref(v) for v in lay))
+    lib.sdb_last_layout(legs[0]["ctx"], *(ctypes.byref(v) for v in lay))
     lanes, persistent, ctas_per_sm, variant, _ = (int(v.value) for v in lay)
-    lane_width = int(lib.sdb_last_lane_width(ctx))
-    launches_per_step = int(lib.sdb_last_launch_count(ctx))
+    lane_width = int(lib.sdb_last_lane_width(legs[0]["ctx"]))
+    launches_per_step = sum(int(lib.sdb_last_launch_count(l["ctx"])) for l in legs)
 
-    clocks = ClockSampler(local)
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-          for _ in range(args.steps)]
+    for leg in legs:
+        torch.cuda.set_device(leg["dev"])
+        leg["ev"] = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                     for _ in range(args.steps)]
     barrier(dist)
-    torch.cuda.synchronize()
+    sync_all()
     clocks.start()
-    time.sleep(0.3)  # let the sampler attach before the first timed launch
+    time.sleep(0.15)  # let the sampler attach before the first timed launch
     for i in range(args.steps):
-        flush.zero_()
-        ev[i][0].record(stream)
-        launch()
-        ev[i][1].record(stream)
-    torch.cuda.synchronize()
+        for leg in legs:
+            torch.cuda.set_device(leg["dev"])
+            leg["flush"].zero_()
+            leg["ev"][i][0].record(leg["stream"])
+            launch(leg)
+            leg["ev"][i][1].record(leg["stream"])
+    sync_all()
+    clocks.pause()
     barrier(dist)
-    clock_info = clocks.stop()
-    kernel_ms = [a.elapsed_time(b) for a, b in ev]
-    total_ms = reduce_max(dist, float(sum(kernel_ms)))
-    ms_per_step = total_ms / args.steps
-    orbit_steps = float(m) * steps
-    value = world * orbit_steps / (ms_per_step * 1e-3)
-
-    # sanity: the timed runs produced finite final states
-    assert torch.isfinite(d_values).all().item(), "non-finite states in the benchmark run"
+    per_leg = [[a.elapsed_time(b) for a, b in leg["ev"]] for leg in legs]
+    kernel_ms = [max(col) for col in zip(*per_leg)]  # the step ends with its slowest GPU
+    ms_per_step = reduce_max(dist, float(sum(kernel_ms))) / args.steps
+    orbit_steps = float(m_total) * steps
+    value = orbit_steps / (ms_per_step * 1e-3)
+    for leg in legs:
+        assert torch.isfinite(leg["values"]).all().item(), "non-finite states in the bench run"
 
     # --- e2e through the public API (host numpy buffers) ---
-    host_batch = sdb.OrbitBatch(init=batch.init.copy(), params=batch.params.copy())
     api = sdb.run_coherence if coherence else sdb.run_batch
-    api(model, cfg, host_batch, orbit_offset=offset)  # warm (autotune cache, pinned staging)
+    if len(legs) == 1:
+        host = legs[0]["batch"]
+        lo0, rows_e2e = legs[0]["lo"], legs[0]["rows"]
+    else:  # one process, N devices: the whole batch through EngineConfig(devices=range(N))
+        host = sdb.OrbitBatch(init=np.concatenate([l["batch"].init for l in legs]),
+                              params=np.concatenate([l["batch"].params for l in legs]))
+        lo0, rows_e2e = legs[0]["lo"], legs[-1]["hi"] - legs[0]["lo"]
+    cfg_e2e = sdb.EngineConfig(dt=w["dt"], tspan=w["dt"] * steps, ksteps=w["ksteps"],
+                               orbits=rows_e2e, solver=w["solver"], seed=SEED, stream=w["stream"],
+                               coupling=args.coupling, devices=devices, max_store_bytes=1 << 40)
+    for leg in legs:  # the device-resident copies are not needed any more
+        for key in ("init", "params", "values", "fail", "flush"):
+            leg.pop(key)
+        leg.pop("batch")
+    gc.collect()
+    torch.cuda.empty_cache()
+    api(model, cfg_e2e, host, orbit_offset=lo0)  # warm: layout cache, pinned staging
     barrier(dist)
-    e2e_steps = max(1, min(args.steps, 5))
     per_call, hashes = [], []
     for _ in range(e2e_steps):
         t0 = time.perf_counter()
-        store = api(model, cfg, host_batch, orbit_offset=offset)
+        store = api(model, cfg_e2e, host, orbit_offset=lo0)
         per_call.append(time.perf_counter() - t0)
         # repeat-determinism check (the reference bench hashes every repeat,
         # bench.py:91-96) outside the per-call timing; the store is then
         # dropped, as a sweep that consumes each result would
         hashes.append(result_hash(sdb, store, coherence))
         del store
-    e2e_s = reduce_max(dist, float(sum(per_call))) / e2e_steps
-    h2d = batch.init.nbytes + batch.params.nbytes
-    d2h = (m * (chunks + 1) * 2 * 8 if coherence else m * chunks * n * 8) + m * 8
-    e2e = {"value": world * orbit_steps / e2e_s, "unit": "orbit-steps/s",
-           "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-           "ms_per_step": e2e_s * 1e3,
-           "median_ms": float(np.median(per_call)) * 1e3,
+    e2e_s = reduce_max_cpu(dist, float(np.mean(per_call)))
+    h2d = host.init.nbytes + host.params.nbytes
+    d2h = (rows_e2e * (chunks + 1) * 2 * 8 if coherence else rows_e2e * chunks * n * 8) + rows_e2e * 8
+    e2e = {"value": orbit_steps / e2e_s, "unit": "orbit-steps/s",
+           "h2d_bytes_per_step": int(h2d) * world, "d2h_bytes_per_step": int(d2h) * world,
+           "ms_per_step": e2e_s * 1e3, "median_ms": float(np.median(per_call)) * 1e3,
            "host_buffers": "pageable numpy (%s; large stores on recycled host mappings)"
                            % api.__name__,
-           "result_sha256": hashes[0][:16],
-           "repeats_identical": len(set(hashes)) == 1}
+           "result_sha256": hashes[0][:16], "repeats_identical": len(set(hashes)) == 1}
+    del host
+    gc.collect()
 
-    # --- roofline (FP64 pipe) ---
-    peak_ops = ctypes_peak(lib, ctx)
+    # --- roofline (FP64 pipe) of the stepper on the first device ---
     ops = (template_fp64_ops(n, w["model"], args.coupling) if "model" in w
            else algorithmic_fp64_ops(n, w["solver"], args.coupling))
-    achieved = ops * orbit_steps / (np.mean(kernel_ms) * 1e-3)
+    leg_ms = float(np.mean(per_leg[0]))
+    leg_orbit_steps = float(legs[0]["rows"]) * steps
+    achieved = ops * leg_orbit_steps / (leg_ms * 1e-3)
     roofline = {
         "bound": "fp64", "unit": "TFLOP/s",
         "achieved": 2 * achieved / 1e12, "peak": 2 * peak_ops / 1e12,
         "frac": achieved / peak_ops,
-        "traffic": measured_traffic(args.workload),
+        "frac_basis": "the kernel's own algorithmic FP64 lane-ops per orbit-step (%s form)"
+                      % ("generated template program" if "model" in w else args.coupling),
         "algorithmic_fp64_ops_per_orbit_step": ops,
+        "traffic": measured_traffic(name),
+        "traffic_basis": "ncu dram__bytes_read.sum + dram__bytes_write.sum per launch "
+                         "(profiles/traffic.json)",
+        "algorithmic_bytes_per_launch": algorithmic_bytes(w, legs[0]["rows"]),
+        "achieved_hbm_gbs": algorithmic_bytes(w, legs[0]["rows"]) / (leg_ms * 1e-3) / 1e9,
         "peak_source": "measured live: sdb_fp64_peak DFMA-throughput kernel (FLOP = 2 x DFMA)",
-        "pairwise_equivalent_frac": pairwise_equivalent_ops(n) * orbit_steps
-        / (np.mean(kernel_ms) * 1e-3) / peak_ops if w["solver"] == "em" else None,
+    }
+    if w["solver"] == "em" and "model" not in w:
+        roofline["w_em_ops_per_orbit_step"] = pairwise_equivalent_ops(n)
+        roofline["w_em_frac"] = (pairwise_equivalent_ops(n) * leg_orbit_steps
+                                 / (leg_ms * 1e-3) / peak_ops)
+        roofline["w_em_basis"] = ("SURVEY.md 8d W_EM(n) = 9n(n-1)+41n of the reference's "
+                                  "term-by-term algorithm against the same time; exceeds 1 for "
+                                  "the meanfield form, which does O(n) instead of O(n^2) work")
+    return {
+        "name": name, "value": value, "ms_per_step": ms_per_step, "kernel_ms": kernel_ms,
+        "e2e": e2e, "roofline": roofline, "launches_per_step": launches_per_step,
+        "layout": {"lanes_per_orbit": lanes, "oscillators_per_lane": lane_width,
+                   "persistent_grid": bool(persistent), "ctas_per_sm": ctas_per_sm,
+                   "register_capped": bool(variant)},
+        "orbits_per_gpu": [l["rows"] for l in legs],
     }
 
+
+def algorithmic_bytes(w, rows: int) -> float:
+    """HBM bytes one launch must move: init + params read once, the samples
+    1..k (or (r, Phi) planes) and the failure word written once."""
+    n, chunks = w["n"], w["steps"] // w["ksteps"]
+    nparams = TEMPLATES[w["model"]][2](n) if "model" in w else 2 * n + 1
+    out = 2 * (chunks + 1) if w.get("coherence") else chunks * n
+    return float(rows) * 8.0 * (n + nparams + out + 1)
+
+
+def cold_probe(args):
+    """--cold-probe: in a fresh process, the first run_batch call after the
+    batch exists (its sampling touched the device, so CUDA context creation
+    is outside), then a second call: prints both."""
+    import paper_1908_03869_b200 as sdb
+    w = WORKLOADS[args.workload]
+    model = make_model(sdb, w)
+    devices = tuple(range(args.gpus))
+    batch = make_batch(sdb, w)
+    cfg = sdb.EngineConfig(dt=w["dt"], tspan=w["dt"] * w["steps"], ksteps=w["ksteps"],
+                           orbits=w["orbits"], solver=w["solver"], seed=SEED, stream=w["stream"],
+                           coupling=args.coupling, devices=devices, max_store_bytes=1 << 40)
+    api = sdb.run_coherence if w.get("coherence") else sdb.run_batch
+    times = []
+    for _ in range(2):
+        t0 = time.perf_counter()
+        store = api(model, cfg, batch)
+        times.append(time.perf_counter() - t0)
+        del store
+        gc.collect()
+    print(json.dumps({"cold_s": times[0], "second_s": times[1]}), flush=True)
+
+
+def run_cold(args, name, w):
+    """cold_e2e of one workload: bench.py --cold-probe in a subprocess with an
+    empty on-disk layout cache (a fresh box)."""
+    with tempfile.TemporaryDirectory() as tmp:
+        env = dict(os.environ, SDEB200_TUNE_CACHE=os.path.join(tmp, "layouts.json"))
+        out = subprocess.run([sys.executable, os.path.abspath(__file__), "--cold-probe",
+                              "--workload", name, "--gpus", str(args.gpus), "--coupling",
+                              args.coupling], capture_output=True, text=True, env=env,
+                             timeout=900)
+    if out.returncode != 0:
+        return {"error": (out.stderr or out.stdout).strip().splitlines()[-1:]}
+    res = json.loads(out.stdout.strip().splitlines()[-1])
+    orbit_steps = float(w["orbits"]) * w["steps"]
+    return {"value": orbit_steps / res["cold_s"], "unit": "orbit-steps/s",
+            "ms": res["cold_s"] * 1e3, "second_call_ms": res["second_s"] * 1e3,
+            "how": "first run_batch() of a fresh process (empty layout cache; batch sampling "
+                   "and CUDA context creation before the timed call), host buffers"}
+
+
+def run_ours(args, world, rank, local, dist):
+    import torch
+
+    from paper_1908_03869_b200 import _native as nat
+
+    w_top = WORKLOADS[args.workload]
+    names = list(w_top.get("sizes", (args.workload,)))
+    headline = w_top.get("headline", args.workload)
+    secondary = list(w_top.get("secondary", ())) if not args.no_secondary else []
+    if world == 1:
+        have = nat.device_count()
+        if args.gpus > have:
+            raise SystemExit("--gpus %d but only %d CUDA device(s) are visible" % (args.gpus, have))
+        if args.devices and (max(args.devices) >= have or len(set(args.devices)) != args.gpus):
+            raise SystemExit("--devices %s does not name --gpus %d distinct visible devices"
+                             % (args.devices, args.gpus))
+    n_gpus = world if world > 1 else args.gpus
+    torch.cuda.set_device(local)
+    peak_ops = ctypes_peak(nat.lib(), nat.context((local,)))
+    clocks = ClockSampler(local)
+    results = {}
+    for name in names + secondary:
+        w = WORKLOADS[name]
+        shards = plan_shards(w["orbits"], world, rank, local, args.gpus, args.devices)
+        e2e_steps = max(1, min(args.steps, 5 if name in names else 3))
+        results[name] = measure(args, name, w, shards, world, dist, clocks, e2e_steps, peak_ops)
+        gc.collect()
+        torch.cuda.empty_cache()
+    clock_info = clocks.summary()
+    head = results[headline]
+    wh = WORKLOADS[headline]
+
+    cold = None
+    if rank == 0 and world == 1 and not args.no_cold:
+        cold = run_cold(args, headline, wh)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(w, args.cpu_seconds)
+        cpu = cpu_baseline(wh, args.cpu_seconds)
 
-    if rank == 0:
-        line = {
-            "metric": "orbit-steps/s", "value": value, "unit": "orbit-steps/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-            "higher_is_better": True, "scaling": "weak",
-            # only the paper-protocol workloads have a published number (SODECL on a
-            # P100, BASELINE.md section 2); cfg2 has none
-            "vs_baseline": (value / w["published"]) if w.get("published") else None,
-            "dtype": "f64",
-            "data": "synthetic (device-sampled Kuramoto batch, reference sampler bit-exact)",
-            "config": {"workload": args.workload, "desc": w["desc"], "n": n,
-                       "orbits_per_gpu": m, "sde_steps": steps, "ksteps": w["ksteps"],
-                       "solver": w["solver"], "stream": w["stream"], "coupling": args.coupling,
-                       "lanes_per_orbit": lanes, "oscillators_per_lane": lane_width,
-                       "persistent_grid": bool(persistent),
-                       "ctas_per_sm": ctas_per_sm, "register_capped": bool(variant),
-                       "template_model": w.get("model"),
-                       "parallelism": "orbit-shard x%d" % world,
-                       "l2": "flushed (512 MiB memset) between timed steps, outside the "
-                             "event pairs"},
-            "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu,
-            "gpu_launches": launches_per_step * args.steps,
-            "clocks": clock_info,
-            "kernel_ms": kernel_ms,
-        }
-        print(json.dumps(line), flush=True)
+    if rank != 0:
+        return
+
+    def brief(r):
+        out = {"value": r["value"], "ms_per_step": r["ms_per_step"], "e2e": r["e2e"]["value"],
+               "e2e_ms": r["e2e"]["ms_per_step"], "frac": r["roofline"]["frac"],
+               "w_em_frac": r["roofline"].get("w_em_frac"),
+               "traffic": r["roofline"]["traffic"],
+               "achieved_hbm_gbs": r["roofline"]["achieved_hbm_gbs"]}
+        out.update(r["layout"])
+        return out
+
+    line = {
+        "metric": "orbit-steps/s", "value": head["value"], "unit": "orbit-steps/s",
+        "n_gpus": n_gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": head["ms_per_step"], "higher_is_better": True, "scaling": "strong",
+        # only the paper-protocol workloads have a published number (SODECL on a
+        # P100, BASELINE.md section 2); cfg3 has none
+        "vs_baseline": (head["value"] / wh["published"]) if wh.get("published") else None,
+        "dtype": "f64",
+        "data": "synthetic (device-sampled Kuramoto batch, reference sampler bit-exact)",
+        "config": {"workload": args.workload, "headline": headline, "desc": w_top["desc"],
+                   "n": wh["n"], "orbits": wh["orbits"], "sde_steps": wh["steps"],
+                   "ksteps": wh["ksteps"], "solver": wh["solver"], "stream": wh["stream"],
+                   "coupling": args.coupling, "orbits_per_gpu": head["orbits_per_gpu"],
+                   "template_model": wh.get("model"),
+                   "parallelism": "contiguous orbit shards x%d (%s), no data-path collective"
+                                  % (len(head["orbits_per_gpu"]) * world,
+                                     "torchrun, one process per GPU" if world > 1
+                                     else "one process driving devices %s"
+                                     % (args.devices or list(range(args.gpus)))),
+                   "l2": "flushed (512 MiB memset) between timed steps, outside the event "
+                         "pairs; inputs also exceed L2 for cfg3",
+                   **head["layout"]},
+        "e2e": head["e2e"], "cold_e2e": cold, "roofline": head["roofline"],
+        "cpu_baseline": cpu,
+        "gpu_launches": head["launches_per_step"] * args.steps * world,
+        "clocks": clock_info,
+        "kernel_ms": head["kernel_ms"],
+        "sizes": {k: brief(results[k]) for k in names},
+        "secondary": {k: brief(results[k]) for k in secondary},
+    }
+    print(json.dumps(line), flush=True)
 
 
 def result_hash(sdb, store, coherence: bool) -> str:
@@ -574,22 +909,34 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="cfg2")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default=DEFAULT_WORKLOAD)
     ap.add_argument("--coupling", choices=["meanfield", "pairwise"], default="meanfield")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-seconds", type=float, default=10.0)
-    ap.add_argument("--ref-seconds", type=float, default=2.0)
+    ap.add_argument("--no-cold", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=4.0,
+                    help="seconds per timed reference run in the cpu_baseline legs")
+    ap.add_argument("--ref-seconds", type=float, default=8.0,
+                    help="cap on the seconds per step of --impl reference")
+    ap.add_argument("--devices", type=lambda t: [int(x) for x in t.split(",")], default=None,
+                    help="device id per in-process shard (default 0..gpus-1); repeats run "
+                         "several shards on one GPU (host-pipeline studies)")
+    ap.add_argument("--cold-probe", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
+    if args.gpus < 1:
+        raise SystemExit("--gpus must be >= 1")
+    if args.cold_probe:
+        cold_probe(args)
+        return
     w = WORKLOADS[args.workload]
-    world, rank, local, dist = (int(os.environ.get("WORLD_SIZE", "1")),
-                                int(os.environ.get("RANK", "0")),
-                                int(os.environ.get("LOCAL_RANK", "0")), None)
+    world, rank = int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0"))
     if args.impl == "reference":
-        run_reference_arm(args, w, world, rank)
+        head = w.get("headline", args.workload)
+        run_reference_arm(args, dict(WORKLOADS[head], name=head), world, rank)
         return
     world, rank, local, dist = dist_setup(args.gpus)
     try:
-        run_ours(args, w, world, rank, local, dist)
+        run_ours(args, world, rank, local, dist)
     finally:
         if dist is not None:
             dist.destroy_process_group()

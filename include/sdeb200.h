@@ -112,6 +112,12 @@ void sdb_last_layout(const sdb_ctx* ctx, int32_t* lanes, int32_t* persistent,
  * (meanfield);
  * SDEB200_LAYOUT's optional 5th field pins it ("1,1,0,0,5"). */
 int32_t sdb_last_lane_width(const sdb_ctx* ctx);
+/* Microseconds the last call spent choosing launch layouts (autotune probes;
+ * 0 when the layout came from the in-memory or on-disk cache, or was pinned).
+ * The probe is budgeted at ~10% of the predicted run; its decisions persist in
+ * SDEB200_TUNE_CACHE (default ~/.cache/sdeb200/layouts-v2.tsv; "" disables),
+ * keyed by GPU, driver, build and launch shape. */
+int64_t sdb_last_tune_us(const sdb_ctx* ctx);
 
 /* ---- noise streams (rng.py) ------------------------------------------------ */
 

@@ -58,6 +58,7 @@ SIGNATURES = {
     "sdb_last_launch_count": (ctypes.c_int64, [ctypes.c_void_p]),
     "sdb_last_lanes": (ctypes.c_int32, [ctypes.c_void_p]),
     "sdb_last_lane_width": (ctypes.c_int32, [ctypes.c_void_p]),
+    "sdb_last_tune_us": (ctypes.c_int64, [ctypes.c_void_p]),
     "sdb_last_layout": (None, [ctypes.c_void_p] + [ctypes.POINTER(ctypes.c_int32)] * 5),
     "sdb_philox_words": (ctypes.c_int, [ctypes.c_void_p, _c_u32_p, ctypes.c_int64, _c_u32_p]),
     "sdb_run_to_file": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(SdbDesc),

@@ -6,6 +6,7 @@
 // fused kernel of sdeb_kuramoto.cuh.
 #include <cuda_runtime.h>
 #include <fcntl.h>
+#include <sys/stat.h>
 #include <sys/mman.h>
 #if defined(__SSE2__)
 #include <emmintrin.h>
@@ -121,6 +122,7 @@ struct Slot {
     int32_t tight = 0;
     int32_t lane_width = 0;  // oscillators per lane (J) of the last launch
     int32_t tiles = 0;  // orbit tiles of the last host-buffer run
+    int64_t tune_us = 0;  // autotune probe time of the current call
     // end of the last launch that used this slot's scratch (state, rng, work),
     // and the stream it ran on: a launch on another stream waits for it first
     cudaEvent_t done = nullptr;
@@ -154,6 +156,7 @@ struct sdb_ctx {
     int32_t last_tight = 0;
     int32_t last_lane_width = 0;
     int32_t last_tiles = 0;
+    int64_t last_tune_us = 0;
     std::map<TuneKey, Layout> tune;
     std::mutex mu;  // guards tune and error: shard threads of one run share the context
     // Serialises the public entry points on one context: its slots' device
@@ -511,6 +514,247 @@ bool trace_enabled() {
     return on;
 }
 
+double now_ms();
+
+// ---- layout selection ------------------------------------------------------
+//
+// Every layout gives bit-identical results (canonical summation tree, exact
+// slab hand-off), so choosing one only affects speed.  The choice costs at
+// most ~10% of the run it is made for, and is remembered on disk:
+//   1. in-memory cache per context, then the on-disk cache (SDEB200_TUNE_CACHE,
+//      default ~/.cache/sdeb200/layouts-v2.tsv) keyed by GPU, driver, build
+//      and shape;
+//   2. otherwise the candidates are ordered by a cost model (prior_cost) and
+//      probed on ONE resident wave of orbits (every SM full, so the per-wave
+//      step time is the steady state of a long run) for a differential pair
+//      of step counts; the full-run time of each candidate is then predicted
+//      from its wave count (ragged last wave for one CTA per group, the
+//      fractional count for the persistent grid).  Probe step counts are
+//      sized so the whole probe stays within ~10% of the predicted run; when
+//      that budget is too small to resolve a candidate, the prior order
+//      decides the rest.
+
+// Cost-model ordering of the candidates (smaller is better): FP64 work per
+// thread-step of a lane (J oscillators incl. padding, log2(L) butterfly levels
+// of the two coupling sums), at the SM throughput the resident warps can
+// sustain (latency hiding saturates at ~12 warps/SM), times the wave count
+// of the launch mode.  Only an ordering for the probe and a fallback.
+double prior_cost(const sdb_desc& d, const Layout& l, int J, int sms) {
+    const int L = l.lanes;
+    const double lane_work = double(J) * 40.0 + 6.0 * ilog2(L) + 12.0;
+    const double warps = double(l.ctas_per_sm) * sdeb::kBlock / 32.0;
+    const double eff = std::min(1.0, warps / 12.0);
+    const double per_wave = double(sms) * l.ctas_per_sm;
+    const double ctas = double(cta_groups(d, L));
+    const double waves = l.persistent ? std::max(1.0, ctas / per_wave) : std::ceil(ctas / per_wave);
+    // a wave's duration is one CTA's: lane_work per step per thread over the
+    // SM's share of the pipe (per_wave CTAs run side by side)
+    return waves * lane_work * double(l.ctas_per_sm) / eff;
+}
+
+std::string disk_cache_path() {
+    const char* e = std::getenv("SDEB200_TUNE_CACHE");
+    if (e) return (*e == '\0' || std::strcmp(e, "0") == 0) ? std::string() : std::string(e);
+    const char* xdg = std::getenv("XDG_CACHE_HOME");
+    const char* home = std::getenv("HOME");
+    std::string base = (xdg && *xdg) ? std::string(xdg) : (home && *home ? std::string(home) + "/.cache" : "");
+    return base.empty() ? std::string() : base + "/sdeb200/layouts-v2.tsv";
+}
+
+// Key of one tuning decision: the device and software it was measured on
+// (name, SM count, driver, this build) and the launch shape.
+std::string disk_key(int device, const sdb_desc& d, int kind_solver, int kind_stream) {
+    cudaDeviceProp prop{};
+    cudaGetDeviceProperties(&prop, device);
+    int driver = 0;
+    cudaDriverGetVersion(&driver);
+    const int64_t total = d.chunks * d.ksteps;
+    char buf[512];
+    std::snprintf(buf, sizeof(buf), "%s|sm%d|cc%d.%d|drv%d|abi%d|%s %s|n%d|s%d|r%d|c%d|L%d|M%lld|T%lld",
+                  prop.name, prop.multiProcessorCount, prop.major, prop.minor, driver,
+                  SDB_ABI_VERSION, __DATE__, __TIME__, d.nequat, kind_solver, kind_stream,
+                  d.coupling, d.lanes, (long long)d.orbits,
+                  (long long)std::min<int64_t>(total, int64_t(1) << 20));
+    std::string k(buf);
+    for (char& c : k)
+        if (c == '\t' || c == '\n') c = ' ';
+    return k;
+}
+
+std::mutex g_disk_mu;
+bool g_disk_loaded = false;
+std::map<std::string, Layout> g_disk;
+
+void disk_load_locked() {
+    if (g_disk_loaded) return;
+    g_disk_loaded = true;
+    const std::string path = disk_cache_path();
+    if (path.empty()) return;
+    FILE* f = std::fopen(path.c_str(), "r");
+    if (!f) return;
+    char line[1024];
+    while (std::fgets(line, sizeof(line), f)) {
+        char* tab = std::strchr(line, '\t');
+        if (!tab) continue;
+        *tab = '\0';
+        Layout l;
+        if (std::sscanf(tab + 1, "%d,%d,%d,%d,%d,%d", &l.lanes, &l.persistent, &l.smem,
+                        &l.ctas_per_sm, &l.tight, &l.J) == 6 && l.lanes > 0)
+            g_disk[line] = l;  // later lines win
+    }
+    std::fclose(f);
+}
+
+bool disk_lookup(const std::string& key, Layout* out) {
+    std::lock_guard<std::mutex> lock(g_disk_mu);
+    disk_load_locked();
+    auto it = g_disk.find(key);
+    if (it == g_disk.end()) return false;
+    *out = it->second;
+    return true;
+}
+
+void disk_store(const std::string& key, const Layout& l) {
+    std::lock_guard<std::mutex> lock(g_disk_mu);
+    disk_load_locked();
+    g_disk[key] = l;
+    const std::string path = disk_cache_path();
+    if (path.empty()) return;
+    const size_t slash = path.rfind('/');
+    if (slash != std::string::npos && slash > 0) {  // mkdir -p of the parent
+        for (size_t i = 1; i <= slash; ++i)
+            if (path[i] == '/' || i == slash) ::mkdir(path.substr(0, i == slash ? slash : i).c_str(), 0755);
+    }
+    char row[1200];
+    const int len = std::snprintf(row, sizeof(row), "%s\t%d,%d,%d,%d,%d,%d\n", key.c_str(),
+                                  l.lanes, l.persistent, l.smem, l.ctas_per_sm, l.tight, l.J);
+    const int fd = ::open(path.c_str(), O_WRONLY | O_CREAT | O_APPEND | O_CLOEXEC, 0644);
+    if (fd < 0) return;  // a read-only home only costs the next process a probe
+    if (len > 0 && len < int(sizeof(row))) {
+        ssize_t w = ::write(fd, row, size_t(len));
+        (void)w;
+    }
+    ::close(fd);
+}
+
+// Probe the candidates (see the section comment) and return the best.
+sdb_status probe_layouts(sdb_ctx* ctx, Slot& s, const sdb_desc& d, int kind_solver,
+                         int kind_stream, const double* d_init, const double* d_params,
+                         cudaStream_t st, std::vector<Layout>& cands, Layout* best_out) {
+    int sms = 148;
+    SDB_CUDA(ctx, cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s.device));
+    const int64_t total = d.chunks * d.ksteps;
+    std::stable_sort(cands.begin(), cands.end(), [&](const Layout& a, const Layout& b) {
+        return prior_cost(d, a, layout_J(d, a), sms) < prior_cost(d, b, layout_J(d, b), sms);
+    });
+    // one resident wave of the largest-occupancy candidate bounds the scratch
+    int64_t wave_rows_max = 1;
+    for (const Layout& l : cands)
+        wave_rows_max = std::max<int64_t>(
+            wave_rows_max, int64_t(sms) * l.ctas_per_sm * (sdeb::kBlock / l.lanes));
+    const int64_t rows_cap = std::min<int64_t>(d.orbits, wave_rows_max);
+    SDB_CUDA(ctx, s.t_values.ensure(size_t(rows_cap) * d.nequat * sizeof(double)));
+    SDB_CUDA(ctx, s.t_state.ensure(size_t(rows_cap) * d.nequat * sizeof(double)));
+    SDB_CUDA(ctx, s.t_fail.ensure(size_t(rows_cap) * sizeof(int64_t)));
+    SDB_CUDA(ctx, s.t_rng.ensure(std::max<size_t>(rng_words(d, rows_cap), 4) * sizeof(uint64_t)));
+    cudaEvent_t e0, e1;
+    SDB_CUDA(ctx, cudaEventCreate(&e0));
+    SDB_CUDA(ctx, cudaEventCreate(&e1));
+    // one launch of `steps` steps over the candidate's wave: ms (best of 2)
+    auto timed = [&](const Layout& lay, int64_t rows, int64_t steps, float* ms_out) -> sdb_status {
+        sdb_desc pd = d;
+        pd.orbits = rows;
+        sdeb::RunArgs a = make_args(pd, lay.lanes);
+        a.state_in = d_init;
+        a.params = d_params;
+        a.state_out = nullptr;
+        a.values = s.t_values.as<double>();
+        a.vstride = 1;
+        a.fail_step = s.t_fail.as<int64_t>();
+        a.rng_state = nullptr;
+        a.ksteps = steps;
+        a.chunk_end = 1;
+        a.smem_pad = lay.smem;
+        a.groups = cta_groups(pd, lay.lanes);
+        a.persistent = 0;  // one wave: every CTA-group resident at once
+        const int J = layout_J(d, lay);
+        float best = 1e30f;
+        for (int rep = 0; rep < 2; ++rep) {
+            cudaEventRecord(e0, st);
+            cudaError_t e = launch_run(a, J, kind_solver, kind_stream, d.coupling,
+                                       kernel_variant(d, lay.lanes, J, lay.tight), st);
+            cudaEventRecord(e1, st);
+            if (e == cudaSuccess) e = cudaEventSynchronize(e1);
+            if (e != cudaSuccess) return cuda_fail(ctx, e, "autotune launch");
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, e0, e1);
+            best = std::min(best, ms);
+            s.launches += 1;
+        }
+        *ms_out = best;
+        return SDB_OK;
+    };
+    // predicted full-run ms of a layout from its per-wave step time
+    auto predict = [&](const Layout& l, double wave_step_ms, int64_t rows) {
+        if (rows >= d.orbits) return wave_step_ms * double(total);  // the probe was the run
+        const double per_wave = double(sms) * l.ctas_per_sm;
+        const double ctas = double(cta_groups(d, l.lanes));
+        // one CTA per group: the ragged last wave costs a whole one; the
+        // persistent grid balances to the fractional count (+1%: slab hand-offs)
+        const double waves = l.persistent ? 1.01 * ctas / per_wave : std::ceil(ctas / per_wave);
+        return wave_step_ms * double(total) * std::max(1.0, waves);
+    };
+    sdb_status rc = SDB_OK;
+    double spent_ms = 0.0, budget_ms = -1.0;
+    int64_t p1 = 32;  // first probe: the cost model's favourite, 32 + 64 steps
+    double best_pred = 1e300;
+    Layout best = cands[0];
+    for (size_t ci = 0; ci < cands.size() && rc == SDB_OK; ++ci) {
+        const Layout& lay = cands[ci];
+        const int64_t rows =
+            std::min<int64_t>(d.orbits, int64_t(sms) * lay.ctas_per_sm * (sdeb::kBlock / lay.lanes));
+        float t1 = 0.f, t2 = 0.f;
+        rc = timed(lay, rows, p1, &t1);
+        if (rc != SDB_OK) break;
+        rc = timed(lay, rows, 2 * p1, &t2);
+        if (rc != SDB_OK) break;
+        spent_ms += 2.0 * (t1 + t2);
+        const double step_ms = std::max(1e-9, double(t2 - t1) / double(p1));
+        const double pred = predict(lay, step_ms, rows);
+        if (trace_enabled())
+            std::fprintf(stderr, "[sdeb200] tune n=%d L=%d J=%d pers=%d ctas=%d tight=%d: "
+                                 "%.5f ms/step/wave (%lld rows, %lld steps) -> %.3f ms predicted\n",
+                         d.nequat, lay.lanes, layout_J(d, lay), lay.persistent, lay.ctas_per_sm,
+                         lay.tight, step_ms, (long long)rows, (long long)p1, pred);
+        if (pred < best_pred) {
+            best_pred = pred;
+            best = lay;
+        }
+        if (budget_ms < 0.0) {
+            // 10% of the predicted run for the whole probe; the remaining
+            // candidates share what is left (3 p steps each, 2 repetitions)
+            budget_ms = 0.1 * pred;
+            const double left = budget_ms - spent_ms;
+            const double per_cand = left / double(std::max<size_t>(1, cands.size() - 1));
+            const double per_step = double(t2) / double(2 * p1);  // launch overhead included
+            const int64_t p = int64_t(per_cand / (6.0 * std::max(1e-6, per_step)));
+            if (p < 16) {
+                // too short a run to resolve more layouts: keep the cost-model
+                // order, probing as many of the next ones as the budget allows
+                p1 = 16;
+            } else {
+                p1 = std::min<int64_t>(p, 2048);
+            }
+        }
+        if (ci + 1 < cands.size() && spent_ms >= budget_ms) break;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (rc != SDB_OK) return rc;
+    *best_out = best;
+    return SDB_OK;
+}
+
 // Pick the launch layout: cached, pinned (SDEB200_LAYOUT), single candidate,
 // or timed on a short probe into scratch buffers.  Every layout gives
 // bit-identical results (canonical summation tree, exact slab hand-off), so
@@ -559,129 +803,33 @@ sdb_status choose_layout(sdb_ctx* ctx, Slot& s, const sdb_desc& d, const double*
     sdb_status rc = candidate_layouts(ctx, s, d, kind_solver, kind_stream, &cands);
     if (rc != SDB_OK) return rc;
     if (cands.empty()) return fail_with(ctx, SDB_ERR_CUDA, "no launchable layout for n=%d", d.nequat);
-    if (cands.size() == 1) {
-        *out = cands[0];
-        {
-            std::lock_guard<std::mutex> lock(ctx->mu);
-            ctx->tune[key] = cands[0];
+    const std::string dkey = disk_key(s.device, d, kind_solver, kind_stream);
+    Layout lay_disk;
+    if (disk_lookup(dkey, &lay_disk)) {
+        for (const Layout& c : cands) {  // only a layout this build can still launch
+            if (c.lanes == lay_disk.lanes && c.persistent == lay_disk.persistent &&
+                c.smem == lay_disk.smem && c.ctas_per_sm == lay_disk.ctas_per_sm &&
+                c.tight == lay_disk.tight && c.J == lay_disk.J) {
+                std::lock_guard<std::mutex> lock(ctx->mu);
+                ctx->tune[key] = c;
+                *out = c;
+                return SDB_OK;
+            }
         }
-        return SDB_OK;
     }
-    // Differential probe: time P1 and P2 = 2*P1 steps and rank layouts by
-    // t(P2) - t(P1), the steady-state cost of P1 more steps.  Launch and
-    // end-of-run costs cancel; a one-CTA-per-group layout keeps its wave
-    // quantisation (every wave gets longer), a persistent grid does not
-    // (its drain tail cancels), so both are compared as they scale.
-    const int64_t p1 = std::min<int64_t>(total, std::max<int64_t>(64, std::min<int64_t>(256, total / 40)));
-    const int64_t p2 = std::min<int64_t>(total, 2 * p1);
-    SDB_CUDA(ctx, s.t_values.ensure(size_t(d.orbits) * d.nequat * sizeof(double)));
-    SDB_CUDA(ctx, s.t_state.ensure(size_t(d.orbits) * d.nequat * sizeof(double)));
-    SDB_CUDA(ctx, s.t_fail.ensure(size_t(d.orbits) * sizeof(int64_t)));
-    SDB_CUDA(ctx, s.t_rng.ensure(std::max<size_t>(rng_words(d, d.orbits), 4) * sizeof(uint64_t)));
-    cudaEvent_t e0, e1;
-    SDB_CUDA(ctx, cudaEventCreate(&e0));
-    SDB_CUDA(ctx, cudaEventCreate(&e1));
-    float best = 1e30f;
     Layout best_l = cands[0];
-    // reps launches of `steps` steps, best time; real_slabs: persistent slabs
-    // sized as a real run of that length would size them
-    auto timed = [&](const Layout& lay, int64_t steps, float* ms_out, int reps = 2,
-                     bool real_slabs = false) -> sdb_status {
-        sdeb::RunArgs a = make_args(d, lay.lanes);
-        a.state_in = d_init;
-        a.params = d_params;
-        a.state_out = s.t_state.as<double>();
-        a.values = s.t_values.as<double>();
-        a.vstride = 1;
-        a.fail_step = s.t_fail.as<int64_t>();
-        a.rng_state = s.t_rng.as<uint64_t>();
-        a.ksteps = steps;
-        a.chunk_end = 1;
-        float ms_best = 1e30f;
-        for (int rep = 0; rep < reps; ++rep) {
-            // real_slabs: persistent slabs sized for the whole run, as it will run
-            sdb_status r2 = configure_layout(ctx, s, s.t_work, d, lay, real_slabs ? total : steps,
-                                             st, &a);
-            if (r2 != SDB_OK) return r2;
-            if (a.persistent && !real_slabs) a.slab_steps = std::max<int64_t>(16, p1 / 2);
-            cudaEventRecord(e0, st);
-            const int J = layout_J(d, lay);
-            cudaError_t e = launch_run(a, J, kind_solver, kind_stream, d.coupling,
-                                       kernel_variant(d, lay.lanes, J, lay.tight), st);
-            cudaEventRecord(e1, st);
-            if (e == cudaSuccess) e = cudaEventSynchronize(e1);
-            if (e != cudaSuccess) return cuda_fail(ctx, e, "autotune launch");
-            float ms = 0.f;
-            cudaEventElapsedTime(&ms, e0, e1);
-            ms_best = std::min(ms_best, ms);
-            s.launches += 1;
-        }
-        *ms_out = ms_best;
-        return SDB_OK;
-    };
-    // stage 1: every candidate on the short differential probe
-    std::vector<std::pair<float, size_t>> scores;
-    for (size_t ci = 0; ci < cands.size(); ++ci) {
-        const Layout& lay = cands[ci];
-        float t1 = 0.f, t2 = 0.f;
-        rc = timed(lay, p1, &t1);
-        if (rc != SDB_OK) break;
-        float score = t1;
-        if (p2 > p1) {
-            rc = timed(lay, p2, &t2);
-            if (rc != SDB_OK) break;
-            score = t2 - t1;
-        }
-        scores.emplace_back(score, ci);
-        if (trace_enabled())
-            std::fprintf(stderr, "[sdeb200] tune n=%d L=%d J=%d pers=%d ctas=%d tight=%d: %.4f ms/%lld steps\n",
-                         d.nequat, lay.lanes, layout_J(d, lay), lay.persistent, lay.ctas_per_sm, lay.tight, score,
-                         (long long)(p2 - p1 > 0 ? p2 - p1 : p1));
-        if (score < best) {
-            best = score;
-            best_l = lay;
-        }
+    if (cands.size() > 1) {
+        const double t0 = now_ms();
+        rc = probe_layouts(ctx, s, d, kind_solver, kind_stream, d_init, d_params, st, cands,
+                           &best_l);
+        s.tune_us += int64_t(1e3 * (now_ms() - t0));
+        if (rc != SDB_OK) return rc;
     }
-    // stage 2: the four best re-timed on a long probe (>= 1/8 of the run and
-    // >= 4 of the run's persistent slabs, persistent slabs sized as in the real
-    // run, best of 5): the short probe cannot resolve layouts a few percent
-    // apart, and with short slabs it over-charges the persistent hand-offs
-    std::sort(scores.begin(), scores.end());
-    int64_t longest_slab = 0;  // the probe must span several real slabs
-    for (size_t r = 0; r < scores.size() && r < 4; ++r) {
-        const Layout& l = cands[scores[r].second];
-        if (!l.persistent) continue;
-        int sms = 148;
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s.device);
-        longest_slab = std::max(longest_slab, slab_steps_for(total, cta_groups(d, l.lanes),
-                                                             int64_t(sms) * l.ctas_per_sm));
-    }
-    const int64_t p3 = std::min<int64_t>(
-        total, std::max<int64_t>({p2, total / 8, std::min<int64_t>(4 * longest_slab, 8192)}));
-    if (rc == SDB_OK && p3 > p2 && scores.size() > 1) {
-        float best3 = 1e30f;
-        for (size_t r = 0; r < scores.size() && r < 4; ++r) {
-            float t3 = 0.f;
-            rc = timed(cands[scores[r].second], p3, &t3, 5, true);
-            if (rc != SDB_OK) break;
-            if (trace_enabled()) {
-                const Layout& l = cands[scores[r].second];
-                std::fprintf(stderr, "[sdeb200] tune stage 2 L=%d J=%d pers=%d ctas=%d tight=%d: %.4f ms/%lld steps\n",
-                             l.lanes, layout_J(d, l), l.persistent, l.ctas_per_sm, l.tight, t3, (long long)p3);
-            }
-            if (t3 < best3) {
-                best3 = t3;
-                best_l = cands[scores[r].second];
-            }
-        }
-    }
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
-    if (rc != SDB_OK) return rc;
     {
         std::lock_guard<std::mutex> lock(ctx->mu);
         ctx->tune[key] = best_l;
     }
+    disk_store(dkey, best_l);
     *out = best_l;
     return SDB_OK;
 }
@@ -774,18 +922,23 @@ sdb_status launch_device_ordered(sdb_ctx* ctx, Slot& s, const sdb_desc& d, sdb_m
     Layout lay;
     sdb_status rc = choose_layout(ctx, s, d, d_init, d_params, st, &lay);
     if (rc != SDB_OK) return rc;
-    SDB_CUDA(ctx, s.state.ensure(size_t(d.orbits) * d.nequat * sizeof(double)));
-    const size_t rw = rng_words(d, d.orbits);
-    if (rw) SDB_CUDA(ctx, s.rng.ensure(rw * sizeof(uint64_t)));
+    if (lay.persistent) {
+        SDB_CUDA(ctx, s.state.ensure(size_t(d.orbits) * d.nequat * sizeof(double)));
+        const size_t rw = rng_words(d, d.orbits);
+        if (rw) SDB_CUDA(ctx, s.rng.ensure(rw * sizeof(uint64_t)));
+    }
     int kind_solver, kind_stream;
     kernel_kind(d, &kind_solver, &kind_stream);
     sdeb::RunArgs a = make_args(d, lay.lanes);
     a.state_in = d_init;
     a.params = d_params;
-    a.state_out = s.state.as<double>();
+    // continuation state and stream states are only read back by the next
+    // slab of a persistent grid: a one-pass launch writes neither (2 GB of
+    // HBM writes at cfg3 n=256)
+    a.state_out = lay.persistent ? s.state.as<double>() : nullptr;
     a.values = d_values;
     a.fail_step = d_fail;
-    a.rng_state = s.rng.as<uint64_t>();
+    a.rng_state = lay.persistent ? s.rng.as<uint64_t>() : nullptr;
     rc = configure_layout(ctx, s, s.work, d, lay, d.chunks * d.ksteps, st, &a);
     if (rc != SDB_OK) return rc;
     const int J = layout_J(d, lay);
@@ -1330,6 +1483,7 @@ sdb_status run_host(sdb_ctx* ctx, const sdb_desc& d, sdb_model* m, const double*
     std::vector<std::thread> threads;
     for (Slot& s : ctx->slots) {
         s.launches = 0;
+        s.tune_us = 0;
         s.error.clear();
     }
     // contiguous shards [g*M/G, (g+1)*M/G)
@@ -1345,7 +1499,11 @@ sdb_status run_host(sdb_ctx* ctx, const sdb_desc& d, sdb_model* m, const double*
         for (auto& t : threads) t.join();
     }
     ctx->launches = 0;
-    for (int64_t g = 0; g < used; ++g) ctx->launches += ctx->slots[g].launches;
+    ctx->last_tune_us = 0;
+    for (int64_t g = 0; g < used; ++g) {
+        ctx->launches += ctx->slots[g].launches;
+        ctx->last_tune_us = std::max(ctx->last_tune_us, ctx->slots[g].tune_us);
+    }
     ctx->last_lanes = ctx->slots[0].lanes;
     ctx->last_persistent = ctx->slots[0].persistent;
     ctx->last_ctas_per_sm = ctx->slots[0].ctas_per_sm;
@@ -1372,9 +1530,11 @@ sdb_status run_dev(sdb_ctx* ctx, const sdb_desc& d, sdb_model* m, const double* 
     Slot& s = ctx->slots[0];
     SDB_CUDA(ctx, cudaSetDevice(s.device));
     s.launches = 0;
+    s.tune_us = 0;
     sdb_status rc = launch_device(ctx, s, d, m, d_init, d_params, d_values, d_fail_step,
                                   static_cast<cudaStream_t>(stream), out_mode);
     ctx->launches = s.launches;
+    ctx->last_tune_us = s.tune_us;
     ctx->last_lanes = s.lanes;
     ctx->last_persistent = s.persistent;
     ctx->last_ctas_per_sm = s.ctas_per_sm;
@@ -1503,6 +1663,8 @@ int64_t sdb_last_launch_count(const sdb_ctx* ctx) { return ctx ? ctx->launches :
 int32_t sdb_last_lanes(const sdb_ctx* ctx) { return ctx ? ctx->last_lanes : 0; }
 
 int32_t sdb_last_lane_width(const sdb_ctx* ctx) { return ctx ? ctx->last_lane_width : 0; }
+
+int64_t sdb_last_tune_us(const sdb_ctx* ctx) { return ctx ? ctx->last_tune_us : 0; }
 
 void sdb_last_layout(const sdb_ctx* ctx, int32_t* lanes, int32_t* persistent,
                      int32_t* ctas_per_sm, int32_t* variant, int32_t* tiles) {

@@ -39,7 +39,7 @@ struct RunArgs {
     double* state_out;        // [orbits][n] state at chunk_end (may be null)
     double* values;           // sample of chunk c, row r: values[(r*vstride + c-chunk_begin)*n + i]
     int64_t* fail_step;       // [orbits] first non-finite absolute step or -1 (may be null)
-    uint64_t* rng_state;      // [orbits][nblocks][4] for stateful streams
+    uint64_t* rng_state;      // [orbits][nblocks][4] for stateful streams (null: not saved)
     int64_t orbits, orbit_offset, vstride;
     int64_t ksteps, chunk_begin, chunk_end;
     uint64_t seed;
@@ -565,7 +565,7 @@ __device__ __forceinline__ void run_item(const RunArgs& a, int64_t cg, uint64_t 
             }
             if (a.fail_step != nullptr && lane == 0) a.fail_step[row] = gf;
             if constexpr (kStateful) {
-                if (base % 4 == 0) {
+                if (a.rng_state != nullptr && base % 4 == 0) {
 #pragma unroll
                     for (int t = 0; t < NB; ++t) {
                         const int b = base / 4 + t;

@@ -327,6 +327,7 @@ def last_launch_info(devices=None) -> dict:
     lib.sdb_last_layout(ctx, *(ctypes.byref(v) for v in lay))
     lanes, persistent, ctas, variant, tiles = (int(v.value) for v in lay)
     return {"launches": int(lib.sdb_last_launch_count(ctx)), "lanes": lanes,
+            "tune_us": int(lib.sdb_last_tune_us(ctx)),
             "lane_width": int(lib.sdb_last_lane_width(ctx)),
             "persistent_grid": bool(persistent), "ctas_per_sm": ctas,
             "register_capped": bool(variant), "tiles": tiles}

@@ -19,6 +19,12 @@ PARITY_TOL = 1e-10
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200) and libsdeb200.so")
+    # the layout autotuner's on-disk cache: a per-session file, so every test
+    # session probes like a fresh box and nothing lands in ~/.cache
+    if "SDEB200_TUNE_CACHE" not in os.environ:
+        import tempfile
+        os.environ["SDEB200_TUNE_CACHE"] = os.path.join(
+            tempfile.mkdtemp(prefix="sdeb200-tune-"), "layouts.tsv")
 
 
 @pytest.fixture(scope="session")
