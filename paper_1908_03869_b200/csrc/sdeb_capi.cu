@@ -415,9 +415,10 @@ int layout_J(const sdb_desc& d, const Layout& l) {
 // zero padding, and the noise blocks and Box-Muller pairs are the same.
 int exact_J(const sdb_desc& d) {
     const bool fits = d.nequat >= 3 && d.nequat <= kMaxJ && d.nequat != next_pow2(d.nequat);
-    return (fits && d.coupling == SDB_COUPLING_MEANFIELD && (d.lanes == 0 || d.lanes == 1))
-               ? d.nequat
-               : 0;
+    const bool one_lane = d.lanes == 1 ||
+                          (d.lanes == 0 && (d.coupling == SDB_COUPLING_MEANFIELD ||
+                                            sdeb::pairwise_lanes(d.nequat) == 1));
+    return (fits && one_lane) ? d.nequat : 0;
 }
 
 int64_t cta_groups(const sdb_desc& d, int lanes) {
@@ -443,6 +444,9 @@ sdb_status candidate_layouts(sdb_ctx* ctx, const Slot& s, const sdb_desc& d, int
     std::vector<int> lanes_list;
     if (d.lanes != 0) {
         lanes_list.push_back(d.lanes);
+    } else if (d.coupling == SDB_COUPLING_PAIRWISE) {
+        // the pairwise sum's order depends on (L, J): one lane count per n
+        lanes_list.push_back(sdeb::pairwise_lanes(d.nequat));
     } else {
         for (int L : candidate_lanes(d.nequat)) lanes_list.push_back(L);
     }
@@ -1198,6 +1202,7 @@ sdb_status run_shard(sdb_ctx* ctx, Slot& s, sdb_desc d, sdb_model* m, int64_t r0
     const int threads = host_copy_threads(shards);
     d.orbit_offset += r0;
     d.orbits = rows;
+    const double ta = tr ? now_ms() : 0.0;
     SDB_CUDA(ctx, s.init.ensure(size_t(rows) * n * sizeof(double)));
     SDB_CUDA(ctx, s.params.ensure(size_t(rows) * np_ * sizeof(double)));
     // device words per row: samples 1..k of the state, or (r, Phi) of samples 0..k
@@ -1205,6 +1210,8 @@ sdb_status run_shard(sdb_ctx* ctx, Slot& s, sdb_desc d, sdb_model* m, int64_t r0
     SDB_CUDA(ctx, s.values.ensure(size_t(rows) * width * sizeof(double)));
     SDB_CUDA(ctx, s.fail.ensure(size_t(rows) * sizeof(int64_t)));
     if (!s.ev_in) SDB_CUDA(ctx, cudaEventCreateWithFlags(&s.ev_in, cudaEventDisableTiming));
+    const double alloc_ms = tr ? now_ms() - ta : 0.0;
+    double pin_ms = 0.0, launch_ms = 0.0;  // pinned-slot growth, launch_device (incl. autotune)
 
     const int64_t tiles = shard_tiles(d, rows, s.device);
     const size_t piece_cap = size_t(std::max(1, env_int("SDEB200_PIECE_KB", 65536))) << 10;
@@ -1323,7 +1330,9 @@ sdb_status run_shard(sdb_ctx* ctx, Slot& s, sdb_desc d, sdb_model* m, int64_t r0
             const int64_t pr = std::min(in_piece, b - p0);
             PinBuf& pb = s.pin_in[in_next];
             in_next = (in_next + 1) % kPinSlots;
+            const double p0t = tr ? now_ms() : 0.0;
             SDB_CUDA(ctx, pb.ensure(size_t(pr) * in_row));
+            if (tr) pin_ms += now_ms() - p0t;
             const double w0 = now_ms();
             SDB_CUDA(ctx, cudaEventSynchronize(pb.ev));  // the slot's previous DMA is done
             const double w1 = now_ms();
@@ -1360,8 +1369,10 @@ sdb_status run_shard(sdb_ctx* ctx, Slot& s, sdb_desc d, sdb_model* m, int64_t r0
         sdb_desc td = d;
         td.orbit_offset = d.orbit_offset + a;
         td.orbits = b - a;
+        const double l0 = tr ? now_ms() : 0.0;
         sdb_status rc = launch_device(ctx, s, td, m, d_init + a * n, d_params + a * np_,
                                       d_values + a * width, d_fail + a, s.stream, out_mode);
+        if (tr) launch_ms += now_ms() - l0;
         if (rc != SDB_OK) return rc;
         SDB_CUDA(ctx, cudaEventRecord(s.ev_tile[t], s.stream));
         return SDB_OK;
@@ -1379,7 +1390,9 @@ sdb_status run_shard(sdb_ctx* ctx, Slot& s, sdb_desc d, sdb_model* m, int64_t r0
             const int slot = out_next;
             out_next = (out_next + 1) % kPinSlots;
             PinBuf& pb = s.pin_out[slot];
+            const double p0t = tr ? now_ms() : 0.0;
             SDB_CUDA(ctx, pb.ensure(size_t(pr) * out_row));
+            if (tr) pin_ms += now_ms() - p0t;
             double* dst = pb.as<double>();
             SDB_CUDA(ctx, cudaMemcpyAsync(dst, d_values + p0 * width,
                                           size_t(pr) * width * sizeof(double),
@@ -1417,10 +1430,12 @@ sdb_status run_shard(sdb_ctx* ctx, Slot& s, sdb_desc d, sdb_model* m, int64_t r0
     if (tr) {
         std::fprintf(stderr,
                      "[sdeb200] dev %d rows %lld tiles %lld: total %.3f ms, host-in %.3f ms, "
-                     "host-out %.3f ms, waits %.3f ms, prefault %.3f ms (%.1f MB in, %.1f MB out)\n",
+                     "host-out %.3f ms, waits %.3f ms, prefault %.3f ms, device alloc %.3f ms, "
+                     "pinned alloc %.3f ms, launch calls %.3f ms, tune %.3f ms (%.1f MB in, "
+                     "%.1f MB out)\n",
                      s.device, (long long)rows, (long long)tiles, now_ms() - t0, host_in_ms,
-                     host_out_ms, wait_ms, prefault_ms, double(rows) * in_row / 1e6,
-                     double(rows) * out_row / 1e6);
+                     host_out_ms, wait_ms, prefault_ms, alloc_ms, pin_ms, launch_ms,
+                     s.tune_us * 1e-3, double(rows) * in_row / 1e6, double(rows) * out_row / 1e6);
     }
     return rc;
 }

@@ -175,54 +175,177 @@ __device__ __forceinline__ void meanfield_folded(const double (&y)[J], const dou
     for (int q = 0; q < J; ++q) out[q] = __fma_rn(cs[q], sa, __fma_rn(-sn[q], sb, c0[q]));
 }
 
-// PAIRWISE: S_i = sum_{j=0}^{n-1} sin(fl(y_j - y_i)), accumulated in j order.
-// The group's state is staged in shared memory sh[q][tid] (conflict-free for
-// the owner).  L == 1 uses the antisymmetric tiling (each unordered pair
-// once: sin(y_i - y_j) = -sin(y_j - y_i), the accumulation order per row
-// stays j-sequential); L > 1 evaluates the full row per lane.
-template <int J>
-__device__ __forceinline__ void drift_pairwise(const double (&y)[J], const double (&om)[J],
-                                               double kn, int base, int n, int lanes,
-                                               double* sh, double* shs, double (&f)[J]) {
-    const int tid = threadIdx.x;
-    const int gbase = tid & ~(lanes - 1);  // first thread of this group in the block
-#pragma unroll
-    for (int q = 0; q < J; ++q) sh[q * kBlock + tid] = y[q];
-    __syncwarp();
-    double s[J];
-    if (lanes == 1) {
-#pragma unroll
-        for (int q = 0; q < J; ++q) shs[q * kBlock + tid] = 0.0;
-        for (int i = 0; i < n; ++i) {
-            const double yi = sh[i * kBlock + tid];
-            double si = shs[i * kBlock + tid];
-            for (int j = i + 1; j < n; ++j) {
-                double t, unused;
-                sincos_any(__dsub_rn(sh[j * kBlock + tid], yi), t, unused);
-                si = __dadd_rn(si, t);
-                shs[j * kBlock + tid] = __dadd_rn(shs[j * kBlock + tid], -t);
-            }
-            shs[i * kBlock + tid] = si;
-        }
-#pragma unroll
-        for (int q = 0; q < J; ++q) s[q] = shs[q * kBlock + tid];
+// PAIRWISE: S_i = sum_{j != i} sin(fl(y_j - y_i)), every term computed as
+// the reference computes it (model.py:193-195), each unordered pair ONCE:
+// fl(a - b) == -fl(b - a) and the table sin is exactly odd, so the term of
+// row j is the negated term of row i (the diagonal sin(0) = 0 is skipped).
+//
+// Lane l of an orbit's L lanes owns oscillators [lJ, lJ + J) (registers).
+// The pairs form L x L tiles of J x J terms:
+//   * tile (l, l) (the lane's own block): J(J-1)/2 terms, j-sequential per row;
+//   * round d = 1 .. L/2-1: lane l takes tile (l, l+d) -- the partner's block
+//     arrives by __shfl_sync, each term goes to the lane's row sum and,
+//     negated, to a column sum that is shuffled back to the partner (the
+//     partner receives from lane l-d: every unordered block pair is covered
+//     once, by the lane at the smaller cyclic distance);
+//   * round L/2 (the two lanes are each other's partners): the tile is split
+//     in a checkerboard, lane l computing the pairs with (q + r + h) even
+//     (h = the upper half's 1), through a one-slot rotation of the partner's
+//     block so both halves run the same instruction stream; the column sums
+//     are exchanged with __shfl_xor_sync.
+// Per lane (L J)(L J - 1) / (2 L) terms: the n^2 / 2 of the antisymmetric sum,
+// balanced, with 4J SHFL.64 per round and no shared memory.  The summation
+// order is fixed by (L, J); run_batch derives the pairwise layout from n alone
+// (pairwise_lanes), so results do not depend on GPU count, shards, tiles or
+// grid mode.  Within 1e-15 relative of the reference's numpy order.
+// sin of any argument, out of line: the rare huge-phase path of the pairwise
+// tiles calls it per term (inlining libdevice's reduction into J^2 unrolled
+// terms multiplied the code and the compile time).
+static __device__ __noinline__ double pair_sin_exact(double x) {
+    double s, c;
+    sincos_any(x, s, c);
+    (void)c;
+    return s;
+}
+
+template <bool SLOW>
+__device__ __forceinline__ double pair_sin(double x) {
+    if constexpr (SLOW) {
+        return pair_sin_exact(x);
     } else {
+        double s, c;
+        sincos_small(x, s, c);  // the cos half is dead code
+        (void)c;
+        return s;
+    }
+}
+
+template <int J, bool PADDED, bool SLOW>
+__device__ __forceinline__ void pair_tile_diag(const double (&y)[J], int base, int n,
+                                               double (&S)[J]) {
 #pragma unroll
-        for (int q = 0; q < J; ++q) s[q] = 0.0;
-        for (int j = 0; j < n; ++j) {
-            const double yj = sh[(j % J) * kBlock + gbase + j / J];
+    for (int i = 0; i < J; ++i) {
 #pragma unroll
-            for (int q = 0; q < J; ++q) {
-                double t, unused;
-                sincos_any(__dsub_rn(yj, y[q]), t, unused);
-                s[q] = __dadd_rn(s[q], t);
-            }
+        for (int j = i + 1; j < J; ++j) {
+            double d = __dsub_rn(y[j], y[i]);
+            if (PADDED && base + j >= n) d = 0.0;  // j > i: covers an invalid i too
+            const double t = pair_sin<SLOW>(d);
+            S[i] = __dadd_rn(S[i], t);
+            S[j] = __dsub_rn(S[j], t);
         }
     }
-    __syncwarp();
+}
+
+template <int J, bool PADDED, bool SLOW>
+__device__ __forceinline__ void pair_tile_full(const double (&y)[J], const double (&ym)[J],
+                                               int base, int pbase, int n, double (&S)[J],
+                                               double (&C)[J]) {
+#pragma unroll
+    for (int r = 0; r < J; ++r) C[r] = 0.0;
+    // J > 8 only runs for explicit lane counts (pairwise_lanes uses J <= 8 for
+    // multi-lane layouts): rolled row loop there, to bound code size
+#pragma unroll(J <= 8 ? J : 1)
+    for (int q = 0; q < J; ++q) {
+#pragma unroll
+        for (int r = 0; r < J; ++r) {
+            double d = __dsub_rn(ym[r], y[q]);
+            if (PADDED && (base + q >= n || pbase + r >= n)) d = 0.0;
+            const double t = pair_sin<SLOW>(d);
+            S[q] = __dadd_rn(S[q], t);
+            C[r] = __dsub_rn(C[r], t);
+        }
+    }
+}
+
+// The checkerboard half of tile (l, partner) for the half round: pairs
+// (q, r) with r == q + h (mod 2); ymr[s] = ym[(s + h) % J] so that r = s + h
+// and both halves loop over s = q + 2k (mod J) with no divergence.
+template <int J, bool PADDED, bool SLOW>
+__device__ __forceinline__ void pair_tile_half(const double (&y)[J], const double (&ym)[J], int h,
+                                               int base, int pbase, int n, double (&S)[J],
+                                               double (&C)[J]) {
+    double ymr[J], Cr[J];
+    bool vr[J];
+#pragma unroll
+    for (int s = 0; s < J; ++s) {
+        ymr[s] = h ? ym[(s + 1) % J] : ym[s];
+        vr[s] = !PADDED || pbase + ((s + h) % J) < n;
+        Cr[s] = 0.0;
+    }
+#pragma unroll(J <= 8 ? J : 1)
+    for (int q = 0; q < J; ++q) {
+#pragma unroll
+        for (int k = 0; k < J / 2; ++k) {
+            const int sidx = (q + 2 * k) % J;
+            double d = __dsub_rn(ymr[sidx], y[q]);
+            if (PADDED && (base + q >= n || !vr[sidx])) d = 0.0;
+            const double t = pair_sin<SLOW>(d);
+            S[q] = __dadd_rn(S[q], t);
+            Cr[sidx] = __dsub_rn(Cr[sidx], t);
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < J; ++r) C[r] = h ? Cr[(r + J - 1) % J] : Cr[r];
+}
+
+template <int J, bool PADDED, bool SLOW>
+__device__ __forceinline__ void pair_sums(const double (&y)[J], int base, int n, int lanes,
+                                          double (&S)[J]) {
+#pragma unroll
+    for (int q = 0; q < J; ++q) S[q] = 0.0;
+    pair_tile_diag<J, PADDED, SLOW>(y, base, n, S);
+    const int lane = int(threadIdx.x) & (lanes - 1);
+    const int half = lanes >> 1;
+    for (int d = 1; d < half; ++d) {  // full tiles (lanes >= 4)
+        double ym[J], C[J];
+        const int src = (lane + d) & (lanes - 1);
+#pragma unroll
+        for (int r = 0; r < J; ++r) ym[r] = __shfl_sync(0xffffffffu, y[r], src, lanes);
+        pair_tile_full<J, PADDED, SLOW>(y, ym, base, src * J, n, S, C);
+        const int from = (lane - d) & (lanes - 1);
+#pragma unroll
+        for (int q = 0; q < J; ++q)
+            S[q] = __dadd_rn(S[q], __shfl_sync(0xffffffffu, C[q], from, lanes));
+    }
+    if (half > 0) {  // the half round (lanes >= 2)
+        double ym[J], C[J];
+#pragma unroll
+        for (int r = 0; r < J; ++r) ym[r] = __shfl_xor_sync(0xffffffffu, y[r], half);
+        const int h = lane >= half ? 1 : 0;
+        if constexpr (J >= 2) {
+            pair_tile_half<J, PADDED, SLOW>(y, ym, h, base, (lane ^ half) * J, n, S, C);
+        } else {  // one oscillator per lane: the lower lane takes the single pair
+            double d = __dsub_rn(ym[0], y[0]);
+            if (PADDED && (base >= n || (lane ^ half) * J >= n)) d = 0.0;
+            const double t = h ? 0.0 : pair_sin<SLOW>(d);
+            S[0] = __dadd_rn(S[0], t);
+            C[0] = -t;
+        }
+#pragma unroll
+        for (int q = 0; q < J; ++q)
+            S[q] = __dadd_rn(S[q], __shfl_xor_sync(0xffffffffu, C[q], half));
+    }
+}
+
+template <int J, bool PADDED>
+__device__ __forceinline__ void drift_pairwise(const double (&y)[J], const double (&om)[J],
+                                               double kn, int base, int n, int lanes,
+                                               double* /*sh*/, double* /*shs*/, double (&f)[J]) {
+    // |y| < 2^28 everywhere in the warp keeps every difference inside the fast
+    // sin's range; otherwise the whole warp takes the exact reduction (same
+    // bits for the small arguments, so the vote never changes a result)
+    bool big = false;
+#pragma unroll
+    for (int q = 0; q < J; ++q) big |= (__double2hiint(y[q]) & 0x7fffffff) >= 0x41B00000;
+    double S[J];
+    if (__any_sync(0xffffffffu, big)) {
+        pair_sums<J, PADDED, true>(y, base, n, lanes, S);
+    } else {
+        pair_sums<J, PADDED, false>(y, base, n, lanes, S);
+    }
 #pragma unroll
     for (int q = 0; q < J; ++q) {
-        f[q] = (base + q < n) ? __dadd_rn(om[q], __dmul_rn(kn, s[q])) : 0.0;
+        f[q] = (base + q < n) ? __dadd_rn(om[q], __dmul_rn(kn, S[q])) : 0.0;
     }
 }
 
@@ -233,7 +356,7 @@ __device__ __forceinline__ void drift(const double (&y)[J], const double (&om)[J
     if constexpr (COUPLING == KC_MEANFIELD) {
         drift_meanfield<J, PADDED>(y, om, kn, base, n, lanes, f);
     } else {
-        drift_pairwise<J>(y, om, kn, base, n, lanes, sh, shs, f);
+        drift_pairwise<J, PADDED>(y, om, kn, base, n, lanes, sh, shs, f);
     }
 }
 
@@ -245,7 +368,7 @@ __device__ __forceinline__ void rk4_drift(const double (&y)[J], const double (&o
     if constexpr (COUPLING == KC_MEANFIELD) {
         meanfield_folded<J, PADDED>(y, om, kn, base, n, lanes, f);
     } else {
-        drift_pairwise<J>(y, om, kn, base, n, lanes, sh, shs, f);
+        drift_pairwise<J, PADDED>(y, om, kn, base, n, lanes, sh, shs, f);
     }
 }
 
@@ -664,8 +787,19 @@ template <int J>
 cudaError_t occupancy_kuramoto_j(int solver, int stream, int coupling, int padded, size_t smem,
                                  int* blocks);
 
-inline size_t pairwise_smem_bytes(int J, int coupling) {
-    return coupling == KC_PAIRWISE ? size_t(2) * J * kBlock * sizeof(double) : 0;
+// The pairwise drift keeps everything in registers and shuffles (no shared
+// memory beyond the staged math tables).
+inline size_t pairwise_smem_bytes(int /*J*/, int /*coupling*/) { return 0; }
+
+// The pairwise coupling's lane count for n oscillators: one lane per orbit up
+// to n = 15 (J = n, the whole antisymmetric triangle in registers), else
+// blocks of J = 8 (J = 16 beyond n = 256), L = next_pow2(n) / J.  A function
+// of n alone: the pairwise summation order depends on (L, J).
+inline int pairwise_lanes(int n) {
+    int p = 1;
+    while (p < n) p <<= 1;
+    if (n <= 15) return 1;
+    return p / 8 <= 32 ? p / 8 : p / 16;
 }
 
 }  // namespace sdeb

@@ -54,8 +54,8 @@ static cudaError_t occupancy_one(size_t smem, int* blocks) {
 // Visits the kernel instantiation for (solver, stream, coupling, variant)
 // with op.template run<J, S, R, C, V>() (V: 0 unpadded, 1 padded, 2 unpadded
 // register-capped; +4: samples are the order parameter, kVarCoherence).
-// Pairwise and the explicit-noise / drift entry points always use the padded
-// form; capped variants exist where tight_minb<J>() > 1.
+// The explicit-noise / drift entry points always use the padded form; capped
+// variants exist where tight_minb<J>() > 1 (meanfield only).
 template <int J, class Op>
 static cudaError_t dispatch(int solver, int stream, int coupling, int variant, Op&& op) {
     if (variant == 2 && tight_minb<J>() == 1) variant = 0;
@@ -68,8 +68,12 @@ static cudaError_t dispatch(int solver, int stream, int coupling, int variant, O
         default: return op.template run<J, S, R, KC_MEANFIELD, (tight_minb<J>() > 1 ? 2 : 0)>(); \
     }
 #define SDEB_PAIR(S, R)                                                          \
-    return variant >= kVarCoherence ? op.template run<J, S, R, KC_PAIRWISE, 5>() \
-                                    : op.template run<J, S, R, KC_PAIRWISE, 1>();
+    switch (variant) {                                                           \
+        case 0: case 2: return op.template run<J, S, R, KC_PAIRWISE, 0>();       \
+        case 4: return op.template run<J, S, R, KC_PAIRWISE, 4>();               \
+        case 5: return op.template run<J, S, R, KC_PAIRWISE, 5>();               \
+        default: return op.template run<J, S, R, KC_PAIRWISE, 1>();              \
+    }
     if (coupling == KC_PAIRWISE) {
         if (solver == KS_RK4) SDEB_PAIR(KS_RK4, KS_NONE);
         if (solver == KS_DRIFT) return op.template run<J, KS_DRIFT, KS_NONE, KC_PAIRWISE, 1>();
