@@ -459,7 +459,7 @@ sdb_status candidate_layouts(sdb_ctx* ctx, const Slot& s, const sdb_desc& d, int
       const int L = shape.first, J = shape.second;
       const int XJ = J == P / L ? 0 : J;  // Layout::J (0 = the power-of-two span)
       const bool can_tight = d.nequat == P && d.coupling == SDB_COUPLING_MEANFIELD &&
-                             (J == 4 || J == 8);
+                             (J == 4 || J == 8 || J == 16);
       for (int tight = 0; tight <= (can_tight ? 1 : 0); ++tight) {
         const int padded = kernel_variant(d, L, J, tight);
         int occ = 0;

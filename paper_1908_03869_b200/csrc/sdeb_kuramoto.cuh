@@ -152,10 +152,10 @@ __device__ __forceinline__ void drift_meanfield(const double (&y)[J], const doub
 // -- 2 FP64 ops per oscillator instead of 4 (+2 per lane).  A reassociation
 // of the reference's (ω + (K/n) S) by a few ulp (folded
 // update); drift_eval keeps the exact form above.
-template <int J, bool PADDED>
-__device__ __forceinline__ void meanfield_folded(const double (&y)[J], const double (&c0)[J],
-                                                 double scale, int base, int n, int lanes,
-                                                 double (&out)[J]) {
+template <int J, bool PADDED, class C0>
+__device__ __forceinline__ void meanfield_folded_acc(const double (&y)[J], C0&& c0, double scale,
+                                                     int base, int n, int lanes,
+                                                     double (&out)[J]) {
     double sn[J], cs[J], ts[J], tc[J];
     sincos_vec<J>(y, sn, cs);
 #pragma unroll
@@ -172,7 +172,14 @@ __device__ __forceinline__ void meanfield_folded(const double (&y)[J], const dou
     group_sum2(a, b, lanes);
     const double sa = __dmul_rn(scale, a), sb = __dmul_rn(scale, b);
 #pragma unroll
-    for (int q = 0; q < J; ++q) out[q] = __fma_rn(cs[q], sa, __fma_rn(-sn[q], sb, c0[q]));
+    for (int q = 0; q < J; ++q) out[q] = __fma_rn(cs[q], sa, __fma_rn(-sn[q], sb, c0(q)));
+}
+
+template <int J, bool PADDED>
+__device__ __forceinline__ void meanfield_folded(const double (&y)[J], const double (&c0)[J],
+                                                 double scale, int base, int n, int lanes,
+                                                 double (&out)[J]) {
+    meanfield_folded_acc<J, PADDED>(y, [&](int q) { return c0[q]; }, scale, base, n, lanes, out);
 }
 
 // PAIRWISE: S_i = sum_{j != i} sin(fl(y_j - y_i)), every term computed as
@@ -492,7 +499,8 @@ __device__ __forceinline__ void step_noise_apply(const RunArgs& a, int64_t row, 
 // (analysis.py coherence_series fused into the run): per orbit row a plane of
 // r then a plane of Phi, values[row*2*vstride + {0, vstride} + 1 + c-chunk_begin],
 // sample 0 (the initial state) at offset 0.
-template <int J, int SOLVER, int STREAM, int COUPLING, bool PADDED, bool COH = false>
+template <int J, int SOLVER, int STREAM, int COUPLING, bool PADDED, bool COH = false,
+          bool CSM = false>
 __device__ __forceinline__ void run_item(const RunArgs& a, int64_t cg, uint64_t s0, uint64_t s1,
                                          bool first, double* sh, double* shs) {
     constexpr bool kStochastic = (SOLVER == KS_EM) && (STREAM != KS_NONE);
@@ -522,13 +530,22 @@ __device__ __forceinline__ void run_item(const RunArgs& a, int64_t cg, uint64_t 
         sg[q] = (kStochastic && valid) ? __ldg(prow + 1 + n + i) : 0.0;
     }
 
-    // folded step constants of the meanfield EM form (see the step below)
+    // folded step constants of the meanfield EM form (see the step below).
+    // CSM (register-capped J >= 16): they live in this thread's shared-memory
+    // column instead of 4J registers and are re-read where each step uses
+    // them (volatile: never hoisted back into registers), which is what lets
+    // 3 CTAs fit per SM
     double omdt[J], sgs[J];
     const double kndt = __dmul_rn(kn, a.dt);
+    volatile double* cst = sh + threadIdx.x;  // CSM: [2J][kBlock]
 #pragma unroll
     for (int q = 0; q < J; ++q) {
         omdt[q] = __dmul_rn(om[q], a.dt);
         sgs[q] = __dmul_rn(a.sqrt_dt, sg[q]);
+        if constexpr (CSM) {
+            cst[q * kBlock] = omdt[q];
+            cst[(J + q) * kBlock] = sgs[q];
+        }
     }
 
     if constexpr (SOLVER == KS_DRIFT) {
@@ -590,11 +607,20 @@ __device__ __forceinline__ void run_item(const RunArgs& a, int64_t cg, uint64_t 
                     // (K/n)*dt folded into the sums, the noise product unrounded
                     // (a few ulp per step): 4 FP64 ops instead of 10
                     double inc[J];
-                    meanfield_folded<J, PADDED>(y, omdt, kndt, base, n, lanes, inc);
-                    step_noise_apply<J, STREAM, PADDED>(
-                        a, row, orbit_g, step, base, rs, [&](int q, double z) {
-                            y[q] = __fma_rn(sgs[q], z, __dadd_rn(y[q], inc[q]));
-                        });
+                    if constexpr (CSM) {
+                        meanfield_folded_acc<J, PADDED>(
+                            y, [&](int q) { return cst[q * kBlock]; }, kndt, base, n, lanes, inc);
+                        step_noise_apply<J, STREAM, PADDED>(
+                            a, row, orbit_g, step, base, rs, [&](int q, double z) {
+                                y[q] = __fma_rn(cst[(J + q) * kBlock], z, __dadd_rn(y[q], inc[q]));
+                            });
+                    } else {
+                        meanfield_folded<J, PADDED>(y, omdt, kndt, base, n, lanes, inc);
+                        step_noise_apply<J, STREAM, PADDED>(
+                            a, row, orbit_g, step, base, rs, [&](int q, double z) {
+                                y[q] = __fma_rn(sgs[q], z, __dadd_rn(y[q], inc[q]));
+                            });
+                    }
                 } else if constexpr (kStochastic) {
                     drift<J, COUPLING, PADDED>(y, om, kn, base, n, lanes, sh, shs, f);
                     // (y + f*dt) + sqrt(dt) * (s_i * N_i)   (solvers.py:70-71, model.py:201)
@@ -730,7 +756,22 @@ __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
 constexpr int kVarCoherence = 4;
 template <int J>
 __host__ __device__ constexpr int tight_minb() {
-    return J == 4 ? 6 : (J == 8 ? 4 : 1);
+    return J == 4 ? 6 : (J == 8 ? 4 : (J == 16 ? 3 : 1));
+}
+
+// Dynamic shared memory a kernel instantiation needs for itself: the CSM
+// constant columns of the register-capped J = 16 meanfield EM stepper.
+template <int J, int SOLVER, int STREAM, int COUPLING, int VAR>
+__host__ __device__ constexpr bool uses_const_smem() {
+    return VAR == 2 && J >= 16 && SOLVER == KS_EM && STREAM != KS_NONE &&
+           STREAM != KS_EXPLICIT && COUPLING == KC_MEANFIELD;
+}
+
+template <int J, int SOLVER, int STREAM, int COUPLING, int VAR>
+__host__ __device__ constexpr size_t own_smem_bytes() {
+    return uses_const_smem<J, SOLVER, STREAM, COUPLING, VAR>()
+               ? size_t(2) * J * kBlock * sizeof(double)
+               : 0;
 }
 
 template <int J, int SOLVER, int STREAM, int COUPLING, int VAR>
@@ -740,8 +781,8 @@ __global__ void __launch_bounds__(kBlock, (VAR == 2 ? tight_minb<J>() : 0))
     constexpr bool COH = VAR >= kVarCoherence;
     stage_tables();
     extern __shared__ double smem[];
-    double* sh = smem;                  // pairwise: [J][kBlock]
-    double* shs = smem + J * kBlock;    // pairwise L==1: [J][kBlock]
+    double* sh = smem;                  // CSM constants: [2J][kBlock]
+    double* shs = smem + J * kBlock;
     const uint64_t begin = uint64_t(a.chunk_begin) * uint64_t(a.ksteps);
     const uint64_t end = uint64_t(a.chunk_end) * uint64_t(a.ksteps);
     // One run_item call site for both modes (two inlined copies cost ~40
@@ -769,7 +810,9 @@ __global__ void __launch_bounds__(kBlock, (VAR == 2 ? tight_minb<J>() : 0))
         if (persistent) __syncthreads();
         const uint64_t s0 = begin + uint64_t(k) * slab;
         const uint64_t s1 = s0 + slab < end ? s0 + slab : end;
-        run_item<J, SOLVER, STREAM, COUPLING, PADDED, COH>(a, cg, s0, s1, k == 0, sh, shs);
+        run_item<J, SOLVER, STREAM, COUPLING, PADDED, COH,
+                 uses_const_smem<J, SOLVER, STREAM, COUPLING, VAR>()>(a, cg, s0, s1, k == 0, sh,
+                                                                      shs);
         if (!persistent) break;
         __threadfence();
         __syncthreads();
@@ -786,10 +829,6 @@ cudaError_t launch_kuramoto_j(const RunArgs& a, int solver, int stream, int coup
 template <int J>
 cudaError_t occupancy_kuramoto_j(int solver, int stream, int coupling, int padded, size_t smem,
                                  int* blocks);
-
-// The pairwise drift keeps everything in registers and shuffles (no shared
-// memory beyond the staged math tables).
-inline size_t pairwise_smem_bytes(int /*J*/, int /*coupling*/) { return 0; }
 
 // The pairwise coupling's lane count for n oscillators: one lane per orbit up
 // to n = 15 (J = n, the whole antisymmetric triangle in registers), else

@@ -10,8 +10,9 @@ static cudaError_t launch_one(const RunArgs& a, cudaStream_t st) {
     const int64_t threads = a.orbits * int64_t(a.lanes);
     const unsigned grid = a.persistent > 0 ? unsigned(a.persistent)
                                            : unsigned((threads + kBlock - 1) / kBlock);
-    const size_t need = pairwise_smem_bytes(J, C);
-    const size_t smem = need > size_t(a.smem_pad) ? need : size_t(a.smem_pad);
+    constexpr size_t need = own_smem_bytes<J, S, R, C, P>();
+    size_t smem = size_t(a.smem_pad);
+    if constexpr (need > 0) smem = smem < need ? need : smem;
     // static shared memory (the staged math tables) counts against the 48 KB
     // default too: opt in whenever the sum exceeds it
     if (smem + kStaticSmemBytes > 48 * 1024) {
@@ -35,8 +36,8 @@ static inline size_t smem_optin_bytes() {
 
 template <int J, int S, int R, int C, int P>
 static cudaError_t occupancy_one(size_t smem, int* blocks) {
-    const size_t need = pairwise_smem_bytes(J, C);
-    if (smem < need) smem = need;
+    constexpr size_t need = own_smem_bytes<J, S, R, C, P>();
+    if constexpr (need > 0) smem = smem < need ? need : smem;
     if (smem + kStaticSmemBytes > smem_optin_bytes()) {  // cannot launch: no resident CTA
         *blocks = 0;
         return cudaSuccess;
