@@ -266,6 +266,16 @@ sdb_status sdb_model_step(sdb_ctx* ctx, sdb_model* model, int32_t solver, double
                           int64_t count, const double* y, const double* p, const double* noise,
                           double* out);
 
+/* Page-locked host memory for run inputs (cudaHostAlloc, portable across the
+ * context's devices).  When init and params of a host-buffer run lie in such
+ * memory, sdb_run / sdb_run_coherence / sdb_run_to_file DMA them straight to
+ * the device instead of copying them through the library's pinned staging
+ * slots (the host copy is what bounds the input leg of large runs).  The
+ * reference has no counterpart (its arrays are ordinary numpy buffers);
+ * ordinary pageable buffers keep working unchanged. */
+sdb_status sdb_host_alloc(int64_t bytes, void** out);
+void sdb_host_free(void* ptr);
+
 #ifdef __cplusplus
 }
 #endif

@@ -11,7 +11,7 @@ __version__ = "0.1.0"
 from .model import (ModelSpec, OrbitBatch, ModelDefinitionError, kuramoto_model,
                     kuramoto_dsl_model, sample_kuramoto_batch, speed_protocol_batch,
                     accuracy_protocol_batch, model_from_name, model_from_file,
-                    model_from_dsl, drift_eval, diffusion_eval)
+                    model_from_dsl, drift_eval, diffusion_eval, pin_batch)
 from .engine import (EngineConfig, TrajectoryStore, OrbitFailure, ConfigError, run_batch,
                      iteration_count, partition_orbits)
 from .solvers import (euler_maruyama_step, euler_step, rk4_step, implicit_euler_step,
@@ -27,6 +27,7 @@ __all__ = [
     "ModelSpec", "OrbitBatch", "ModelDefinitionError", "kuramoto_model", "kuramoto_dsl_model",
     "sample_kuramoto_batch", "speed_protocol_batch", "accuracy_protocol_batch",
     "model_from_name", "model_from_file", "model_from_dsl", "drift_eval", "diffusion_eval",
+    "pin_batch",
     "EngineConfig", "TrajectoryStore", "OrbitFailure", "ConfigError", "run_batch",
     "iteration_count", "partition_orbits",
     "euler_maruyama_step", "euler_step", "rk4_step",

@@ -59,6 +59,8 @@ SIGNATURES = {
     "sdb_last_lanes": (ctypes.c_int32, [ctypes.c_void_p]),
     "sdb_last_lane_width": (ctypes.c_int32, [ctypes.c_void_p]),
     "sdb_last_tune_us": (ctypes.c_int64, [ctypes.c_void_p]),
+    "sdb_host_alloc": (ctypes.c_int, [ctypes.c_int64, ctypes.POINTER(ctypes.c_void_p)]),
+    "sdb_host_free": (None, [ctypes.c_void_p]),
     "sdb_last_layout": (None, [ctypes.c_void_p] + [ctypes.POINTER(ctypes.c_int32)] * 5),
     "sdb_philox_words": (ctypes.c_int, [ctypes.c_void_p, _c_u32_p, ctypes.c_int64, _c_u32_p]),
     "sdb_run_to_file": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(SdbDesc),
@@ -303,3 +305,33 @@ def host_empty(shape, dtype=np.float64) -> np.ndarray:
     buf = (ctypes.c_char * nbytes).from_address(addr)
     buf._owner = _StoreMapping(addr, nbytes)  # ctypes buffers take attributes
     return np.frombuffer(buf, dtype=dtype).reshape(shape)
+
+
+class _PinnedBlock:
+    """Owner of one sdb_host_alloc block (freed when the last view dies)."""
+
+    __slots__ = ("addr",)
+
+    def __init__(self, addr: int):
+        self.addr = addr
+
+    def __del__(self):
+        try:
+            if _lib is not None:
+                _lib.sdb_host_free(self.addr)
+        except Exception:  # interpreter shutdown
+            pass
+
+
+def host_pinned(shape, dtype=np.float64) -> np.ndarray:
+    """An ndarray in page-locked host memory (cudaHostAlloc through
+    sdb_host_alloc).  Run inputs in such arrays are DMA'd to the GPU without
+    the host staging copy; pinning costs ~0.3 s per GB, so allocate once and
+    refill, as for any pinned buffer."""
+    dtype = np.dtype(dtype)
+    nbytes = int(np.prod(shape, dtype=np.int64)) * dtype.itemsize
+    out = ctypes.c_void_p()
+    check(lib().sdb_host_alloc(nbytes, ctypes.byref(out)), None, "sdb_host_alloc")
+    buf = (ctypes.c_char * max(nbytes, 1)).from_address(out.value)
+    buf._owner = _PinnedBlock(out.value)
+    return np.frombuffer(buf, dtype=dtype, count=int(np.prod(shape, dtype=np.int64))).reshape(shape)

@@ -459,7 +459,7 @@ sdb_status candidate_layouts(sdb_ctx* ctx, const Slot& s, const sdb_desc& d, int
       const int L = shape.first, J = shape.second;
       const int XJ = J == P / L ? 0 : J;  // Layout::J (0 = the power-of-two span)
       const bool can_tight = d.nequat == P && d.coupling == SDB_COUPLING_MEANFIELD &&
-                             (J == 4 || J == 8 || J == 16);
+                             (J == 4 || J == 8);
       for (int tight = 0; tight <= (can_tight ? 1 : 0); ++tight) {
         const int padded = kernel_variant(d, L, J, tight);
         int occ = 0;
@@ -1132,6 +1132,22 @@ int host_copy_threads(int /*shards*/) {
     return std::max(1, env_int("SDEB200_HOST_THREADS", std::min(32, std::max(1, hw / procs))));
 }
 
+// True when [p, p + bytes) lies in page-locked memory the driver knows
+// (cudaHostAlloc / cudaHostRegister): the DMA engines can read it directly.
+bool is_pinned_range(const void* p, size_t bytes) {
+    if (!p || bytes == 0) return false;
+    const char* lo = static_cast<const char*>(p);
+    for (const char* q : {lo, lo + bytes - 1}) {
+        cudaPointerAttributes attr{};
+        if (cudaPointerGetAttributes(&attr, q) != cudaSuccess) {
+            cudaGetLastError();
+            return false;
+        }
+        if (attr.type != cudaMemoryTypeHost) return false;
+    }
+    return true;
+}
+
 // Orbit tiles of a host-buffer shard: copies of tile t+1 / t-1 overlap the
 // kernel of tile t.  A tile must keep the kernel well fed (>= ~8 waves of
 // resident threads at a typical lanes-per-orbit, 2 for transfer-heavy runs)
@@ -1325,7 +1341,20 @@ sdb_status run_shard(sdb_ctx* ctx, Slot& s, sdb_desc d, sdb_model* m, int64_t r0
         return SDB_OK;
     };
 
+    // inputs in page-locked memory (sdb_host_alloc): one DMA per tile straight
+    // from the caller's rows, no host copy
+    const bool pinned_in = is_pinned_range(init + r0 * n, size_t(rows) * n * sizeof(double)) &&
+                           is_pinned_range(params + r0 * np_, size_t(rows) * np_ * sizeof(double));
     auto stage_inputs = [&](int64_t a, int64_t b) -> sdb_status {
+        if (pinned_in) {
+            SDB_CUDA(ctx, cudaMemcpyAsync(d_init + a * n, init + (r0 + a) * n,
+                                          size_t(b - a) * n * sizeof(double),
+                                          cudaMemcpyHostToDevice, s.h2d));
+            SDB_CUDA(ctx, cudaMemcpyAsync(d_params + a * np_, params + (r0 + a) * np_,
+                                          size_t(b - a) * np_ * sizeof(double),
+                                          cudaMemcpyHostToDevice, s.h2d));
+            return SDB_OK;
+        }
         for (int64_t p0 = a; p0 < b; p0 += in_piece) {
             const int64_t pr = std::min(in_piece, b - p0);
             PinBuf& pb = s.pin_in[in_next];
@@ -1680,6 +1709,18 @@ int32_t sdb_last_lanes(const sdb_ctx* ctx) { return ctx ? ctx->last_lanes : 0; }
 int32_t sdb_last_lane_width(const sdb_ctx* ctx) { return ctx ? ctx->last_lane_width : 0; }
 
 int64_t sdb_last_tune_us(const sdb_ctx* ctx) { return ctx ? ctx->last_tune_us : 0; }
+
+sdb_status sdb_host_alloc(int64_t bytes, void** out) {
+    if (!out || bytes < 0) return fail_with(nullptr, SDB_ERR_ARGUMENT, "bad host allocation");
+    *out = nullptr;
+    cudaError_t e = cudaHostAlloc(out, size_t(std::max<int64_t>(bytes, 1)), cudaHostAllocPortable);
+    if (e != cudaSuccess) return cuda_fail(nullptr, e, "cudaHostAlloc");
+    return SDB_OK;
+}
+
+void sdb_host_free(void* ptr) {
+    if (ptr) cudaFreeHost(ptr);
+}
 
 void sdb_last_layout(const sdb_ctx* ctx, int32_t* lanes, int32_t* persistent,
                      int32_t* ctas_per_sm, int32_t* variant, int32_t* tiles) {

@@ -564,3 +564,24 @@ def test_layout_autotune_is_bounded_and_persisted():
     tune_us2, launches2, _, second = fresh_run()  # a new context: the disk cache answers
     assert tune_us2 == 0 and launches2 == 0
     assert np.array_equal(first, second)
+
+
+def test_pinned_inputs_take_the_direct_dma_path_bit_identically(monkeypatch):
+    # sdb.pin_batch: inputs in page-locked memory are DMA'd without the host
+    # staging copy; results equal the pageable path for every tiling / shard count
+    from paper_1908_03869_b200 import _native as nat
+    n, m = 32, 40000
+    batch = sdb.sample_kuramoto_batch(n, m, (0.2, 0.4), (0.01, 0.1), 0.3, seed=21)
+    pinned = sdb.pin_batch(batch)
+    assert np.array_equal(pinned.init, batch.init) and np.array_equal(pinned.params, batch.params)
+    cfg = EngineConfig(dt=1e-3, tspan=0.1, ksteps=25, orbits=m, seed=4)
+    want = sdb.store_hash(run_batch(sdb.kuramoto_model(n), cfg, batch))
+    assert sdb.store_hash(run_batch(sdb.kuramoto_model(n), cfg, pinned)) == want
+    monkeypatch.setenv("SDEB200_TILES", "3")
+    assert sdb.store_hash(run_batch(sdb.kuramoto_model(n), cfg, pinned)) == want
+    assert sdb.store_hash(run_batch(sdb.kuramoto_model(n),
+                                    dataclasses.replace(cfg, devices=(0, 0)), pinned)) == want
+    # a pinned scratch array of any shape
+    a = nat.host_pinned((3, 5))
+    a[:] = 7.0
+    assert a.sum() == 105.0
