@@ -220,8 +220,25 @@ int ilog2(int x) {
     return l;
 }
 
+// Lane widths J whose kernel module this process has launched from: the first
+// launch from a module pays its (lazy) load, ~6-45 ms on B200 (measured,
+// tools/module_load_probe.py), which the layout probe budgets for.
+std::atomic<uint32_t> g_loaded_j{0};
+
+cudaError_t launch_run_j(const sdeb::RunArgs& a, int J, int solver, int stream, int coupling,
+                         int padded, cudaStream_t st);
+
 cudaError_t launch_run(const sdeb::RunArgs& a, int J, int solver, int stream, int coupling,
                        int padded, cudaStream_t st) {
+    const cudaError_t e = launch_run_j(a, J, solver, stream, coupling, padded, st);
+    if (e == cudaSuccess && J >= 0 && J < 32) g_loaded_j.fetch_or(1u << J);
+    return e;
+}
+
+bool module_loaded(int J) { return J >= 0 && J < 32 && (g_loaded_j.load() >> J) & 1u; }
+
+cudaError_t launch_run_j(const sdeb::RunArgs& a, int J, int solver, int stream, int coupling,
+                         int padded, cudaStream_t st) {
     switch (J) {
         case 1: return sdeb::launch_kuramoto_j<1>(a, solver, stream, coupling, padded, st);
         case 2: return sdeb::launch_kuramoto_j<2>(a, solver, stream, coupling, padded, st);
@@ -541,16 +558,19 @@ double now_ms();
 // Cost-model ordering of the candidates (smaller is better): FP64 work per
 // thread-step of a lane (J oscillators incl. padding, log2(L) butterfly levels
 // of the two coupling sums), at the SM throughput the resident warps can
-// sustain (latency hiding saturates at ~12 warps/SM), times the wave count
-// of the launch mode.  Only an ordering for the probe and a fallback.
+// sustain (latency hiding saturates at ~8 warps/SM, measured r02), times the
+// wave count of the launch mode.  Only an ordering for the probe and, when a
+// short run leaves no budget to probe more (cold module loads count), the
+// decision itself.
 double prior_cost(const sdb_desc& d, const Layout& l, int J, int sms) {
     const int L = l.lanes;
     const double lane_work = double(J) * 40.0 + 6.0 * ilog2(L) + 12.0;
     const double warps = double(l.ctas_per_sm) * sdeb::kBlock / 32.0;
-    const double eff = std::min(1.0, warps / 12.0);
+    const double eff = std::min(1.0, warps / 8.0);  // J=16 at 8 warps/SM ran as fast as at 12
     const double per_wave = double(sms) * l.ctas_per_sm;
     const double ctas = double(cta_groups(d, L));
-    const double waves = l.persistent ? std::max(1.0, ctas / per_wave) : std::ceil(ctas / per_wave);
+    const double waves = l.persistent ? std::max(1.0, 1.01 * ctas / per_wave)
+                                      : std::ceil(ctas / per_wave);
     // a wave's duration is one CTA's: lane_work per step per thread over the
     // SM's share of the pipe (per_wave CTAs run side by side)
     return waves * lane_work * double(l.ctas_per_sm) / eff;
@@ -713,16 +733,22 @@ sdb_status probe_layouts(sdb_ctx* ctx, Slot& s, const sdb_desc& d, int kind_solv
     int64_t p1 = 32;  // first probe: the cost model's favourite, 32 + 64 steps
     double best_pred = 1e300;
     Layout best = cands[0];
+    constexpr double kModuleLoadMs = 40.0;  // first launch from a not yet loaded module
     for (size_t ci = 0; ci < cands.size() && rc == SDB_OK; ++ci) {
         const Layout& lay = cands[ci];
+        // a candidate in a module this process has not loaded yet costs its
+        // load on top of the probe: only within the budget (never the first)
+        if (ci > 0 && !module_loaded(layout_J(d, lay)) && spent_ms + kModuleLoadMs > budget_ms)
+            continue;
         const int64_t rows =
             std::min<int64_t>(d.orbits, int64_t(sms) * lay.ctas_per_sm * (sdeb::kBlock / lay.lanes));
         float t1 = 0.f, t2 = 0.f;
+        const double w0 = now_ms();
         rc = timed(lay, rows, p1, &t1);
         if (rc != SDB_OK) break;
         rc = timed(lay, rows, 2 * p1, &t2);
         if (rc != SDB_OK) break;
-        spent_ms += 2.0 * (t1 + t2);
+        spent_ms += now_ms() - w0;  // wall time: launches, module loads, syncs
         const double step_ms = std::max(1e-9, double(t2 - t1) / double(p1));
         const double pred = predict(lay, step_ms, rows);
         if (trace_enabled())
@@ -735,8 +761,9 @@ sdb_status probe_layouts(sdb_ctx* ctx, Slot& s, const sdb_desc& d, int kind_solv
             best = lay;
         }
         if (budget_ms < 0.0) {
-            // 10% of the predicted run for the whole probe; the remaining
-            // candidates share what is left (3 p steps each, 2 repetitions)
+            // 10% of the predicted run for the whole probe (the first
+            // candidate's load and probe included); the remaining candidates
+            // share what is left (3 p steps each, 2 repetitions)
             budget_ms = 0.1 * pred;
             const double left = budget_ms - spent_ms;
             const double per_cand = left / double(std::max<size_t>(1, cands.size() - 1));

@@ -488,76 +488,6 @@ __device__ __forceinline__ void step_noise_apply(const RunArgs& a, int64_t row, 
     }
 }
 
-// One whole noise block t of a lane (J % 4 == 0, unpadded): its 4 words
-// (Philox at the step's counter, or the block's stateful stream) and two
-// Box-Muller pairs, handed to apply(q, z).
-template <int J, int STREAM, class Apply>
-__device__ __forceinline__ void noise_block_whole(const RunArgs& a, uint32_t orbit_g,
-                                                  uint64_t step, int base, StreamState& rs, int t,
-                                                  Apply&& apply) {
-    Words4 w;
-    if constexpr (STREAM == KS_PHILOX) {
-        w = philox4x32_10(uint32_t(a.seed >> 32), uint32_t(step >> 32), uint32_t(step),
-                          uint32_t(base / 4 + t), uint32_t(a.seed), orbit_g);
-    } else {
-        w = stream_block<STREAM>(rs);
-    }
-    double z0, z1;
-    box_muller_pair(w.w0, w.w1, z0, z1);
-    apply(4 * t, z0);
-    apply(4 * t + 1, z1);
-    box_muller_pair(w.w2, w.w3, z0, z1);
-    apply(4 * t + 2, z0);
-    apply(4 * t + 3, z1);
-}
-
-// The meanfield EM step with the coupling-sum butterfly and the noise
-// interleaved: level t's shuffles are issued, noise block t (Philox + two
-// Box-Muller pairs, independent of the sums) is drawn and applied while they
-// are in flight, then level t's additions complete.  The shuffle latency of
-// the log2(L)-level butterfly, a serial chain that was exposed once per step
-// (cfg3 lost ~9% between L = 2 and L = 16), now overlaps FP64 and integer
-// work.  Sums: the canonical tree (lane_tree_sum, then xor levels 1, 2, 4..),
-// update: y <- fma(sqrt(dt) s_i, N_i, y) + fma(cos, (K/n)dt Sum sin,
-// fma(-sin, (K/n)dt Sum cos, omega dt)) -- identical to the general path.
-template <int J, int STREAM, class C0, class SG>
-__device__ __forceinline__ void meanfield_em_interleaved(const RunArgs& a, double (&y)[J],
-                                                         C0&& c0, SG&& sgq, double scale,
-                                                         int lanes, uint32_t orbit_g,
-                                                         uint64_t step, int base,
-                                                         StreamState (&rs)[J / 4]) {
-    constexpr int NB = J / 4;
-    double sn[J], cs[J], ts[J], tc[J];
-    sincos_vec<J>(y, sn, cs);
-#pragma unroll
-    for (int q = 0; q < J; ++q) {
-        ts[q] = sn[q];
-        tc[q] = cs[q];
-    }
-    double sa = lane_tree_sum<J>(ts);
-    double sb = lane_tree_sum<J>(tc);
-    auto apply = [&](int q, double z) { y[q] = __fma_rn(sgq(q), z, y[q]); };
-#pragma unroll
-    for (int t = 0; t < 5; ++t) {
-        const int o = 1 << t;
-        const bool level = o < lanes;  // warp-uniform
-        double pa = 0.0, pb = 0.0;
-        if (level) {
-            pa = __shfl_xor_sync(0xffffffffu, sa, o);
-            pb = __shfl_xor_sync(0xffffffffu, sb, o);
-        }
-        if (t < NB) noise_block_whole<J, STREAM>(a, orbit_g, step, base, rs[t < NB ? t : 0], t, apply);
-        if (level) {
-            sa = __dadd_rn(sa, pa);
-            sb = __dadd_rn(sb, pb);
-        }
-    }
-    const double ka = __dmul_rn(scale, sa), kb = __dmul_rn(scale, sb);
-#pragma unroll
-    for (int q = 0; q < J; ++q)
-        y[q] = __dadd_rn(y[q], __fma_rn(cs[q], ka, __fma_rn(-sn[q], kb, c0(q))));
-}
-
 // ---- the fused run kernel ----------------------------------------------------
 
 // One work item: CTA-group `cg` (kBlock/L orbits) advanced over the absolute
@@ -569,8 +499,7 @@ __device__ __forceinline__ void meanfield_em_interleaved(const RunArgs& a, doubl
 // (analysis.py coherence_series fused into the run): per orbit row a plane of
 // r then a plane of Phi, values[row*2*vstride + {0, vstride} + 1 + c-chunk_begin],
 // sample 0 (the initial state) at offset 0.
-template <int J, int SOLVER, int STREAM, int COUPLING, bool PADDED, bool COH = false,
-          bool CSM = false>
+template <int J, int SOLVER, int STREAM, int COUPLING, bool PADDED, bool COH = false>
 __device__ __forceinline__ void run_item(const RunArgs& a, int64_t cg, uint64_t s0, uint64_t s1,
                                          bool first, double* sh, double* shs) {
     constexpr bool kStochastic = (SOLVER == KS_EM) && (STREAM != KS_NONE);
@@ -600,22 +529,13 @@ __device__ __forceinline__ void run_item(const RunArgs& a, int64_t cg, uint64_t 
         sg[q] = (kStochastic && valid) ? __ldg(prow + 1 + n + i) : 0.0;
     }
 
-    // folded step constants of the meanfield EM form (see the step below).
-    // CSM (unpadded meanfield EM at J = 16): they live in this thread's
-    // shared-memory column instead of 4J registers and are re-read where each
-    // step uses them (volatile: never hoisted back into registers) -- room for
-    // the interleaved butterfly / noise step without spills
+    // folded step constants of the meanfield EM form (see the step below)
     double omdt[J], sgs[J];
     const double kndt = __dmul_rn(kn, a.dt);
-    volatile double* cst = sh + threadIdx.x;  // CSM: [2J][kBlock]
 #pragma unroll
     for (int q = 0; q < J; ++q) {
         omdt[q] = __dmul_rn(om[q], a.dt);
         sgs[q] = __dmul_rn(a.sqrt_dt, sg[q]);
-        if constexpr (CSM) {
-            cst[q * kBlock] = omdt[q];
-            cst[(J + q) * kBlock] = sgs[q];
-        }
     }
 
     if constexpr (SOLVER == KS_DRIFT) {
@@ -676,25 +596,12 @@ __device__ __forceinline__ void run_item(const RunArgs& a, int64_t cg, uint64_t 
                     // reference's (y + f*dt) + sqrt(dt)*(s_i*N_i) reassociated,
                     // (K/n)*dt folded into the sums, the noise product unrounded
                     // (a few ulp per step): 4 FP64 ops instead of 10
-                    // every layout: y <- fma(sqrt(dt) s_i, N_i, y) + inc_i (the same
-                    // expression, so lane layouts stay bit-identical)
-                    auto c0 = [&](int q) { return CSM ? cst[q * kBlock] : omdt[q]; };
-                    auto sgq = [&](int q) { return CSM ? cst[(J + q) * kBlock] : sgs[q]; };
-                    // interleaved at J = 16 (every multi-level butterfly of the
-                    // cfg3 sizes; the extra live range costs J = 8 its 3 CTAs/SM)
-                    if constexpr (!PADDED && J == 16 && STREAM != KS_EXPLICIT) {
-                        meanfield_em_interleaved<J, STREAM>(a, y, c0, sgq, kndt, lanes, orbit_g,
-                                                            step, base, rs);
-                    } else {
-                        double inc[J];
-                        meanfield_folded_acc<J, PADDED>(y, c0, kndt, base, n, lanes, inc);
-                        step_noise_apply<J, STREAM, PADDED>(
-                            a, row, orbit_g, step, base, rs, [&](int q, double z) {
-                                y[q] = __fma_rn(sgq(q), z, y[q]);
-                            });
-#pragma unroll
-                        for (int q = 0; q < J; ++q) y[q] = __dadd_rn(y[q], inc[q]);
-                    }
+                    double inc[J];
+                    meanfield_folded<J, PADDED>(y, omdt, kndt, base, n, lanes, inc);
+                    step_noise_apply<J, STREAM, PADDED>(
+                        a, row, orbit_g, step, base, rs, [&](int q, double z) {
+                            y[q] = __fma_rn(sgs[q], z, __dadd_rn(y[q], inc[q]));
+                        });
                 } else if constexpr (kStochastic) {
                     drift<J, COUPLING, PADDED>(y, om, kn, base, n, lanes, sh, shs, f);
                     // (y + f*dt) + sqrt(dt) * (s_i * N_i)   (solvers.py:70-71, model.py:201)
@@ -833,19 +740,12 @@ __host__ __device__ constexpr int tight_minb() {
     return J == 4 ? 6 : (J == 8 ? 4 : 1);
 }
 
-// Dynamic shared memory a kernel instantiation needs for itself: the CSM
-// constant columns of the unpadded J = 16 meanfield EM stepper (32 KB/CTA).
-template <int J, int SOLVER, int STREAM, int COUPLING, int VAR>
-__host__ __device__ constexpr bool uses_const_smem() {
-    return (VAR & 1) == 0 && J >= 16 && SOLVER == KS_EM && STREAM != KS_NONE &&
-           STREAM != KS_EXPLICIT && COUPLING == KC_MEANFIELD;
-}
-
+// Dynamic shared memory a kernel instantiation needs for itself (none: the
+// pairwise tiles live in registers; measured and dropped in r02: step
+// constants in shared memory for J = 16, profiles/r02/experiments.md).
 template <int J, int SOLVER, int STREAM, int COUPLING, int VAR>
 __host__ __device__ constexpr size_t own_smem_bytes() {
-    return uses_const_smem<J, SOLVER, STREAM, COUPLING, VAR>()
-               ? size_t(2) * J * kBlock * sizeof(double)
-               : 0;
+    return 0;
 }
 
 template <int J, int SOLVER, int STREAM, int COUPLING, int VAR>
@@ -855,7 +755,7 @@ __global__ void __launch_bounds__(kBlock, (VAR == 2 ? tight_minb<J>() : 0))
     constexpr bool COH = VAR >= kVarCoherence;
     stage_tables();
     extern __shared__ double smem[];
-    double* sh = smem;                  // CSM constants: [2J][kBlock]
+    double* sh = smem;                  // spare: no instantiation uses dynamic smem
     double* shs = smem + J * kBlock;
     const uint64_t begin = uint64_t(a.chunk_begin) * uint64_t(a.ksteps);
     const uint64_t end = uint64_t(a.chunk_end) * uint64_t(a.ksteps);
@@ -884,9 +784,7 @@ __global__ void __launch_bounds__(kBlock, (VAR == 2 ? tight_minb<J>() : 0))
         if (persistent) __syncthreads();
         const uint64_t s0 = begin + uint64_t(k) * slab;
         const uint64_t s1 = s0 + slab < end ? s0 + slab : end;
-        run_item<J, SOLVER, STREAM, COUPLING, PADDED, COH,
-                 uses_const_smem<J, SOLVER, STREAM, COUPLING, VAR>()>(a, cg, s0, s1, k == 0, sh,
-                                                                      shs);
+        run_item<J, SOLVER, STREAM, COUPLING, PADDED, COH>(a, cg, s0, s1, k == 0, sh, shs);
         if (!persistent) break;
         __threadfence();
         __syncthreads();
