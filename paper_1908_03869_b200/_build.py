@@ -12,6 +12,7 @@ from __future__ import annotations
 
 import hashlib
 import os
+import re
 import shutil
 import subprocess
 import sys
@@ -127,17 +128,64 @@ def _compile(src: str, log: list) -> str:
     deps = [os.path.join(CSRC, src)] + [os.path.join(CSRC, h) for h in HEADERS]
     if src == "sdeb_dsl.cu":
         deps.append(RTC_INC)
+    if src == "sdeb_capi.cu":
+        deps.append(KERNEL_TABLE)
     deps.append(os.path.join(ROOT, "include", "sdeb200.h"))
     key = _digest(toolchain_id(), NVCC_FLAGS, src, *deps)
-    if _stamp_ok(obj, key):
+    if _stamp_ok(obj, key) and os.path.exists(obj + ".ptxas"):
         return obj
     cmd = [nvcc()] + NVCC_FLAGS + ["-c", os.path.join(CSRC, src), "-o", obj]
     res = subprocess.run(cmd, capture_output=True, text=True)
     log.append((src, res.stdout + res.stderr))
     if res.returncode != 0:
         raise RuntimeError("nvcc failed for %s:\n%s" % (src, res.stdout + res.stderr))
+    with open(obj + ".ptxas", "w") as f:  # resource usage, read by _write_kernel_table
+        f.write(res.stdout + res.stderr)
     _write_stamp(obj, key)
     return obj
+
+
+KERNEL_TABLE = os.path.join(OBJ, "sdeb_kernel_table.inc")
+_ENTRY = re.compile(r"Compiling entry function '_ZN4sdeb19kuramoto_run_kernelILi(\d+)ELi(\d+)"
+                    r"ELi(\d+)ELi(\d+)ELi(\d+)EEEvNS_7RunArgsE'")
+_USED = re.compile(r"Used (\d+) registers.*?(\d+) bytes smem")
+
+
+def _write_kernel_table(objs) -> None:
+    """sdeb_kernel_table.inc: registers and static shared memory of every
+    kuramoto_run_kernel instantiation, from ptxas -v of the stepper objects.
+    The layout autotuner estimates occupancy from it without touching (and so
+    lazily loading) kernel modules it may never launch."""
+    rows = set()
+    for obj in objs:
+        try:
+            with open(obj + ".ptxas") as f:
+                text = f.read()
+        except OSError:
+            continue
+        cur = None
+        for ln in text.splitlines():
+            m = _ENTRY.search(ln)
+            if m:
+                cur = tuple(int(x) for x in m.groups())
+                continue
+            m = _USED.search(ln)
+            if m and cur:
+                rows.add(cur + (int(m.group(1)), int(m.group(2))))
+                cur = None
+    body = ["// generated by _build.py from ptxas -v; {J, solver, stream, coupling, variant, "
+            "registers, static smem bytes}",
+            "const KernelRes kKernelRes[] = {"]
+    body += ["    {%d, %d, %d, %d, %d, %d, %d}," % r for r in sorted(rows)]
+    body += ["    {0, 0, 0, 0, 0, 0, 0},", "};", ""]
+    text = "\n".join(body)
+    if os.path.exists(KERNEL_TABLE):
+        with open(KERNEL_TABLE) as f:
+            if f.read() == text:
+                return
+    with open(KERNEL_TABLE + ".tmp", "w") as f:
+        f.write(text)
+    os.replace(KERNEL_TABLE + ".tmp", KERNEL_TABLE)
 
 
 def build(verbose: bool = False, force: bool = False) -> str:
@@ -147,8 +195,14 @@ def build(verbose: bool = False, force: bool = False) -> str:
             os.remove(os.path.join(OBJ, f))
     _write_rtc_headers()
     log: list = []
+    # the stepper objects first: their ptxas resource usage becomes a table the
+    # host code (sdeb_capi.cu) is compiled with
+    steppers = [x for x in SOURCES if x.startswith("sdeb_kuramoto_j")]
+    others = [x for x in SOURCES if x not in steppers]
     with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as pool:
-        objs = list(pool.map(lambda s: _compile(s, log), SOURCES))
+        stepper_objs = list(pool.map(lambda s: _compile(s, log), steppers))
+        _write_kernel_table(stepper_objs)
+        objs = list(pool.map(lambda s: _compile(s, log), others)) + stepper_objs
     cmd = ([nvcc()] + ARCH + ["-shared", "-cudart", "static", "-o", LIB] + objs
            + ["-L", CUDA_LIB, "-lnvrtc", "-Xlinker", "-rpath=" + CUDA_LIB])
     lib_key = _digest(toolchain_id(), cmd, *objs)

@@ -140,7 +140,16 @@ struct Layout {
     int ctas_per_sm = 0;
     int tight = 0;  // register-capped kernel variant (unpadded meanfield, J in {4, 8})
     int J = 0;      // oscillators per lane; 0 = next_pow2(n) / lanes
+    int exact = 1;  // 0: ctas_per_sm estimated from the build's resource table
 };
+
+// Registers / static shared memory of every stepper instantiation (ptxas -v at
+// build time, _build.py): occupancy without loading a kernel module.
+struct KernelRes {
+    short J, solver, stream, coupling, variant, regs;
+    int smem;
+};
+#include "sdeb_kernel_table.inc"
 
 using TuneKey = std::tuple<int, int, int, int, int, int64_t, int, int>;
 
@@ -200,6 +209,10 @@ struct CallScope {
 sdb_status cuda_fail(sdb_ctx* ctx, cudaError_t e, const char* what) {
     return fail_with(ctx, SDB_ERR_CUDA, "%s: %s (%s)", what, cudaGetErrorString(e),
                      cudaGetErrorName(e));
+}
+
+sdb_status cuda_fail_if(sdb_ctx* ctx, cudaError_t e) {
+    return e == cudaSuccess ? SDB_OK : cuda_fail(ctx, e, "autotune scratch");
 }
 
 #define SDB_CUDA(ctx, expr)                                      \
@@ -283,6 +296,33 @@ cudaError_t occupancy_run(int J, int solver, int stream, int coupling, int padde
     }
 }
 
+
+// Resident CTAs per SM of an instantiation from the build's resource table
+// (registers in 256-register warp allocations, static shared memory + 1 KB
+// per CTA of the SM's opt-in maximum, 16 warps... the 32-CTA and 64-warp
+// limits), or -1 when the table has no entry.  An estimate for ordering
+// candidates: a layout that is launched is re-checked with the CUDA
+// occupancy query (finalize_layout), which the persistent grid relies on.
+int table_occupancy(int device, int J, int solver, int stream, int coupling, int variant) {
+    for (int pass = 0; pass < 2; ++pass) {
+        const int want = pass == 0 ? variant : (variant == 2 ? 0 : -1);
+        if (want < 0) break;
+        for (const KernelRes* r = kKernelRes; r->J != 0; ++r) {
+            if (r->J != J || r->solver != solver || r->stream != stream ||
+                r->coupling != coupling || r->variant != want)
+                continue;
+            int sm_smem = 0, regs_sm = 0;
+            cudaDeviceGetAttribute(&sm_smem, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device);
+            cudaDeviceGetAttribute(&regs_sm, cudaDevAttrMaxRegistersPerMultiprocessor, device);
+            const int per_warp = ((int(r->regs) * 32 + 255) / 256) * 256;
+            const int warps = per_warp > 0 ? regs_sm / per_warp : 64;
+            const int by_regs = std::min(warps, 64) / (sdeb::kBlock / 32);
+            const int by_smem = sm_smem / (r->smem + 1024);
+            return std::max(0, std::min({by_regs, by_smem, 32}));
+        }
+    }
+    return -1;
+}
 
 // Kernel kind for a validated descriptor.
 void kernel_kind(const sdb_desc& d, int* solver, int* stream) {
@@ -479,13 +519,20 @@ sdb_status candidate_layouts(sdb_ctx* ctx, const Slot& s, const sdb_desc& d, int
                              (J == 4 || J == 8);
       for (int tight = 0; tight <= (can_tight ? 1 : 0); ++tight) {
         const int padded = kernel_variant(d, L, J, tight);
-        int occ = 0;
-        SDB_CUDA(ctx, occupancy_run(J, kind_solver, kind_stream, d.coupling, padded, 0, &occ));
+        // a kernel whose module this process has not loaded: estimate its
+        // occupancy from the build's resource table rather than loading the
+        // module (~20-40 ms lazily) for a layout the probe may never run
+        int occ = -1;
+        if (!module_loaded(J))
+            occ = table_occupancy(s.device, J, kind_solver, kind_stream, d.coupling, padded);
+        const int exact = occ < 0 ? 1 : 0;
+        if (exact)
+            SDB_CUDA(ctx, occupancy_run(J, kind_solver, kind_stream, d.coupling, padded, 0, &occ));
         if (occ < 1) continue;
         const int64_t ctas = cta_groups(d, L);
-        out->push_back(Layout{L, 0, 0, occ, tight, XJ});
-        if (ctas > int64_t(sms) * occ) out->push_back(Layout{L, 1, 0, occ, tight, XJ});
-        if (tight) continue;
+        out->push_back(Layout{L, 0, 0, occ, tight, XJ, exact});
+        if (ctas > int64_t(sms) * occ) out->push_back(Layout{L, 1, 0, occ, tight, XJ, exact});
+        if (tight || !exact) continue;  // wave-shaping caps need the exact query
         for (int cap = occ - 1; cap >= 1 && cap >= occ - 4; --cap) {
             const double waves_cap = double(ctas) / (double(sms) * cap);
             const double waves_occ = double(ctas) / (double(sms) * occ);
@@ -498,6 +545,25 @@ sdb_status candidate_layouts(sdb_ctx* ctx, const Slot& s, const sdb_desc& d, int
         }
       }
     }
+    return SDB_OK;
+}
+
+// Replace a table-estimated occupancy by the CUDA occupancy query (this loads
+// the kernel, which is about to run): the persistent grid must be exactly the
+// resident CTAs.
+sdb_status finalize_layout(sdb_ctx* ctx, const sdb_desc& d, Layout* lay) {
+    if (lay->exact) return SDB_OK;
+    int kind_solver, kind_stream;
+    kernel_kind(d, &kind_solver, &kind_stream);
+    const int J = lay->J ? lay->J : next_pow2(d.nequat) / lay->lanes;
+    int occ = 0;
+    SDB_CUDA(ctx, occupancy_run(J, kind_solver, kind_stream, d.coupling,
+                                kernel_variant(d, lay->lanes, J, lay->tight), size_t(lay->smem),
+                                &occ));
+    if (occ < 1) return fail_with(ctx, SDB_ERR_CUDA, "layout L=%d J=%d cannot be resident",
+                                  lay->lanes, J);
+    lay->ctas_per_sm = occ;
+    lay->exact = 1;
     return SDB_OK;
 }
 
@@ -733,23 +799,43 @@ sdb_status probe_layouts(sdb_ctx* ctx, Slot& s, const sdb_desc& d, int kind_solv
     int64_t p1 = 32;  // first probe: the cost model's favourite, 32 + 64 steps
     double best_pred = 1e300;
     Layout best = cands[0];
+    // the probe runs every candidate as one resident wave of one CTA per
+    // group, so a persistent layout and its one-CTA-per-group twin measure the
+    // same launch: time it once, predict both (no noise-driven mode flips)
+    std::map<std::tuple<int, int, int, int, int>, double> measured;
     constexpr double kModuleLoadMs = 40.0;  // first launch from a not yet loaded module
     for (size_t ci = 0; ci < cands.size() && rc == SDB_OK; ++ci) {
-        const Layout& lay = cands[ci];
         // a candidate in a module this process has not loaded yet costs its
         // load on top of the probe: only within the budget (never the first)
-        if (ci > 0 && !module_loaded(layout_J(d, lay)) && spent_ms + kModuleLoadMs > budget_ms)
+        if (ci > 0 && !module_loaded(layout_J(d, cands[ci])) && spent_ms + kModuleLoadMs > budget_ms)
             continue;
+        rc = finalize_layout(ctx, d, &cands[ci]);
+        if (rc != SDB_OK) break;
+        const Layout& lay = cands[ci];
         const int64_t rows =
             std::min<int64_t>(d.orbits, int64_t(sms) * lay.ctas_per_sm * (sdeb::kBlock / lay.lanes));
+        if (rows > rows_cap) {  // the exact occupancy exceeded the table's estimate
+            rc = cuda_fail_if(ctx, s.t_values.ensure(size_t(rows) * d.nequat * sizeof(double)));
+            if (rc == SDB_OK) rc = cuda_fail_if(ctx, s.t_fail.ensure(size_t(rows) * sizeof(int64_t)));
+            if (rc != SDB_OK) break;
+        }
         float t1 = 0.f, t2 = 0.f;
-        const double w0 = now_ms();
-        rc = timed(lay, rows, p1, &t1);
-        if (rc != SDB_OK) break;
-        rc = timed(lay, rows, 2 * p1, &t2);
-        if (rc != SDB_OK) break;
-        spent_ms += now_ms() - w0;  // wall time: launches, module loads, syncs
-        const double step_ms = std::max(1e-9, double(t2 - t1) / double(p1));
+        const auto mkey = std::make_tuple(lay.lanes, layout_J(d, lay), lay.tight, lay.smem,
+                                          lay.ctas_per_sm);
+        double step_ms;
+        auto hit = measured.find(mkey);
+        if (hit != measured.end()) {
+            step_ms = hit->second;
+        } else {
+            const double w0 = now_ms();
+            rc = timed(lay, rows, p1, &t1);
+            if (rc != SDB_OK) break;
+            rc = timed(lay, rows, 2 * p1, &t2);
+            if (rc != SDB_OK) break;
+            spent_ms += now_ms() - w0;  // wall time: launches, module loads, syncs
+            step_ms = std::max(1e-9, double(t2 - t1) / double(p1));
+            measured[mkey] = step_ms;
+        }
         const double pred = predict(lay, step_ms, rows);
         if (trace_enabled())
             std::fprintf(stderr, "[sdeb200] tune n=%d L=%d J=%d pers=%d ctas=%d tight=%d: "
@@ -760,7 +846,7 @@ sdb_status probe_layouts(sdb_ctx* ctx, Slot& s, const sdb_desc& d, int kind_solv
             best_pred = pred;
             best = lay;
         }
-        if (budget_ms < 0.0) {
+        if (budget_ms < 0.0 && t2 > 0.f) {
             // 10% of the predicted run for the whole probe (the first
             // candidate's load and probe included); the remaining candidates
             // share what is left (3 p steps each, 2 repetitions)
@@ -837,13 +923,15 @@ sdb_status choose_layout(sdb_ctx* ctx, Slot& s, const sdb_desc& d, const double*
     const std::string dkey = disk_key(s.device, d, kind_solver, kind_stream);
     Layout lay_disk;
     if (disk_lookup(dkey, &lay_disk)) {
-        for (const Layout& c : cands) {  // only a layout this build can still launch
-            if (c.lanes == lay_disk.lanes && c.persistent == lay_disk.persistent &&
-                c.smem == lay_disk.smem && c.ctas_per_sm == lay_disk.ctas_per_sm &&
-                c.tight == lay_disk.tight && c.J == lay_disk.J) {
+        for (const Layout& c : cands) {  // only a shape this build can still launch
+            if (c.lanes == lay_disk.lanes && c.tight == lay_disk.tight && c.J == lay_disk.J) {
+                Layout use = lay_disk;  // incl. a wave-shaping smem cap; occupancy re-queried
+                use.exact = 0;
+                rc = finalize_layout(ctx, d, &use);
+                if (rc != SDB_OK) return rc;
                 std::lock_guard<std::mutex> lock(ctx->mu);
-                ctx->tune[key] = c;
-                *out = c;
+                ctx->tune[key] = use;
+                *out = use;
                 return SDB_OK;
             }
         }
@@ -856,6 +944,8 @@ sdb_status choose_layout(sdb_ctx* ctx, Slot& s, const sdb_desc& d, const double*
         s.tune_us += int64_t(1e3 * (now_ms() - t0));
         if (rc != SDB_OK) return rc;
     }
+    rc = finalize_layout(ctx, d, &best_l);
+    if (rc != SDB_OK) return rc;
     {
         std::lock_guard<std::mutex> lock(ctx->mu);
         ctx->tune[key] = best_l;
@@ -953,25 +1043,28 @@ sdb_status launch_device_ordered(sdb_ctx* ctx, Slot& s, const sdb_desc& d, sdb_m
     Layout lay;
     sdb_status rc = choose_layout(ctx, s, d, d_init, d_params, st, &lay);
     if (rc != SDB_OK) return rc;
-    if (lay.persistent) {
-        SDB_CUDA(ctx, s.state.ensure(size_t(d.orbits) * d.nequat * sizeof(double)));
-        const size_t rw = rng_words(d, d.orbits);
-        if (rw) SDB_CUDA(ctx, s.rng.ensure(rw * sizeof(uint64_t)));
-    }
     int kind_solver, kind_stream;
     kernel_kind(d, &kind_solver, &kind_stream);
     sdeb::RunArgs a = make_args(d, lay.lanes);
     a.state_in = d_init;
     a.params = d_params;
-    // continuation state and stream states are only read back by the next
-    // slab of a persistent grid: a one-pass launch writes neither (2 GB of
-    // HBM writes at cfg3 n=256)
-    a.state_out = lay.persistent ? s.state.as<double>() : nullptr;
     a.values = d_values;
     a.fail_step = d_fail;
-    a.rng_state = lay.persistent ? s.rng.as<uint64_t>() : nullptr;
     rc = configure_layout(ctx, s, s.work, d, lay, d.chunks * d.ksteps, st, &a);
     if (rc != SDB_OK) return rc;
+    // continuation state and stream states are only read back by a later slab
+    // of a persistent grid: a launch whose groups finish in one pass (one CTA
+    // per group, or one slab) writes neither -- 2 GB of HBM writes at cfg3
+    // n=256
+    a.state_out = nullptr;
+    a.rng_state = nullptr;
+    if (a.persistent > 0 && a.slab_steps < d.chunks * d.ksteps) {
+        SDB_CUDA(ctx, s.state.ensure(size_t(d.orbits) * d.nequat * sizeof(double)));
+        const size_t rw = rng_words(d, d.orbits);
+        if (rw) SDB_CUDA(ctx, s.rng.ensure(rw * sizeof(uint64_t)));
+        a.state_out = s.state.as<double>();
+        a.rng_state = s.rng.as<uint64_t>();
+    }
     const int J = layout_J(d, lay);
     int variant = kernel_variant(d, lay.lanes, J, out_mode ? 0 : lay.tight);
     if (out_mode) {

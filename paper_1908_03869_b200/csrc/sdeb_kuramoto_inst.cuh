@@ -38,7 +38,12 @@ template <int J, int S, int R, int C, int P>
 static cudaError_t occupancy_one(size_t smem, int* blocks) {
     constexpr size_t need = own_smem_bytes<J, S, R, C, P>();
     if constexpr (need > 0) smem = smem < need ? need : smem;
-    if (smem + kStaticSmemBytes > smem_optin_bytes()) {  // cannot launch: no resident CTA
+    // the kernel's own static shared memory (tables + scheduling slot) plus the
+    // dynamic request must fit the opt-in limit, else no CTA can be resident
+    cudaFuncAttributes fa{};
+    cudaError_t ea = cudaFuncGetAttributes(&fa, kuramoto_run_kernel<J, S, R, C, P>);
+    if (ea != cudaSuccess) return ea;
+    if (smem + fa.sharedSizeBytes > smem_optin_bytes()) {
         *blocks = 0;
         return cudaSuccess;
     }
