@@ -155,9 +155,13 @@ __device__ __forceinline__ void drift_meanfield(const double (&y)[J], const doub
 template <int J, bool PADDED, class C0>
 __device__ __forceinline__ void meanfield_folded_acc(const double (&y)[J], C0&& c0, double scale,
                                                      int base, int n, int lanes,
-                                                     double (&out)[J]) {
+                                                     double (&out)[J], int big_hint = -1) {
     double sn[J], cs[J], ts[J], tc[J];
-    sincos_vec<J>(y, sn, cs);
+    if (big_hint < 0) {
+        sincos_vec<J>(y, sn, cs);
+    } else {
+        sincos_vec_hint<J>(y, sn, cs, big_hint != 0);
+    }
 #pragma unroll
     for (int q = 0; q < J; ++q) {
         if (PADDED && base + q >= n) {
@@ -178,8 +182,9 @@ __device__ __forceinline__ void meanfield_folded_acc(const double (&y)[J], C0&& 
 template <int J, bool PADDED>
 __device__ __forceinline__ void meanfield_folded(const double (&y)[J], const double (&c0)[J],
                                                  double scale, int base, int n, int lanes,
-                                                 double (&out)[J]) {
-    meanfield_folded_acc<J, PADDED>(y, [&](int q) { return c0[q]; }, scale, base, n, lanes, out);
+                                                 double (&out)[J], int big_hint = -1) {
+    meanfield_folded_acc<J, PADDED>(y, [&](int q) { return c0[q]; }, scale, base, n, lanes, out,
+                                    big_hint);
 }
 
 // PAIRWISE: S_i = sum_{j != i} sin(fl(y_j - y_i)), every term computed as
@@ -581,6 +586,10 @@ __device__ __forceinline__ void run_item(const RunArgs& a, int64_t cg, uint64_t 
         }
         const double dt = a.dt;
         const uint64_t ks = uint64_t(a.ksteps);
+        // meanfield EM: |y| scanned once per step (after the update), shared by
+        // the failure test and the next step's sincos range test
+        constexpr bool kMagScan = SOLVER == KS_EM && kStochastic && COUPLING == KC_MEANFIELD;
+        uint32_t hmax = abs_hi_max<J>(y);
         // Segments between chunk ends: the sample write sits outside the hot
         // inner loop (a branch inside it cost ~40 registers of scheduling).
         uint64_t next_sample = (s0 / ks + 1) * ks;  // exclusive end of s0's chunk
@@ -597,7 +606,8 @@ __device__ __forceinline__ void run_item(const RunArgs& a, int64_t cg, uint64_t 
                     // (K/n)*dt folded into the sums, the noise product unrounded
                     // (a few ulp per step): 4 FP64 ops instead of 10
                     double inc[J];
-                    meanfield_folded<J, PADDED>(y, omdt, kndt, base, n, lanes, inc);
+                    meanfield_folded<J, PADDED>(y, omdt, kndt, base, n, lanes, inc,
+                                                hmax >= 0x41C00000u ? 1 : 0);
                     step_noise_apply<J, STREAM, PADDED>(
                         a, row, orbit_g, step, base, rs, [&](int q, double z) {
                             y[q] = __fma_rn(sgs[q], z, __dadd_rn(y[q], inc[q]));
@@ -647,9 +657,17 @@ __device__ __forceinline__ void run_item(const RunArgs& a, int64_t cg, uint64_t 
             // (engine.py:244-261).  Lanes record independently; the group
             // minimum is the orbit's first failing step.  Padding oscillators
             // stay 0, so no validity predicate is needed.
-            bool bad = false;
+            bool bad;
+            if constexpr (kMagScan) {
+                // one magnitude scan: the finiteness test here and the next
+                // step's sincos range test (hmax)
+                hmax = abs_hi_max<J>(y);
+                bad = hmax >= 0x7ff00000u;
+            } else {
+                bad = false;
 #pragma unroll
-            for (int q = 0; q < J; ++q) bad |= !finite_bits(y[q]);
+                for (int q = 0; q < J; ++q) bad |= !finite_bits(y[q]);
+            }
             // a warp vote keeps the (rare) NaN fill out of the issue stream:
             // as predicated code it cost ~11 slots every step
             if (__any_sync(0xffffffffu, bad)) {
@@ -657,6 +675,7 @@ __device__ __forceinline__ void run_item(const RunArgs& a, int64_t cg, uint64_t 
                     if (fail < 0) fail = int64_t(step);
 #pragma unroll
                     for (int q = 0; q < J; ++q) y[q] = CUDART_NAN;
+                    hmax = 0x7ff80000u;
                 }
             }
             }

@@ -238,6 +238,32 @@ __device__ __forceinline__ void sincos_vec(const double (&x)[J], double (&s)[J],
     }
 }
 
+// sincos_vec with the range test already done by the caller: `big` = some
+// |x[q]| >= 2^29, inf or NaN (the stepper knows it from the magnitude scan it
+// makes for its finiteness check).  Same values element for element.
+template <int J>
+__device__ __forceinline__ void sincos_vec_hint(const double (&x)[J], double (&s)[J], double (&c)[J],
+                                                bool big) {
+#pragma unroll
+    for (int q = 0; q < J; ++q) sincos_small(x[q], s[q], c[q]);
+    if (big) {
+#pragma unroll
+        for (int q = 0; q < J; ++q)
+            if (big_arg(x[q])) sincos(x[q], &s[q], &c[q]);
+    }
+}
+
+// Largest |x[q]| as the high word of its bits (sign cleared): one integer
+// max per element serves both the finiteness test (>= 0x7ff00000) and the
+// sincos range test (>= 0x41C00000, big_arg).
+template <int J>
+__device__ __forceinline__ uint32_t abs_hi_max(const double (&x)[J]) {
+    uint32_t m = 0;
+#pragma unroll
+    for (int q = 0; q < J; ++q) m = max(m, uint32_t(__double2hiint(x[q])) & 0x7fffffffu);
+    return m;
+}
+
 // -2 ln(x) for a positive normal double: the Box-Muller radius argument
 // (rng.py:179, -2.0 * log(u)) with the -2 folded into the table and the
 // series.  x = 2^k z, z near c_i; the table holds (-2 invc_i, -2 logc_i) and
@@ -268,18 +294,21 @@ __device__ __forceinline__ double neg2_log_pos(double x) {
     return __dadd_rn(hi, lo);
 }
 
-// sqrt(x) for x >= 0 (x == 0 -> 0).
+// sqrt(x) for x >= 0 (x == 0 -> 0).  The reciprocal-root seed is taken of
+// max(x, 2^-1022) -- an integer max on the high word, no FP64 compare and
+// selects: x == 0 (the Box-Muller u == 1) then runs the Newton steps with
+// g = 0 and returns exactly 0; any x > 0 (normal) is untouched.
 __device__ __forceinline__ double sqrt_nonneg(double x) {
     double r;
-    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    const double xs = __hiloint2double(max(__double2hiint(x), 0x00100000), __double2loint(x));
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(xs));
     double g = __dmul_rn(x, r);
     double h = __dmul_rn(0.5, r);
     const double d = __fma_rn(-g, h, 0.5);
     g = __fma_rn(g, d, g);
     h = __fma_rn(h, d, h);
     const double e = __fma_rn(-g, g, x);
-    g = __fma_rn(e, h, g);
-    return x > 0.0 ? g : x;
+    return __fma_rn(e, h, g);
 }
 
 }  // namespace sdeb
