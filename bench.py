@@ -798,6 +798,7 @@ def run_cold(args, name, w):
     empty on-disk layout cache (a fresh box)."""
     with tempfile.TemporaryDirectory() as tmp:
         env = dict(os.environ, SDEB200_TUNE_CACHE=os.path.join(tmp, "layouts.json"))
+        env.pop("SDEB200_TUNE", None)  # the default, budgeted search of a first call
         out = subprocess.run([sys.executable, os.path.abspath(__file__), "--cold-probe",
                               "--workload", name, "--gpus", str(args.gpus), "--coupling",
                               args.coupling], capture_output=True, text=True, env=env,
@@ -813,6 +814,13 @@ def run_cold(args, name, w):
 
 
 def run_ours(args, world, rank, local, dist):
+    # the measured process amortises a complete layout search in its warm-up
+    # (SDEB200_TUNE=thorough); the cold_e2e subprocess runs the default,
+    # budgeted search a first call pays
+    os.environ.setdefault("SDEB200_TUNE", "thorough")
+    # and keeps its decisions to itself: no timing depends on ~/.cache
+    os.environ.setdefault("SDEB200_TUNE_CACHE", os.path.join(
+        tempfile.mkdtemp(prefix="sdeb200-bench-"), "layouts.tsv"))
     import torch
 
     from paper_1908_03869_b200 import _native as nat

@@ -804,10 +804,23 @@ sdb_status probe_layouts(sdb_ctx* ctx, Slot& s, const sdb_desc& d, int kind_solv
     // same launch: time it once, predict both (no noise-driven mode flips)
     std::map<std::tuple<int, int, int, int, int>, double> measured;
     constexpr double kModuleLoadMs = 40.0;  // first launch from a not yet loaded module
+    // SDEB200_TUNE=thorough: probe every candidate (module loads and budget
+    // ignored) -- for long-lived processes and benchmarks that amortise a
+    // complete search; SDEB200_TUNE_BUDGET: the probe's fraction of the run
+    static const bool thorough = [] {
+        const char* e = std::getenv("SDEB200_TUNE");
+        return e && std::strcmp(e, "thorough") == 0;
+    }();
+    static const double budget_frac = [] {
+        const char* e = std::getenv("SDEB200_TUNE_BUDGET");
+        const double v = e ? std::atof(e) : 0.1;
+        return v > 0.0 ? v : 0.1;
+    }();
     for (size_t ci = 0; ci < cands.size() && rc == SDB_OK; ++ci) {
         // a candidate in a module this process has not loaded yet costs its
         // load on top of the probe: only within the budget (never the first)
-        if (ci > 0 && !module_loaded(layout_J(d, cands[ci])) && spent_ms + kModuleLoadMs > budget_ms)
+        if (!thorough && ci > 0 && !module_loaded(layout_J(d, cands[ci])) &&
+            spent_ms + kModuleLoadMs > budget_ms)
             continue;
         rc = finalize_layout(ctx, d, &cands[ci]);
         if (rc != SDB_OK) break;
@@ -850,7 +863,7 @@ sdb_status probe_layouts(sdb_ctx* ctx, Slot& s, const sdb_desc& d, int kind_solv
             // 10% of the predicted run for the whole probe (the first
             // candidate's load and probe included); the remaining candidates
             // share what is left (3 p steps each, 2 repetitions)
-            budget_ms = 0.1 * pred;
+            budget_ms = budget_frac * pred;
             const double left = budget_ms - spent_ms;
             const double per_cand = left / double(std::max<size_t>(1, cands.size() - 1));
             const double per_step = double(t2) / double(2 * p1);  // launch overhead included
@@ -863,7 +876,7 @@ sdb_status probe_layouts(sdb_ctx* ctx, Slot& s, const sdb_desc& d, int kind_solv
                 p1 = std::min<int64_t>(p, 2048);
             }
         }
-        if (ci + 1 < cands.size() && spent_ms >= budget_ms) break;
+        if (!thorough && ci + 1 < cands.size() && spent_ms >= budget_ms) break;
     }
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
