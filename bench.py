@@ -700,7 +700,7 @@ def measure(args, name, w, shards, world, dist, clocks, e2e_steps, peak_ops):
             # dropped, as a sweep that consumes each result would
             hashes.append(result_hash(sdb, store, coherence))
             del store
-        return reduce_max_cpu(dist, float(np.mean(per_call))), per_call, hashes
+        return reduce_max(dist, float(np.mean(per_call))), per_call, hashes
 
     # the contract's e2e: inputs from pinned host memory (sdb.pin_batch, filled
     # outside the timed region like the reference bench's batch sampling); the
