@@ -585,3 +585,16 @@ def test_pinned_inputs_take_the_direct_dma_path_bit_identically(monkeypatch):
     a = nat.host_pinned((3, 5))
     a[:] = 7.0
     assert a.sum() == 105.0
+
+
+def test_eight_shards_on_one_gpu_pinned_and_pageable_bit_identical():
+    # the host pipeline of an 8-device run (one host thread per shard, shared
+    # copy pool) exercised on one GPU: the store equals the one-shard run's
+    n, m = 32, 50000
+    batch = sdb.sample_kuramoto_batch(n, m, (0.2, 0.4), (0.01, 0.1), 0.3, seed=33)
+    cfg = EngineConfig(dt=1e-3, tspan=0.05, ksteps=25, orbits=m, seed=6)
+    want = sdb.store_hash(run_batch(sdb.kuramoto_model(n), cfg, batch))
+    eight = dataclasses.replace(cfg, devices=(0,) * 8)
+    assert sdb.store_hash(run_batch(sdb.kuramoto_model(n), eight, batch)) == want
+    assert sdb.store_hash(run_batch(sdb.kuramoto_model(n), eight, sdb.pin_batch(batch))) == want
+    assert last_launch_info((0,) * 8)["launches"] >= 8
