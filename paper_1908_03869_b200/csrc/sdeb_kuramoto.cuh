@@ -98,46 +98,6 @@ __device__ __forceinline__ void group_sum2(double& a, double& b, int lanes) {
     }
 }
 
-// The same canonical sums through shared memory for wide groups: each lane
-// publishes its (a, b), then reads the group's L partials (broadcast loads)
-// and adds them in the adjacent-first tree -- the butterfly's exact
-// association, so the bits are identical -- trading its log2(L) dependent
-// shuffle + add levels (~40 cycles each, the serial part of a step that 2
-// warps per scheduler cannot hide) for one exchange and an L-wide tree.
-// `buf` alternates per step: with one __syncwarp per step a lane cannot
-// overwrite a slot a neighbour is still reading.
-template <int LMAX>
-__device__ __forceinline__ void group_sum2_smem(double& a, double& b, int lanes, int buf) {
-    static_assert(LMAX % 4 == 0, "groups of 4 partials");
-    __shared__ double2 red[2][kBlock];
-    const int tid = int(threadIdx.x);
-    red[buf][tid] = make_double2(a, b);
-    __syncwarp();
-    const double2* g = &red[buf][tid & ~(lanes - 1)];
-    // subtrees of 4 adjacent partials (the canonical tree's first two levels),
-    // loaded just in time, then the upper levels over the subtrees
-    double2 p[LMAX / 4];
-#pragma unroll
-    for (int c = 0; c < LMAX / 4; ++c) {
-        if (4 * c < lanes) {  // warp-uniform; lanes >= 4 is a multiple of 4
-            const double2 v0 = g[4 * c], v1 = g[4 * c + 1], v2 = g[4 * c + 2], v3 = g[4 * c + 3];
-            p[c].x = __dadd_rn(__dadd_rn(v0.x, v1.x), __dadd_rn(v2.x, v3.x));
-            p[c].y = __dadd_rn(__dadd_rn(v0.y, v1.y), __dadd_rn(v2.y, v3.y));
-        }
-    }
-#pragma unroll
-    for (int s = 1; s < LMAX / 4; s <<= 1) {
-        if (4 * s >= lanes) break;  // warp-uniform
-#pragma unroll
-        for (int q = 0; q + s < LMAX / 4; q += 2 * s) {
-            p[q].x = __dadd_rn(p[q].x, p[q + s].x);
-            p[q].y = __dadd_rn(p[q].y, p[q + s].y);
-        }
-    }
-    a = p[0].x;
-    b = p[0].y;
-}
-
 __device__ __forceinline__ int64_t group_fail(int64_t f, int lanes) {
     for (int o = 1; o < lanes; o <<= 1) {
         const long long other = __shfl_xor_sync(0xffffffffu, (long long)f, o);
@@ -195,8 +155,7 @@ __device__ __forceinline__ void drift_meanfield(const double (&y)[J], const doub
 template <int J, bool PADDED, class C0>
 __device__ __forceinline__ void meanfield_folded_acc(const double (&y)[J], C0&& c0, double scale,
                                                      int base, int n, int lanes,
-                                                     double (&out)[J], int big_hint = -1,
-                                                     int smem_buf = -1) {
+                                                     double (&out)[J], int big_hint = -1) {
     double sn[J], cs[J], ts[J], tc[J];
     if (big_hint < 0) {
         sincos_vec<J>(y, sn, cs);
@@ -214,11 +173,7 @@ __device__ __forceinline__ void meanfield_folded_acc(const double (&y)[J], C0&& 
     }
     double a = lane_tree_sum<J>(ts);
     double b = lane_tree_sum<J>(tc);
-    if (smem_buf >= 0 && lanes >= 8 && lanes <= 16) {
-        group_sum2_smem<16>(a, b, lanes, smem_buf);
-    } else {
-        group_sum2(a, b, lanes);
-    }
+    group_sum2(a, b, lanes);
     const double sa = __dmul_rn(scale, a), sb = __dmul_rn(scale, b);
 #pragma unroll
     for (int q = 0; q < J; ++q) out[q] = __fma_rn(cs[q], sa, __fma_rn(-sn[q], sb, c0(q)));
@@ -227,10 +182,9 @@ __device__ __forceinline__ void meanfield_folded_acc(const double (&y)[J], C0&& 
 template <int J, bool PADDED>
 __device__ __forceinline__ void meanfield_folded(const double (&y)[J], const double (&c0)[J],
                                                  double scale, int base, int n, int lanes,
-                                                 double (&out)[J], int big_hint = -1,
-                                                 int smem_buf = -1) {
+                                                 double (&out)[J], int big_hint = -1) {
     meanfield_folded_acc<J, PADDED>(y, [&](int q) { return c0[q]; }, scale, base, n, lanes, out,
-                                    big_hint, smem_buf);
+                                    big_hint);
 }
 
 // PAIRWISE: S_i = sum_{j != i} sin(fl(y_j - y_i)), every term computed as
@@ -635,12 +589,6 @@ __device__ __forceinline__ void run_item(const RunArgs& a, int64_t cg, uint64_t 
         // meanfield EM: |y| scanned once per step (after the update), shared by
         // the failure test and the next step's sincos range test
         constexpr bool kMagScan = SOLVER == KS_EM && kStochastic && COUPLING == KC_MEANFIELD;
-        // coupling sums of groups of >= 8 lanes through shared memory (J = 16:
-        // cfg3 n >= 128); SDEB200 build flag for A/B runs
-#ifndef SDEB_SMEM_SUMS
-#define SDEB_SMEM_SUMS 1
-#endif
-        constexpr bool kSmemSums = SDEB_SMEM_SUMS && J == 16;
         uint32_t hmax = abs_hi_max<J>(y);
         // Segments between chunk ends: the sample write sits outside the hot
         // inner loop (a branch inside it cost ~40 registers of scheduling).
@@ -659,8 +607,7 @@ __device__ __forceinline__ void run_item(const RunArgs& a, int64_t cg, uint64_t 
                     // (a few ulp per step): 4 FP64 ops instead of 10
                     double inc[J];
                     meanfield_folded<J, PADDED>(y, omdt, kndt, base, n, lanes, inc,
-                                                hmax >= 0x41C00000u ? 1 : 0,
-                                                kSmemSums ? int(step & 1) : -1);
+                                                hmax >= 0x41C00000u ? 1 : 0);
                     step_noise_apply<J, STREAM, PADDED>(
                         a, row, orbit_g, step, base, rs, [&](int q, double z) {
                             y[q] = __fma_rn(sgs[q], z, __dadd_rn(y[q], inc[q]));
