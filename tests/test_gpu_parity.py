@@ -598,3 +598,20 @@ def test_eight_shards_on_one_gpu_pinned_and_pageable_bit_identical():
     assert sdb.store_hash(run_batch(sdb.kuramoto_model(n), eight, batch)) == want
     assert sdb.store_hash(run_batch(sdb.kuramoto_model(n), eight, sdb.pin_batch(batch))) == want
     assert last_launch_info((0,) * 8)["launches"] >= 8
+
+
+@pytest.mark.parametrize("stream", ["philox", "sfc64"])
+@pytest.mark.parametrize("n", [256, 200, 128])
+def test_wide_group_layouts_bit_identical(n, stream):
+    # 8-32 lanes per orbit (the cfg3 sizes): the butterfly's canonical tree,
+    # the same bits for every layout, and the oracle's values
+    batch = sdb.sample_kuramoto_batch(n, 300, (0.2, 0.4), (0.01, 0.1), 0.3, seed=n)
+    base = EngineConfig(dt=0.01, tspan=0.5, ksteps=10, orbits=300, seed=12, stream=stream)
+    hashes = {L: sdb.store_hash(run_batch(sdb.kuramoto_model(n),
+                                          dataclasses.replace(base, lanes=L), batch))
+              for L in _lane_options(n)}
+    assert len(set(hashes.values())) == 1, hashes
+    want = O.integrate(batch.init[:4], batch.params[:4], dt=0.01, ksteps=10, chunks=5, seed=12,
+                       stream=stream)[1]
+    store = run_batch(sdb.kuramoto_model(n), base, batch)
+    assert O.mixed_error(store.values[:4], want) <= PARITY_TOL
