@@ -803,6 +803,7 @@ sdb_status probe_layouts(sdb_ctx* ctx, Slot& s, const sdb_desc& d, int kind_solv
     // group, so a persistent layout and its one-CTA-per-group twin measure the
     // same launch: time it once, predict both (no noise-driven mode flips)
     std::map<std::tuple<int, int, int, int, int>, double> measured;
+    std::vector<std::pair<double, size_t>> ranked;  // (predicted ms, candidate) of probed ones
     constexpr double kModuleLoadMs = 40.0;  // first launch from a not yet loaded module
     // SDEB200_TUNE=thorough: probe every candidate (module loads and budget
     // ignored) -- for long-lived processes and benchmarks that amortise a
@@ -877,6 +878,69 @@ sdb_status probe_layouts(sdb_ctx* ctx, Slot& s, const sdb_desc& d, int kind_solv
             }
         }
         if (!thorough && ci + 1 < cands.size() && spent_ms >= budget_ms) break;
+        ranked.emplace_back(pred, ci);
+    }
+    // thorough mode, stage 2: the three best predictions re-timed as they will
+    // really run -- every orbit, the real grid mode and slab size -- on a
+    // differential pair of step counts (the one-wave model misjudged
+    // neighbours by a few percent, e.g. cfg3 n=32 L2 J16 vs L4 J8)
+    if (thorough && rc == SDB_OK && ranked.size() > 1 && d.orbits > rows_cap) {
+        std::sort(ranked.begin(), ranked.end());
+        const int64_t p2 = std::min<int64_t>(total, std::max<int64_t>(32, total / 10));
+        const size_t need_v = size_t(d.orbits) * d.nequat * sizeof(double);
+        rc = cuda_fail_if(ctx, s.t_values.ensure(need_v));
+        if (rc == SDB_OK) rc = cuda_fail_if(ctx, s.t_fail.ensure(size_t(d.orbits) * sizeof(int64_t)));
+        if (rc == SDB_OK) rc = cuda_fail_if(ctx, s.t_state.ensure(need_v));
+        if (rc == SDB_OK)
+            rc = cuda_fail_if(ctx, s.t_rng.ensure(std::max<size_t>(rng_words(d, d.orbits), 4) *
+                                                  sizeof(uint64_t)));
+        double best_full = 1e300;
+        for (size_t r = 0; r < ranked.size() && r < 3 && rc == SDB_OK; ++r) {
+            const Layout& lay = cands[ranked[r].second];
+            float tt[2] = {0.f, 0.f};
+            for (int rep = 0; rep < 2 && rc == SDB_OK; ++rep) {
+                const int64_t steps = rep == 0 ? p2 : 2 * p2;
+                sdeb::RunArgs a = make_args(d, lay.lanes);
+                a.state_in = d_init;
+                a.params = d_params;
+                a.values = s.t_values.as<double>();
+                a.vstride = 1;
+                a.fail_step = s.t_fail.as<int64_t>();
+                a.ksteps = steps;
+                a.chunk_end = 1;
+                rc = configure_layout(ctx, s, s.t_work, d, lay, total, st, &a);
+                if (rc != SDB_OK) break;
+                a.state_out = nullptr;
+                a.rng_state = nullptr;
+                if (a.persistent > 0 && a.slab_steps < steps) {
+                    a.state_out = s.t_state.as<double>();
+                    a.rng_state = s.t_rng.as<uint64_t>();
+                }
+                const int J = layout_J(d, lay);
+                cudaEventRecord(e0, st);
+                cudaError_t e = launch_run(a, J, kind_solver, kind_stream, d.coupling,
+                                           kernel_variant(d, lay.lanes, J, lay.tight), st);
+                cudaEventRecord(e1, st);
+                if (e == cudaSuccess) e = cudaEventSynchronize(e1);
+                if (e != cudaSuccess) {
+                    rc = cuda_fail(ctx, e, "autotune launch");
+                    break;
+                }
+                cudaEventElapsedTime(&tt[rep], e0, e1);
+                s.launches += 1;
+            }
+            if (rc != SDB_OK) break;
+            const double full = double(tt[1] - tt[0]) / double(p2) * double(total);
+            if (trace_enabled())
+                std::fprintf(stderr, "[sdeb200] tune stage 2 L=%d J=%d pers=%d ctas=%d: %.3f ms "
+                                     "predicted from a full-grid run of %lld steps\n",
+                             lay.lanes, layout_J(d, lay), lay.persistent, lay.ctas_per_sm, full,
+                             (long long)p2);
+            if (full < best_full) {
+                best_full = full;
+                best = lay;
+            }
+        }
     }
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
