@@ -944,6 +944,9 @@ sdb_status probe_layouts(sdb_ctx* ctx, Slot& s, const sdb_desc& d, int kind_solv
     }
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
+    // full-grid stage-2 scratch can be GBs (cfg3 n=256: 4 GB): give it back
+    for (DevBuf* b : {&s.t_values, &s.t_state, &s.t_rng, &s.t_fail})
+        if (b->cap > (size_t(256) << 20)) b->release();
     if (rc != SDB_OK) return rc;
     *best_out = best;
     return SDB_OK;
