@@ -836,6 +836,11 @@ sdb_status probe_layouts(sdb_ctx* ctx, Slot& s, const sdb_desc& d, int kind_solv
         float t1 = 0.f, t2 = 0.f;
         const auto mkey = std::make_tuple(lay.lanes, layout_J(d, lay), lay.tight, lay.smem,
                                           lay.ctas_per_sm);
+        // thorough search of a batch smaller than one wave (the probe is the
+        // run itself, latency-bound): longer probes, a few-microsecond step
+        // otherwise drowns in launch noise (cfg1: 1,024 orbits)
+        if (thorough && rows >= d.orbits)
+            p1 = std::max<int64_t>(p1, std::min<int64_t>(total / 10, 2048));
         double step_ms;
         auto hit = measured.find(mkey);
         if (hit != measured.end()) {
