@@ -504,7 +504,8 @@ __device__ __forceinline__ void step_noise_apply(const RunArgs& a, int64_t row, 
 // (analysis.py coherence_series fused into the run): per orbit row a plane of
 // r then a plane of Phi, values[row*2*vstride + {0, vstride} + 1 + c-chunk_begin],
 // sample 0 (the initial state) at offset 0.
-template <int J, int SOLVER, int STREAM, int COUPLING, bool PADDED, bool COH = false>
+template <int J, int SOLVER, int STREAM, int COUPLING, bool PADDED, bool COH = false,
+          bool CSM = false>
 __device__ __forceinline__ void run_item(const RunArgs& a, int64_t cg, uint64_t s0, uint64_t s1,
                                          bool first, double* sh, double* shs) {
     constexpr bool kStochastic = (SOLVER == KS_EM) && (STREAM != KS_NONE);
@@ -534,13 +535,21 @@ __device__ __forceinline__ void run_item(const RunArgs& a, int64_t cg, uint64_t 
         sg[q] = (kStochastic && valid) ? __ldg(prow + 1 + n + i) : 0.0;
     }
 
-    // folded step constants of the meanfield EM form (see the step below)
+    // folded step constants of the meanfield EM form (see the step below).
+    // CSM: kept in this thread's shared-memory column (re-read where a step
+    // uses them; volatile, never hoisted back) instead of 4J registers, which
+    // the sincos / Box-Muller chains of a step can then use for ILP
     double omdt[J], sgs[J];
     const double kndt = __dmul_rn(kn, a.dt);
+    volatile double* cst = sh + threadIdx.x;  // CSM: [2J][kBlock]
 #pragma unroll
     for (int q = 0; q < J; ++q) {
         omdt[q] = __dmul_rn(om[q], a.dt);
         sgs[q] = __dmul_rn(a.sqrt_dt, sg[q]);
+        if constexpr (CSM) {
+            cst[q * kBlock] = omdt[q];
+            cst[(J + q) * kBlock] = sgs[q];
+        }
     }
 
     if constexpr (SOLVER == KS_DRIFT) {
@@ -606,11 +615,13 @@ __device__ __forceinline__ void run_item(const RunArgs& a, int64_t cg, uint64_t 
                     // (K/n)*dt folded into the sums, the noise product unrounded
                     // (a few ulp per step): 4 FP64 ops instead of 10
                     double inc[J];
-                    meanfield_folded<J, PADDED>(y, omdt, kndt, base, n, lanes, inc,
-                                                hmax >= 0x41C00000u ? 1 : 0);
+                    meanfield_folded_acc<J, PADDED>(
+                        y, [&](int q) { return CSM ? cst[q * kBlock] : omdt[q]; }, kndt, base, n,
+                        lanes, inc, hmax >= 0x41C00000u ? 1 : 0);
                     step_noise_apply<J, STREAM, PADDED>(
                         a, row, orbit_g, step, base, rs, [&](int q, double z) {
-                            y[q] = __fma_rn(sgs[q], z, __dadd_rn(y[q], inc[q]));
+                            const double sq = CSM ? cst[(J + q) * kBlock] : sgs[q];
+                            y[q] = __fma_rn(sq, z, __dadd_rn(y[q], inc[q]));
                         });
                 } else if constexpr (kStochastic) {
                     drift<J, COUPLING, PADDED>(y, om, kn, base, n, lanes, sh, shs, f);
@@ -762,9 +773,20 @@ __host__ __device__ constexpr int tight_minb() {
 // Dynamic shared memory a kernel instantiation needs for itself (none: the
 // pairwise tiles live in registers; measured and dropped in r02: step
 // constants in shared memory for J = 16, profiles/r02/experiments.md).
+#ifndef SDEB_CSM16
+#define SDEB_CSM16 1
+#endif
+template <int J, int SOLVER, int STREAM, int COUPLING, int VAR>
+__host__ __device__ constexpr bool uses_const_smem() {
+    return SDEB_CSM16 && J == 16 && (VAR & 1) == 0 && SOLVER == KS_EM && STREAM != KS_NONE &&
+           STREAM != KS_EXPLICIT && COUPLING == KC_MEANFIELD;
+}
+
 template <int J, int SOLVER, int STREAM, int COUPLING, int VAR>
 __host__ __device__ constexpr size_t own_smem_bytes() {
-    return 0;
+    return uses_const_smem<J, SOLVER, STREAM, COUPLING, VAR>()
+               ? size_t(2) * J * kBlock * sizeof(double)
+               : 0;
 }
 
 template <int J, int SOLVER, int STREAM, int COUPLING, int VAR>
@@ -803,7 +825,9 @@ __global__ void __launch_bounds__(kBlock, (VAR == 2 ? tight_minb<J>() : 0))
         if (persistent) __syncthreads();
         const uint64_t s0 = begin + uint64_t(k) * slab;
         const uint64_t s1 = s0 + slab < end ? s0 + slab : end;
-        run_item<J, SOLVER, STREAM, COUPLING, PADDED, COH>(a, cg, s0, s1, k == 0, sh, shs);
+        run_item<J, SOLVER, STREAM, COUPLING, PADDED, COH,
+                 uses_const_smem<J, SOLVER, STREAM, COUPLING, VAR>()>(a, cg, s0, s1, k == 0, sh,
+                                                                      shs);
         if (!persistent) break;
         __threadfence();
         __syncthreads();
