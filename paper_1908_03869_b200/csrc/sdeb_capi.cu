@@ -138,7 +138,7 @@ struct Layout {
     int persistent = 0;
     int smem = 0;
     int ctas_per_sm = 0;
-    int tight = 0;  // register-capped kernel variant (unpadded meanfield, J in {4, 8})
+    int tight = 0;  // VAR 2: register-capped J in {4, 8}, or J = 16 with step constants in smem
     int J = 0;      // oscillators per lane; 0 = next_pow2(n) / lanes
     int exact = 1;  // 0: ctas_per_sm estimated from the build's resource table
 };
@@ -516,7 +516,8 @@ sdb_status candidate_layouts(sdb_ctx* ctx, const Slot& s, const sdb_desc& d, int
       const int L = shape.first, J = shape.second;
       const int XJ = J == P / L ? 0 : J;  // Layout::J (0 = the power-of-two span)
       const bool can_tight = d.nequat == P && d.coupling == SDB_COUPLING_MEANFIELD &&
-                             (J == 4 || J == 8);
+                             (J == 4 || J == 8 || (J == 16 && kind_solver == sdeb::KS_EM &&
+                                                    kind_stream != sdeb::KS_NONE));
       for (int tight = 0; tight <= (can_tight ? 1 : 0); ++tight) {
         const int padded = kernel_variant(d, L, J, tight);
         // a kernel whose module this process has not loaded: estimate its

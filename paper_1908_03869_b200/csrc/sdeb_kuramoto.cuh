@@ -770,6 +770,16 @@ __host__ __device__ constexpr int tight_minb() {
     return J == 4 ? 6 : (J == 8 ? 4 : 1);
 }
 
+// Instantiations with a VAR = 2 form: the register-capped J = 4 / 8 steppers,
+// and the J = 16 meanfield EM stepper with its step constants in shared
+// memory (CSM: 166 registers, 3 CTAs/SM for Philox) -- the autotuner picks
+// between it and the register-resident form per workload (cfg3 n=256 +1.3%,
+// cfg5 -2.8%: profiles/r02/experiments.md).
+template <int J>
+__host__ __device__ constexpr bool has_var2() {
+    return tight_minb<J>() > 1 || J == 16;
+}
+
 // Dynamic shared memory a kernel instantiation needs for itself (none: the
 // pairwise tiles live in registers; measured and dropped in r02: step
 // constants in shared memory for J = 16, profiles/r02/experiments.md).
@@ -778,7 +788,7 @@ __host__ __device__ constexpr int tight_minb() {
 #endif
 template <int J, int SOLVER, int STREAM, int COUPLING, int VAR>
 __host__ __device__ constexpr bool uses_const_smem() {
-    return SDEB_CSM16 && J == 16 && (VAR & 1) == 0 && SOLVER == KS_EM && STREAM != KS_NONE &&
+    return SDEB_CSM16 && J == 16 && VAR == 2 && SOLVER == KS_EM && STREAM != KS_NONE &&
            STREAM != KS_EXPLICIT && COUPLING == KC_MEANFIELD;
 }
 
@@ -790,7 +800,7 @@ __host__ __device__ constexpr size_t own_smem_bytes() {
 }
 
 template <int J, int SOLVER, int STREAM, int COUPLING, int VAR>
-__global__ void __launch_bounds__(kBlock, (VAR == 2 ? tight_minb<J>() : 0))
+__global__ void __launch_bounds__(kBlock, (VAR == 2 && tight_minb<J>() > 1 ? tight_minb<J>() : 0))
     kuramoto_run_kernel(const RunArgs a) {
     constexpr bool PADDED = (VAR & 1) != 0;
     constexpr bool COH = VAR >= kVarCoherence;

@@ -64,14 +64,14 @@ static cudaError_t occupancy_one(size_t smem, int* blocks) {
 // variants exist where tight_minb<J>() > 1 (meanfield only).
 template <int J, class Op>
 static cudaError_t dispatch(int solver, int stream, int coupling, int variant, Op&& op) {
-    if (variant == 2 && tight_minb<J>() == 1) variant = 0;
+    if (variant == 2 && !has_var2<J>()) variant = 0;
 #define SDEB_PICK(S, R)                                                          \
     switch (variant) {                                                           \
         case 0: return op.template run<J, S, R, KC_MEANFIELD, 0>();              \
         case 1: return op.template run<J, S, R, KC_MEANFIELD, 1>();              \
         case 4: return op.template run<J, S, R, KC_MEANFIELD, 4>();              \
         case 5: return op.template run<J, S, R, KC_MEANFIELD, 5>();              \
-        default: return op.template run<J, S, R, KC_MEANFIELD, (tight_minb<J>() > 1 ? 2 : 0)>(); \
+        default: return op.template run<J, S, R, KC_MEANFIELD, (has_var2<J>() ? 2 : 0)>(); \
     }
 #define SDEB_PAIR(S, R)                                                          \
     switch (variant) {                                                           \
