@@ -521,11 +521,19 @@ def dist_setup(want_gpus: int):
             raise SystemExit("--gpus %d but torchrun started %d ranks" % (want_gpus, world))
         import torch
         import torch.distributed as dist_mod
+        # SDEB200_BENCH_ONE_GPU=1 (tests only): every rank on GPU 0 over gloo,
+        # to exercise the multi-rank bench path on a one-GPU box
+        one_gpu = os.environ.get("SDEB200_BENCH_ONE_GPU") == "1"
+        if one_gpu:
+            local = 0
         # this rank's device is the default context's too (batch sampling,
         # per-step utilities): nothing lands on GPU 0 by accident
         os.environ["SDEB200_DEVICES"] = str(local)
         torch.cuda.set_device(local)
-        dist_mod.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if one_gpu:
+            dist_mod.init_process_group("gloo")
+        else:
+            dist_mod.init_process_group("nccl", device_id=torch.device("cuda", local))
         dist = dist_mod
     return world, rank, local, dist
 
@@ -534,6 +542,8 @@ def reduce_max(dist, value: float) -> float:
     if dist is None:
         return value
     import torch
+    if dist.get_backend() == "gloo":
+        return reduce_max_cpu(dist, value)
     t = torch.tensor([value], dtype=torch.float64, device="cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
