@@ -1875,8 +1875,17 @@ sdb_status sdb_open(const int* devices, int ndevices, sdb_ctx** out) {
         if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking);
         if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&s.h2d, cudaStreamNonBlocking);
         if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&s.d2h, cudaStreamNonBlocking);
+        // the pinned staging slots belong to the context: open them at a
+        // starting size (the process's first page-locked allocation alone costs
+        // ~45 ms on the B200 host); runs that move more grow them on demand
+        const size_t slot0 = size_t(std::max(0, env_int("SDEB200_SLOT0_MB", 8))) << 20;
+        for (int k = 0; k < kPinSlots && e == cudaSuccess && slot0 > 0; ++k) {
+            e = s.pin_in[k].ensure(slot0);
+            if (e == cudaSuccess) e = s.pin_out[k].ensure(slot0);
+        }
         if (e != cudaSuccess) {
-            delete ctx;
+            for (PinBuf* b : {&s.pin_in[0], &s.pin_in[1], &s.pin_out[0], &s.pin_out[1]}) b->release();
+            sdb_close(ctx);
             return cuda_fail(nullptr, e, "sdb_open");
         }
         ctx->slots.push_back(s);
