@@ -111,6 +111,7 @@ struct Slot {
     cudaEvent_t ev_in = nullptr;
     std::vector<cudaEvent_t> ev_tile;  // end of each tile's kernel
     PinBuf pin_in[kPinSlots], pin_out[kPinSlots];
+    PinBuf pin_warm;  // one small page-locked block opened with the context
     DevBuf init, params, values, state, fail, rng;
     DevBuf t_values, t_state, t_fail, t_rng, t_work;  // autotune scratch
     DevBuf work;  // persistent mode: item counter + per-group slab counters
@@ -655,14 +656,21 @@ std::string disk_cache_path() {
 // Key of one tuning decision: the device and software it was measured on
 // (name, SM count, driver, this build) and the launch shape.
 std::string disk_key(int device, const sdb_desc& d, int kind_solver, int kind_stream) {
-    cudaDeviceProp prop{};
-    cudaGetDeviceProperties(&prop, device);
-    int driver = 0;
+    // attribute queries, not cudaGetDeviceProperties (which costs tens of ms
+    // on this driver -- a cold call would pay it): compute capability, SM
+    // count, memory and clock identify the GPU model well enough for a cache
+    int sms = 0, major = 0, minor = 0, clock = 0, driver = 0;
+    size_t free_b = 0, total_b = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device);
+    cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, device);
+    cudaDeviceGetAttribute(&clock, cudaDevAttrClockRate, device);
+    cudaMemGetInfo(&free_b, &total_b);
     cudaDriverGetVersion(&driver);
     const int64_t total = d.chunks * d.ksteps;
     char buf[512];
-    std::snprintf(buf, sizeof(buf), "%s|sm%d|cc%d.%d|drv%d|abi%d|%s %s|n%d|s%d|r%d|c%d|L%d|M%lld|T%lld",
-                  prop.name, prop.multiProcessorCount, prop.major, prop.minor, driver,
+    std::snprintf(buf, sizeof(buf), "mem%lluGB-clk%d|sm%d|cc%d.%d|drv%d|abi%d|%s %s|n%d|s%d|r%d|c%d|L%d|M%lld|T%lld",
+                  (unsigned long long)(total_b >> 30), clock, sms, major, minor, driver,
                   SDB_ABI_VERSION, __DATE__, __TIME__, d.nequat, kind_solver, kind_stream,
                   d.coupling, d.lanes, (long long)d.orbits,
                   (long long)std::min<int64_t>(total, int64_t(1) << 20));
@@ -1003,10 +1011,15 @@ sdb_status choose_layout(sdb_ctx* ctx, Slot& s, const sdb_desc& d, const double*
         }
     }
     std::vector<Layout> cands;
+    const double tc0 = trace_enabled() ? now_ms() : 0.0;
     sdb_status rc = candidate_layouts(ctx, s, d, kind_solver, kind_stream, &cands);
     if (rc != SDB_OK) return rc;
     if (cands.empty()) return fail_with(ctx, SDB_ERR_CUDA, "no launchable layout for n=%d", d.nequat);
+    const double tc1 = trace_enabled() ? now_ms() : 0.0;
     const std::string dkey = disk_key(s.device, d, kind_solver, kind_stream);
+    if (trace_enabled())
+        std::fprintf(stderr, "[sdeb200] layout search: %zu candidates in %.3f ms, cache key in "
+                             "%.3f ms\n", cands.size(), tc1 - tc0, now_ms() - tc1);
     Layout lay_disk;
     if (disk_lookup(dkey, &lay_disk)) {
         for (const Layout& c : cands) {  // only a shape this build can still launch
@@ -1875,16 +1888,14 @@ sdb_status sdb_open(const int* devices, int ndevices, sdb_ctx** out) {
         if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking);
         if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&s.h2d, cudaStreamNonBlocking);
         if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&s.d2h, cudaStreamNonBlocking);
-        // the pinned staging slots belong to the context: open them at a
-        // starting size (the process's first page-locked allocation alone costs
-        // ~45 ms on the B200 host); runs that move more grow them on demand
-        const size_t slot0 = size_t(std::max(0, env_int("SDEB200_SLOT0_MB", 8))) << 20;
-        for (int k = 0; k < kPinSlots && e == cudaSuccess && slot0 > 0; ++k) {
-            e = s.pin_in[k].ensure(slot0);
-            if (e == cudaSuccess) e = s.pin_out[k].ensure(slot0);
-        }
+        // the process's first page-locked allocation carries a fixed setup
+        // cost (tens of ms on the B200 host): pay it with the context, one
+        // small block; the staging slots are sized by the first run that uses
+        // them (growing a slot later frees the old block, which synchronises)
+        if (e == cudaSuccess && env_int("SDEB200_PIN_WARM", 1) != 0)
+            e = s.pin_warm.ensure(1);
         if (e != cudaSuccess) {
-            for (PinBuf* b : {&s.pin_in[0], &s.pin_in[1], &s.pin_out[0], &s.pin_out[1]}) b->release();
+            s.pin_warm.release();
             sdb_close(ctx);
             return cuda_fail(nullptr, e, "sdb_open");
         }
@@ -1901,7 +1912,8 @@ void sdb_close(sdb_ctx* ctx) {
         for (DevBuf* b : {&s.init, &s.params, &s.values, &s.state, &s.fail, &s.rng, &s.work, &s.scratch,
                           &s.t_values, &s.t_state, &s.t_fail, &s.t_rng, &s.t_work})
             b->release();
-        for (PinBuf* b : {&s.pin_in[0], &s.pin_in[1], &s.pin_out[0], &s.pin_out[1]}) b->release();
+        for (PinBuf* b : {&s.pin_in[0], &s.pin_in[1], &s.pin_out[0], &s.pin_out[1], &s.pin_warm})
+            b->release();
         if (s.ev_in) cudaEventDestroy(s.ev_in);
         if (s.done) cudaEventDestroy(s.done);
         for (cudaEvent_t e : s.ev_tile) cudaEventDestroy(e);
