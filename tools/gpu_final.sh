@@ -9,7 +9,7 @@ mkdir -p $O
 nvidia-smi > $O/nvidia-smi.txt 2>&1; lscpu > $O/lscpu.txt 2>&1; free -g > $O/free.txt 2>&1
 timeout 300 python -c "import __graft_entry__ as g; g.build(); g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?" >> $O/status.txt
 timeout 1800 python -m pytest tests -m gpu -q --tb=short --timeout 900 > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $O/status.txt
-T0=$(date +%s.%N); timeout 1200 python bench.py > $O/bench_default.log 2>&1; echo "bench rc=$? wall_s=$(echo "$(date +%s.%N) - $T0" | bc)" >> $O/status.txt
+T0=$(date +%s); timeout 1200 python bench.py > $O/bench_default.log 2>&1; echo "bench rc=$? wall_s=$(( $(date +%s) - T0 ))" >> $O/status.txt
 timeout 900 python bench.py --impl reference --steps 5 --warmup 3 > $O/bench_reference.log 2>&1; echo "bench ref rc=$?" >> $O/status.txt
 for wl in cfg1 cfg4 cfg5 cfg5_coherence paper_n5 paper_n10 paper_n15 cfg2_codegen ou_codegen; do
   timeout 400 python bench.py --workload $wl --no-cpu-baseline --steps 3 > $O/bench_$wl.log 2>&1; echo "bench $wl rc=$?" >> $O/status.txt
