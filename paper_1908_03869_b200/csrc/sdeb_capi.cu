@@ -861,7 +861,10 @@ sdb_status probe_layouts(sdb_ctx* ctx, Slot& s, const sdb_desc& d, int kind_solv
             rc = timed(lay, rows, 2 * p1, &t2);
             if (rc != SDB_OK) break;
             spent_ms += now_ms() - w0;  // wall time: launches, module loads, syncs
-            step_ms = std::max(1e-9, double(t2 - t1) / double(p1));
+            // differential step time; if timing noise swallowed the difference,
+            // the plain average of the longer probe (launch overhead included)
+            step_ms = t2 > t1 ? double(t2 - t1) / double(p1) : double(t2) / double(2 * p1);
+            step_ms = std::max(1e-9, step_ms);
             measured[mkey] = step_ms;
         }
         const double pred = predict(lay, step_ms, rows);
@@ -944,7 +947,8 @@ sdb_status probe_layouts(sdb_ctx* ctx, Slot& s, const sdb_desc& d, int kind_solv
                 s.launches += 1;
             }
             if (rc != SDB_OK) break;
-            const double full = double(tt[1] - tt[0]) / double(p2) * double(total);
+            const double full = (tt[1] > tt[0] ? double(tt[1] - tt[0]) / double(p2)
+                                               : double(tt[1]) / double(2 * p2)) * double(total);
             if (trace_enabled())
                 std::fprintf(stderr, "[sdeb200] tune stage 2 L=%d J=%d pers=%d ctas=%d: %.3f ms "
                                      "predicted from a full-grid run of %lld steps\n",
