@@ -223,3 +223,25 @@ def test_run_batch_to_file_checks_indices_before_touching_the_file(tmp_path):
         storage.run_batch_to_file(bad, cfg, OrbitBatch(init=np.zeros((2, 2)),
                                                        params=np.zeros((2, 1))), path)
     assert path.read_bytes() == b"existing store"
+
+
+def test_kernel_resource_table_from_ptxas(tmp_path, monkeypatch):
+    # the build turns ptxas -v output into the occupancy table the layout
+    # autotuner reads instead of loading kernel modules (_build.py)
+    from paper_1908_03869_b200 import _build
+    obj = tmp_path / "k.o"
+    (tmp_path / "k.o.ptxas").write_text(
+        "ptxas info    : Compiling entry function "
+        "'_ZN4sdeb19kuramoto_run_kernelILi16ELi0ELi0ELi0ELi2EEEvNS_7RunArgsE' for 'sm_100a'\n"
+        "ptxas info    : Function properties for x\n"
+        "    0 bytes stack frame, 0 bytes spill stores, 0 bytes spill loads\n"
+        "ptxas info    : Used 166 registers, used 1 barriers, 24592 bytes smem, 1024 bytes cmem\n")
+    out = tmp_path / "table.inc"
+    monkeypatch.setattr(_build, "KERNEL_TABLE", str(out))
+    _build._write_kernel_table([str(obj)])
+    text = out.read_text()
+    assert "{16, 0, 0, 0, 2, 166, 24592}," in text and text.rstrip().endswith("};")
+    # the real table of this build covers every lane width's default kernel
+    real = open(os.path.join(os.path.dirname(_build.LIB), "_obj", "sdeb_kernel_table.inc")).read()
+    for J in (1, 2, 4, 8, 16, 3, 5, 15):
+        assert "{%d, 0, 0, 0, 0, " % J in real, J
