@@ -601,7 +601,8 @@ __device__ __forceinline__ void run_item(const RunArgs& a, int64_t cg, uint64_t 
         uint32_t hmax = abs_hi_max<J>(y);
         // Segments between chunk ends: the sample write sits outside the hot
         // inner loop (a branch inside it cost ~40 registers of scheduling).
-        uint64_t next_sample = (s0 / ks + 1) * ks;  // exclusive end of s0's chunk
+        uint64_t chunk = s0 / ks;                // the chunk s0 lies in (one division per item)
+        uint64_t next_sample = (chunk + 1) * ks;  // exclusive end of s0's chunk
         uint64_t step = s0;
         while (step < s1) {
           const uint64_t seg_end = next_sample < s1 ? next_sample : s1;
@@ -698,7 +699,7 @@ __device__ __forceinline__ void run_item(const RunArgs& a, int64_t cg, uint64_t 
 #pragma unroll
                     for (int q = 0; q < J; ++q) y[q] = CUDART_NAN;
                 }
-                const int64_t c = int64_t(step / ks) - 1;
+                const int64_t c = int64_t(chunk++);  // == step / ks - 1, without a 64-bit division
                 if constexpr (COH) {
                     double r, phi;
                     group_order_param<J, PADDED>(y, base, n, lanes, r, phi);
@@ -709,9 +710,21 @@ __device__ __forceinline__ void run_item(const RunArgs& a, int64_t cg, uint64_t 
                     }
                 } else if (active) {
                     double* out = a.values + (row * a.vstride + (c - a.chunk_begin)) * n + base;
+                    bool stored = false;
+                    if constexpr (!PADDED && J % 2 == 0) {
+                        // unpadded rows: the lane's J doubles as 16-byte stores
+                        if ((reinterpret_cast<uintptr_t>(out) & 15) == 0) {
 #pragma unroll
-                    for (int q = 0; q < J; ++q)
-                        if (base + q < n) out[q] = y[q];
+                            for (int q = 0; q < J; q += 2)
+                                *reinterpret_cast<double2*>(out + q) = make_double2(y[q], y[q + 1]);
+                            stored = true;
+                        }
+                    }
+                    if (!stored) {
+#pragma unroll
+                        for (int q = 0; q < J; ++q)
+                            if (base + q < n) out[q] = y[q];
+                    }
                 }
             }
         }
