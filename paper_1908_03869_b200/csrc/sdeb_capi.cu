@@ -915,8 +915,10 @@ sdb_status probe_layouts(sdb_ctx* ctx, Slot& s, const sdb_desc& d, int kind_solv
         for (size_t r = 0; r < ranked.size() && r < 3 && rc == SDB_OK; ++r) {
             const Layout& lay = cands[ranked[r].second];
             float tt[2] = {0.f, 0.f};
-            for (int rep = 0; rep < 2 && rc == SDB_OK; ++rep) {
-                const int64_t steps = rep == 0 ? p2 : 2 * p2;
+            tt[0] = tt[1] = 1e30f;
+            // (p2, 2 p2, p2, 2 p2): the best of two launches per length
+            for (int rep = 0; rep < 4 && rc == SDB_OK; ++rep) {
+                const int64_t steps = (rep & 1) == 0 ? p2 : 2 * p2;
                 sdeb::RunArgs a = make_args(d, lay.lanes);
                 a.state_in = d_init;
                 a.params = d_params;
@@ -943,7 +945,9 @@ sdb_status probe_layouts(sdb_ctx* ctx, Slot& s, const sdb_desc& d, int kind_solv
                     rc = cuda_fail(ctx, e, "autotune launch");
                     break;
                 }
-                cudaEventElapsedTime(&tt[rep], e0, e1);
+                float ms = 0.f;
+                cudaEventElapsedTime(&ms, e0, e1);
+                tt[rep & 1] = std::min(tt[rep & 1], ms);
                 s.launches += 1;
             }
             if (rc != SDB_OK) break;
