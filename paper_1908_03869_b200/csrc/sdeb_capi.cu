@@ -325,45 +325,6 @@ int table_occupancy(int device, int J, int solver, int stream, int coupling, int
     return -1;
 }
 
-// Kernel-module preload: the first launch from each lane-width module costs
-// its lazy load (4-45 ms each on B200, tools/module_load_probe.py).  The first
-// context of a process starts one background thread that touches the default
-// kernel of every module (an occupancy query loads it) while the caller is
-// still preparing its batch, so a first run_batch rarely pays a load.
-// SDEB200_PRELOAD=0 turns it off; the thread is joined at exit.
-std::once_flag g_preload_once;
-std::thread* g_preload_thread = nullptr;
-
-void preload_join() {
-    if (g_preload_thread) {
-        g_preload_thread->join();
-        delete g_preload_thread;
-        g_preload_thread = nullptr;
-    }
-}
-
-int env_int(const char* name, int dflt);
-
-void start_preload(int device) {
-    if (env_int("SDEB200_PRELOAD", 1) == 0) return;
-    std::call_once(g_preload_once, [device] {
-        g_preload_thread = new std::thread([device] {
-            if (cudaSetDevice(device) != cudaSuccess) return;
-            // the cfg3 / cfg2 widths first, then the paper's exact widths
-            const int widths[] = {16, 8, 4, 2, 1, 15, 10, 5, 3, 6, 7, 9, 11, 12, 13, 14};
-            for (int J : widths) {
-                int occ = 0;
-                if (occupancy_run(J, sdeb::KS_EM, sdeb::KS_PHILOX, SDB_COUPLING_MEANFIELD, 0, 0,
-                                  &occ) == cudaSuccess)
-                    g_loaded_j.fetch_or(1u << J);
-                else
-                    cudaGetLastError();
-            }
-        });
-        std::atexit(preload_join);
-    });
-}
-
 // Kernel kind for a validated descriptor.
 void kernel_kind(const sdb_desc& d, int* solver, int* stream) {
     if (d.solver == SDB_SOLVER_RK4) {
@@ -1948,7 +1909,6 @@ sdb_status sdb_open(const int* devices, int ndevices, sdb_ctx** out) {
         }
         ctx->slots.push_back(s);
     }
-    start_preload(ctx->slots[0].device);
     *out = ctx;
     return SDB_OK;
 }
