@@ -911,6 +911,11 @@ sdb_status probe_layouts(sdb_ctx* ctx, Slot& s, const sdb_desc& d, int kind_solv
         if (rc == SDB_OK)
             rc = cuda_fail_if(ctx, s.t_rng.ensure(std::max<size_t>(rng_words(d, d.orbits), 4) *
                                                   sizeof(uint64_t)));
+        // runs predicted to take <= 300 ms are timed at their own length (best
+        // of two): the differential form drops per-launch costs that differ
+        // between layouts (cfg3 n=256: the shared-constant J=16 layout won the
+        // differential and ran 2.6 % slower, profiles/r02/p2u)
+        const bool direct = ranked.front().first <= 300.0;
         double best_full = 1e300;
         for (size_t r = 0; r < ranked.size() && r < 3 && rc == SDB_OK; ++r) {
             const Layout& lay = cands[ranked[r].second];
@@ -918,7 +923,8 @@ sdb_status probe_layouts(sdb_ctx* ctx, Slot& s, const sdb_desc& d, int kind_solv
             tt[0] = tt[1] = 1e30f;
             // (p2, 2 p2, p2, 2 p2): the best of two launches per length
             for (int rep = 0; rep < 4 && rc == SDB_OK; ++rep) {
-                const int64_t steps = (rep & 1) == 0 ? p2 : 2 * p2;
+                if (direct && (rep & 1)) continue;
+                const int64_t steps = direct ? total : (rep & 1) == 0 ? p2 : 2 * p2;
                 sdeb::RunArgs a = make_args(d, lay.lanes);
                 a.state_in = d_init;
                 a.params = d_params;
@@ -951,13 +957,14 @@ sdb_status probe_layouts(sdb_ctx* ctx, Slot& s, const sdb_desc& d, int kind_solv
                 s.launches += 1;
             }
             if (rc != SDB_OK) break;
-            const double full = (tt[1] > tt[0] ? double(tt[1] - tt[0]) / double(p2)
-                                               : double(tt[1]) / double(2 * p2)) * double(total);
+            const double full = direct ? double(tt[0])
+                                : (tt[1] > tt[0] ? double(tt[1] - tt[0]) / double(p2)
+                                                 : double(tt[1]) / double(2 * p2)) * double(total);
             if (trace_enabled())
                 std::fprintf(stderr, "[sdeb200] tune stage 2 L=%d J=%d pers=%d ctas=%d: %.3f ms "
                                      "predicted from a full-grid run of %lld steps\n",
                              lay.lanes, layout_J(d, lay), lay.persistent, lay.ctas_per_sm, full,
-                             (long long)p2);
+                             (long long)(direct ? total : p2));
             if (full < best_full) {
                 best_full = full;
                 best = lay;
